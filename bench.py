@@ -1,0 +1,365 @@
+"""Benchmark: pi(A)v throughput on the 4M-row 3D Laplacian (BASELINE config 3).
+
+One "step" = one application of the preconditioner pi(A) (degree 50 GMRES
+polynomial + pof stability copies, Leja order, built on the device from the
+seeded start vector) to a device-resident vector: eff_degree fused SpMV-factor
+launches over the 424 MB CSR matrix.  `value` is the north-star byte model
+(eff_degree x [12 nnz + 4(n+1) + 16 n]) per second, whole job.  `e2e` is the
+same metric through the C-ABI with pinned host buffers (H2D of v and D2H of
+pi(A)v inside the timed region).  Extra keys report the CGS2 sweep bandwidth
+and the solver's time to nev converged eigenpairs.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Multi-GPU: the path does not exchange data on one GPU's workload (north star:
+one GPU), so N ranks run N independent replicas ("replicas only", weak
+scaling); timing is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "pi(A)v GB/s (north-star byte model), config 3 3D Laplacian 160^3"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                util = float(p[6])
+                if util > 0:
+                    sm.append(float(p[0]))
+                mx = float(p[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(gpus):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def load_golden_poly():
+    with open(os.path.join(ROOT, "tests", "golden", "c3_poly.json")) as f:
+        g = json.load(f)
+    return np.array(g["roots"]["re"]) + 1j * np.array(g["roots"]["im"])
+
+
+def count_launches(roots):
+    launches = 0
+    i = 0
+    r = list(roots)
+    while i < len(r):
+        if abs(r[i].imag) > 1e-13 * abs(r[i]):
+            launches += 2
+            i += 2
+        else:
+            launches += 1
+            i += 1
+    return launches
+
+
+# --------------------------------------------------------------- reference --
+def run_reference(args):
+    ws, rank, _ = dist_setup(args.gpus)
+    if rank != 0:
+        return
+    from oracle import oracle as O
+
+    threads = os.cpu_count() or 1
+    O.set_threads(threads)
+    csr = O.Csr.config(3)
+    n, nnz, _ = csr.info()
+    A = O.csr_operator(csr)
+    roots = load_golden_poly()
+    bspmv = 12.0 * nnz + 4.0 * (n + 1) + 16.0 * n
+    # size the per-step sample: ~3 s of CPU work
+    t1 = O.time_poly_factors(A, roots, 1, 1)
+    nf = int(max(1, min(len(roots), 3.0 / max(t1, 1e-3))))
+    for _ in range(args.warmup):
+        O.time_poly_factors(A, roots, nf, 1)
+    times = [O.time_poly_factors(A, roots, nf, 1) for _ in range(args.steps)]
+    t = float(np.mean(times))
+    gbs = nf * bspmv / t / 1e9
+    line = {
+        "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, BASELINE config 3)", "impl": "reference",
+        "config": {"workload": "config3-laplace3d-160^3-pi(A)v", "n": n, "nnz": nnz,
+                   "eff_degree": len(roots), "sample_factors": nf},
+        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": f"{nf} of {len(roots)} polynomial factors (SpMV+axpy) per step, "
+                                   "oracle restatement of src/gmres_poly.cpp:117-147, OpenMP rows"},
+        "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# -------------------------------------------------------------------- b200 --
+def cpu_baseline_port(roots):
+    """Single-thread oracle (the reference's single-threaded contract)."""
+    from oracle import oracle as O
+
+    O.set_threads(1)
+    csr = O.Csr.config(3)
+    n, nnz, _ = csr.info()
+    A = O.csr_operator(csr)
+    bspmv = 12.0 * nnz + 4.0 * (n + 1) + 16.0 * n
+    t1 = O.time_poly_factors(A, roots, 1, 1)
+    nf = int(max(1, min(len(roots), 10.0 / max(t1, 1e-3))))
+    t = O.time_poly_factors(A, roots, nf, 1)
+    return {"value": round(nf * bspmv / t / 1e9, 3), "unit": "GB/s", "cores": 1, "kind": "port",
+            "sample": f"{nf} of {len(roots)} factors of pi(A)v on config 3 "
+                      f"({t:.1f} s, single thread, oracle -O3)"}
+
+
+def run_b200(args):
+    import torch
+
+    ws, rank, local = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1806_08020_b200 as ppa
+
+    stream = torch.cuda.current_stream()
+    ppa.set_stream(stream)
+    t0 = time.time()
+    csr = ppa.CsrMatrix.config(3)
+    n, nnz, _ = csr.info()
+    A = ppa.make_csr_operator(csr)
+    bspmv = A.model_bytes()
+    b = torch.tensor(ppa.normal_vector(n, 2, ppa.STREAM_POLY), device="cuda")
+    base, _ = ppa.build_gmres_poly(A, b, 50)
+    roots = ppa.add_stability_roots(base, len(base))
+    setup_s = time.time() - t0
+    launches = count_launches(roots)
+    step_bytes = len(roots) * bspmv
+
+    v = torch.tensor(ppa.normal_vector(n, 2, ppa.STREAM_ARNOLDI), device="cuda")
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+
+    def step():
+        ppa.apply_poly(roots, A, v, out)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    with ClockSampler(local) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    ms_step = ms / args.steps
+    value = ws * step_bytes / (ms_step * 1e-3) / 1e9
+    avg_launch_ms = ms_step / launches
+    achieved = bspmv / (avg_launch_ms * 1e-3) / 1e9
+    peak, peak_kind = hbm_peak()
+
+    # e2e: pinned host buffers through the C-ABI (H2D + pi(A)v + D2H per step)
+    op = ppa.make_poly_operator(A, roots, len(base))
+    xh = torch.tensor(ppa.normal_vector(n, 2, ppa.STREAM_ARNOLDI)).pin_memory()
+    yh = torch.empty(n, dtype=torch.float64).pin_memory()
+    import ctypes
+
+    L = ppa.lib()
+    rec = ppa.CostRecord()
+
+    def e2e_step():
+        st = L.ppa_op_apply_host(op._h, ctypes.c_void_p(xh.data_ptr()),
+                                 ctypes.c_void_p(yh.data_ptr()), ctypes.byref(rec))
+        if st:
+            raise RuntimeError(L.ppa_last_error().decode())
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    ke = max(1, args.steps)
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(ke):
+        e2e_step()
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1) / ke
+    if ws > 1:
+        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_val = ws * step_bytes / (e2e_ms * 1e-3) / 1e9
+    e2e_match = bool(np.array_equal(yh.numpy(), out.cpu().numpy()))
+
+    # CGS2 sweep bandwidth at basis size c = 40 (config 3's m)
+    c = 40
+    ld = (n + 31) // 32 * 32
+    V = torch.randn((c + 1) * ld, dtype=torch.float64, device="cuda")
+    w = torch.randn(n, dtype=torch.float64, device="cuda")
+    Hc = torch.empty(c + 2, dtype=torch.float64, device="cuda")
+    flag = torch.zeros(2, dtype=torch.int32, device="cuda")
+    for _ in range(3):
+        ppa.cgs2_step(V, ld, n, c, w, Hc, flag)
+    g0 = torch.cuda.Event(enable_timing=True)
+    g1 = torch.cuda.Event(enable_timing=True)
+    reps = 10
+    g0.record(stream)
+    for _ in range(reps):
+        ppa.cgs2_step(V, ld, n, c, w, Hc, flag)
+    g1.record(stream)
+    torch.cuda.synchronize()
+    cgs_ms = g0.elapsed_time(g1) / reps
+    cgs_gbs = 8.0 * n * (3 * c + 7) / (cgs_ms * 1e-3) / 1e9
+    del V, w
+
+    # time to nev converged eigenpairs (config 3, matrix already on device)
+    solve_info = None
+    if not args.no_solve:
+        cfg = ppa.config_solve_config(3)
+        r = ppa.solve(A, cfg)
+        lam = np.sort(r["eigenvalues"].real)
+        solve_info = {"seconds": round(r["timing"]["total"], 4), "converged": r["converged"],
+                      "cycles": r["cycles"], "mvps": r["cost"]["mvps"], "dots": r["cost"]["dots"],
+                      "eff_degree": r["composite_degree"], "smallest": round(float(lam[0]), 6),
+                      "timing": {k: round(v, 4) for k, v in r["timing"].items()}}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_port(roots)
+
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "spmv_traffic.json")
+    if os.path.exists(tfile):
+        with open(tfile) as f:
+            traffic = json.load(f).get("traffic_bytes_per_launch")
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator; BASELINE config 3)",
+            "config": {"workload": "config3-laplace3d-160^3-pi(A)v", "n": n, "nnz": nnz,
+                       "eff_degree": len(roots), "base_degree": len(base),
+                       "spmv_launches_per_step": launches, "parallelism": f"replicas{ws}",
+                       "l2": "inputs larger than L2 (424 MB matrix stream per SpMV vs 126 MB L2)"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": traffic, "kernel": "k_spmv_rowblock (fused factor)",
+                         "algorithmic_bytes_per_launch": bspmv},
+            "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
+                    "d2h_bytes_per_step": 8 * n, "ms_per_step": round(e2e_ms, 4),
+                    "matches_device_result": e2e_match},
+            "gpu_launches": launches * args.steps,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "cgs2": {"c": c, "gbs_model": round(cgs_gbs, 2), "ms": round(cgs_ms, 4),
+                     "frac": round(cgs_gbs / peak, 4), "bytes_model": "8n(3c+7)"},
+            "time_to_nev": solve_info,
+            "setup_seconds": round(setup_s, 3),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-solve", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

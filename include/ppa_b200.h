@@ -1,0 +1,206 @@
+/*
+ * ppa_b200.h - C-ABI of the B200-native polynomial-preconditioned Arnoldi
+ * hot path (libppa_b200.so).
+ *
+ * The reference (arxiv/paper_1806_08020, /root/reference/proj) is a C++/Eigen
+ * library with no foreign-function layer; these entry points are what a
+ * binding to its hot path would expose.  Each one names the reference
+ * interface it replaces (file:line under /root/reference/proj).
+ *
+ * Conventions
+ *  - Every function returns a status (PPA_OK = 0); on failure
+ *    ppa_last_error() returns the thread-local message, worded as the
+ *    reference's exception text.  No C++ exception crosses the ABI.
+ *      PPA_INVALID_ARGUMENT  <- std::invalid_argument
+ *      PPA_RUNTIME_ERROR     <- std::runtime_error
+ *      PPA_LOGIC_ERROR       <- std::logic_error (malformed root list)
+ *      PPA_CUDA_ERROR        <- CUDA failure
+ *  - "_dev" pointers are device pointers (HBM); everything else is host.
+ *  - Kernels run on the calling thread's stream (ppa_set_stream; default
+ *    stream otherwise).  Calls that return host results synchronise it.
+ *  - ppa_cost mirrors CostRecord (inc/cost.hpp:17-23); calls add the
+ *    reference's counter increments to *cost (may be NULL).
+ */
+#ifndef PPA_B200_H
+#define PPA_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  PPA_OK = 0,
+  PPA_INVALID_ARGUMENT = 1,
+  PPA_RUNTIME_ERROR = 2,
+  PPA_LOGIC_ERROR = 3,
+  PPA_CUDA_ERROR = 4,
+  PPA_INTERNAL_ERROR = 5
+};
+
+/* OperatorKind (inc/operators.hpp:43) */
+enum { PPA_KIND_CSR = 0, PPA_KIND_DIAGONAL = 1, PPA_KIND_SHIFTED = 2, PPA_KIND_BLOCK2 = 3,
+       PPA_KIND_POLY = 4, PPA_KIND_COMPOSITE = 5 };
+/* RitzOrdering (inc/arnoldi.hpp:40) */
+enum { PPA_SMALLEST_MAGNITUDE = 0, PPA_LARGEST_MAGNITUDE = 1, PPA_TARGET_ONE = 2 };
+
+typedef struct ppa_cost {
+  long long mvps;
+  long long dots;
+  long long vops;
+  double nnzr;
+  double wall_seconds;
+} ppa_cost;
+
+typedef struct ppa_host_csr ppa_host_csr; /* CsrMatrix (inc/operators.hpp:15-33) */
+typedef struct ppa_op ppa_op;             /* OperatorPtr (inc/operators.hpp:78) */
+typedef struct ppa_arnoldi ppa_arnoldi;   /* ArnoldiState (inc/arnoldi.hpp:18-26) */
+
+const char* ppa_last_error(void);
+int ppa_abi_version(void);
+int ppa_device_info(int* sm_count, double* l2_bytes);
+int ppa_set_stream(void* cuda_stream);
+int ppa_synchronize(void);
+
+/* ---- host CSR and generators ------------------------------------------ */
+/* CsrMatrix + validate() (src/operators.cpp:12-37) */
+int ppa_host_csr_create(int n, long long nnz, const int* row_ptr, const int* col_idx,
+                        const double* values, ppa_host_csr** out);
+/* CsrMatrix::from_triplets (src/operators.cpp:50-78) */
+int ppa_host_csr_from_triplets(int n, long long count, const int* rows, const int* cols,
+                               const double* vals, ppa_host_csr** out);
+/* make_convection_diffusion (src/operators.cpp:190-244) */
+int ppa_gen_convdiff_ref(int grid_n, ppa_host_csr** out);
+/* BASELINE.json configs 1..5 and their parametric generators */
+int ppa_gen_config(int config, ppa_host_csr** out);
+int ppa_gen_bidiagonal(int n, ppa_host_csr** out);
+int ppa_gen_convdiff_const(int grid_n, double peclet, ppa_host_csr** out);
+int ppa_gen_laplacian_3d(int grid_n, ppa_host_csr** out);
+int ppa_gen_random_poisson(int n, double lambda, unsigned long long seed, ppa_host_csr** out);
+int ppa_host_csr_info(const ppa_host_csr* m, int* n, long long* nnz,
+                      unsigned long long* fingerprint);
+int ppa_host_csr_arrays(const ppa_host_csr* m, const int** row_ptr, const int** col_idx,
+                        const double** values);
+void ppa_host_csr_free(ppa_host_csr* m);
+/* Seeded N(0,1) vector (host), stream ids as in DESIGN.md */
+int ppa_normal_vector(long long n, unsigned long long seed, unsigned long long stream,
+                      double* out);
+
+/* ---- operators --------------------------------------------------------- */
+/* make_csr_operator (inc/operators.hpp:83): validates, uploads to HBM */
+int ppa_csr_operator(const ppa_host_csr* m, ppa_op** out);
+/* make_diagonal (inc/operators.hpp:81) */
+int ppa_diagonal_operator(int n, const double* diag, ppa_op** out);
+/* make_poly_operator / make_poly_complement_operator (inc/gmres_poly.hpp:91,95) */
+int ppa_poly_operator(const ppa_op* base, const double* re, const double* im, int nroots,
+                      int base_degree, int complement, ppa_op** out);
+void ppa_op_free(ppa_op* op);
+/* dim(), mvps_per_apply(), nnzr(), kind() (inc/operators.hpp:53-68) */
+int ppa_op_info(const ppa_op* op, int* dim, int* mvps_per_apply, double* nnzr, int* kind);
+/* LinearOperator::apply (inc/operators.hpp:58-59), device vectors */
+int ppa_op_apply(const ppa_op* op, const double* x_dev, double* y_dev, ppa_cost* cost);
+/* Same with host vectors: H2D of x, apply, D2H of y (the end-to-end call) */
+int ppa_op_apply_host(const ppa_op* op, const double* x, double* y, ppa_cost* cost);
+/* CSR operators: bytes of one SpMV under the north-star byte model */
+int ppa_csr_model_bytes(const ppa_op* op, double* bytes, long long* nnz);
+
+/* ---- polynomial -------------------------------------------------------- */
+/* apply_poly (src/gmres_poly.cpp:117-147): out_dev = pi(A) v_dev */
+int ppa_apply_poly(const double* re, const double* im, int nroots, const ppa_op* a,
+                   const double* v_dev, double* out_dev, ppa_cost* cost);
+/* build_gmres_poly (src/gmres_poly.cpp:95-115); re/im capacity >= degree */
+int ppa_build_gmres_poly(const ppa_op* a, const double* b_dev, int degree, double* re,
+                         double* im, int* nroots, int* truncated, ppa_cost* cost);
+/* leja_order (src/gmres_poly.cpp:38-93) */
+int ppa_leja_order(const double* re, const double* im, int n, double* out_re, double* out_im);
+/* compute_pof (src/gmres_poly.cpp:155-179); arrays sized >= n */
+int ppa_compute_pof(const double* re, const double* im, int n, double* log10_pof, int* copies,
+                    int* ndistinct, double* max_log10_pof, int* total_copies);
+/* add_stability_roots (src/gmres_poly.cpp:181-226); out capacity `cap` */
+int ppa_add_stability_roots(const double* re, const double* im, int n, int base_degree,
+                            int max_copies_per_root, int cap, double* out_re, double* out_im,
+                            int* out_n);
+/* eval_poly (src/gmres_poly.cpp:149-153) */
+int ppa_eval_poly(const double* re, const double* im, int n, double z_re, double z_im,
+                  double* out_re, double* out_im);
+
+/* ---- Arnoldi ----------------------------------------------------------- */
+/* arnoldi_init (src/arnoldi.cpp:99-113) */
+int ppa_arnoldi_init(const double* v0_dev, int n, int m, ppa_cost* cost, ppa_arnoldi** out);
+/* arnoldi_extend (src/arnoldi.cpp:115-152), CGS2 on device */
+int ppa_arnoldi_extend(ppa_arnoldi* st, const ppa_op* op, int to_dim, ppa_cost* cost);
+int ppa_arnoldi_info(const ppa_arnoldi* st, int* cur_dim, int* max_dim, int* breakdown,
+                     long long* ld, double** V_dev);
+/* H, (m+1) x m column-major */
+int ppa_arnoldi_get_H(const ppa_arnoldi* st, double* H);
+/* ritz_pairs (src/arnoldi.cpp:154-176): cur_dim values + residual estimates */
+int ppa_arnoldi_ritz(const ppa_arnoldi* st, int ordering, double* re, double* im, double* resid);
+/* harmonic_ritz_values (src/arnoldi.cpp:178-206) */
+int ppa_arnoldi_harmonic(const ppa_arnoldi* st, double* re, double* im);
+/* ritz_vector (src/arnoldi.cpp:252-265): unit vector j into y_re/y_im (device, n each;
+   y_im untouched and *is_complex = 0 for a real pair) */
+int ppa_arnoldi_ritz_vector(const ppa_arnoldi* st, int ordering, int j, double* y_re_dev,
+                            double* y_im_dev, int* is_complex, ppa_cost* cost);
+/* thick_restart with ritz_pairs(ordering) as keep set (src/arnoldi.cpp:267-334) */
+int ppa_arnoldi_restart(ppa_arnoldi* st, int ordering, int k, ppa_cost* cost, int* kk);
+void ppa_arnoldi_free(ppa_arnoldi* st);
+
+/* ---- raw device kernels -------------------------------------------------- */
+/* y = A x with a CSR operator (src/operators.cpp:39-48) */
+int ppa_spmv(const ppa_op* a, const double* x_dev, double* y_dev);
+/* One CGS2 step (replaces MGS2 of src/arnoldi.cpp:129-150); Hcol_dev c+1, flag_dev int */
+int ppa_cgs2_step(double* V_dev, long long ld, int n, int c, double* w_dev, double* Hcol_dev,
+                  int* flag_dev);
+/* Out = V[:,0:d] G (G d x p col-major, device); in place allowed for p <= d
+   (src/arnoldi.cpp:258, 309) */
+int ppa_ts_combine(const double* V_dev, long long ldv, int n, int d, const double* G_dev, int p,
+                   double* Out_dev, long long ldo);
+
+/* ---- solver ------------------------------------------------------------ */
+/* SolveConfig (inc/solver.hpp:21-58) */
+typedef struct ppa_solve_config {
+  int m, k, nev, degree;
+  double rtol_multiplier;
+  double rtol_absolute;      /* <= 0: unset */
+  int variant;               /* 0 ritz, 1 harmonic */
+  int stability;             /* 0 off, 1 pof_auto */
+  int double_d1, double_d2;  /* solve_double stages when use_double */
+  int use_double;
+  int max_cycles;
+  unsigned long long seed;
+  int allow_nev_above_k;
+} ppa_solve_config;
+
+/* EigResult (inc/solver.hpp:71-89); arrays supplied by the caller */
+typedef struct ppa_solve_result {
+  /* capacities (in) */
+  int cap_nev, cap_roots, cap_cycles;
+  /* per wanted pair */
+  double* eig_re;
+  double* eig_im;
+  double* residuals;
+  int* converged_flags;
+  /* polynomial(s) in effect */
+  double* poly_re;
+  double* poly_im;
+  double* inner_re;
+  double* inner_im;
+  /* per-cycle max residual */
+  double* cycle_max_residual;
+  /* scalars (out) */
+  int n_eig, n_poly, n_inner, n_cycles;
+  int converged, cycles, composite_degree, poly_base_degree;
+  double rtol, max_err, norm_estimate;
+  ppa_cost cost;
+  double t_total, t_setup, t_extend, t_check, t_restart;
+} ppa_solve_result;
+
+/* solve (inc/solver.hpp:94) or solve_double (inc/solver.hpp:111) */
+int ppa_solve(const ppa_op* a, const ppa_solve_config* cfg, ppa_solve_result* res);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PPA_B200_H */

@@ -1,0 +1,596 @@
+"""ctypes bindings of libppa_b200.so (include/ppa_b200.h).
+
+Names follow the reference's API (proj/include/ppa/*.hpp); C status codes
+map back onto the reference's exception types:
+    PPA_INVALID_ARGUMENT -> ValueError   (std::invalid_argument)
+    PPA_RUNTIME_ERROR    -> RuntimeError (std::runtime_error)
+    PPA_LOGIC_ERROR      -> LogicError   (std::logic_error)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libppa_b200.so")
+
+STREAM_NORM, STREAM_POLY, STREAM_ARNOLDI, STREAM_POLY2, STREAM_MATRIX = 1, 2, 3, 4, 5
+SMALLEST_MAGNITUDE, LARGEST_MAGNITUDE, TARGET_ONE = 0, 1, 2
+KINDS = ["csr", "diagonal", "shifted", "block2", "poly", "composite"]
+
+
+class PPAError(RuntimeError):
+    pass
+
+
+class LogicError(RuntimeError):
+    """std::logic_error (e.g. a complex root without adjacent conjugate)."""
+
+
+class CostRecord(C.Structure):
+    """inc/cost.hpp:17-23"""
+
+    _fields_ = [("mvps", C.c_longlong), ("dots", C.c_longlong), ("vops", C.c_longlong),
+                ("nnzr", C.c_double), ("wall_seconds", C.c_double)]
+
+    def as_dict(self):
+        return {"mvps": self.mvps, "dots": self.dots, "vops": self.vops, "nnzr": self.nnzr}
+
+    def __repr__(self):
+        return f"CostRecord(mvps={self.mvps}, dots={self.dots}, vops={self.vops}, nnzr={self.nnzr})"
+
+
+class _SolveConfigC(C.Structure):
+    _fields_ = [("m", C.c_int), ("k", C.c_int), ("nev", C.c_int), ("degree", C.c_int),
+                ("rtol_multiplier", C.c_double), ("rtol_absolute", C.c_double),
+                ("variant", C.c_int), ("stability", C.c_int), ("double_d1", C.c_int),
+                ("double_d2", C.c_int), ("use_double", C.c_int), ("max_cycles", C.c_int),
+                ("seed", C.c_ulonglong), ("allow_nev_above_k", C.c_int)]
+
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+
+
+class _SolveResultC(C.Structure):
+    _fields_ = [("cap_nev", C.c_int), ("cap_roots", C.c_int), ("cap_cycles", C.c_int),
+                ("eig_re", _dp), ("eig_im", _dp), ("residuals", _dp), ("converged_flags", _ip),
+                ("poly_re", _dp), ("poly_im", _dp), ("inner_re", _dp), ("inner_im", _dp),
+                ("cycle_max_residual", _dp),
+                ("n_eig", C.c_int), ("n_poly", C.c_int), ("n_inner", C.c_int),
+                ("n_cycles", C.c_int), ("converged", C.c_int), ("cycles", C.c_int),
+                ("composite_degree", C.c_int), ("poly_base_degree", C.c_int),
+                ("rtol", C.c_double), ("max_err", C.c_double), ("norm_estimate", C.c_double),
+                ("cost", CostRecord),
+                ("t_total", C.c_double), ("t_setup", C.c_double), ("t_extend", C.c_double),
+                ("t_check", C.c_double), ("t_restart", C.c_double)]
+
+
+_lib = None
+
+
+def lib():
+    """The loaded C-ABI library; raises if it was not built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError(f"{_LIB_PATH} missing: run __graft_entry__.build() "
+                              "(there is no CPU fallback for the CUDA path)")
+        L = C.CDLL(_LIB_PATH)
+        vp = C.c_void_p
+        L.ppa_last_error.restype = C.c_char_p
+        sigs = {
+            "ppa_abi_version": [],
+            "ppa_device_info": [_ip, _dp],
+            "ppa_set_stream": [vp],
+            "ppa_synchronize": [],
+            "ppa_host_csr_create": [C.c_int, C.c_longlong, vp, vp, vp, C.POINTER(vp)],
+            "ppa_host_csr_from_triplets": [C.c_int, C.c_longlong, vp, vp, vp, C.POINTER(vp)],
+            "ppa_gen_convdiff_ref": [C.c_int, C.POINTER(vp)],
+            "ppa_gen_config": [C.c_int, C.POINTER(vp)],
+            "ppa_gen_bidiagonal": [C.c_int, C.POINTER(vp)],
+            "ppa_gen_convdiff_const": [C.c_int, C.c_double, C.POINTER(vp)],
+            "ppa_gen_laplacian_3d": [C.c_int, C.POINTER(vp)],
+            "ppa_gen_random_poisson": [C.c_int, C.c_double, C.c_ulonglong, C.POINTER(vp)],
+            "ppa_host_csr_info": [vp, _ip, C.POINTER(C.c_longlong), C.POINTER(C.c_ulonglong)],
+            "ppa_host_csr_arrays": [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)],
+            "ppa_normal_vector": [C.c_longlong, C.c_ulonglong, C.c_ulonglong, vp],
+            "ppa_csr_operator": [vp, C.POINTER(vp)],
+            "ppa_diagonal_operator": [C.c_int, vp, C.POINTER(vp)],
+            "ppa_poly_operator": [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.POINTER(vp)],
+            "ppa_op_info": [vp, _ip, _ip, _dp, _ip],
+            "ppa_op_apply": [vp, vp, vp, C.POINTER(CostRecord)],
+            "ppa_op_apply_host": [vp, vp, vp, C.POINTER(CostRecord)],
+            "ppa_csr_model_bytes": [vp, _dp, C.POINTER(C.c_longlong)],
+            "ppa_apply_poly": [vp, vp, C.c_int, vp, vp, vp, C.POINTER(CostRecord)],
+            "ppa_build_gmres_poly": [vp, vp, C.c_int, vp, vp, _ip, _ip, C.POINTER(CostRecord)],
+            "ppa_leja_order": [vp, vp, C.c_int, vp, vp],
+            "ppa_compute_pof": [vp, vp, C.c_int, vp, vp, _ip, _dp, _ip],
+            "ppa_add_stability_roots": [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, _ip],
+            "ppa_eval_poly": [vp, vp, C.c_int, C.c_double, C.c_double, _dp, _dp],
+            "ppa_arnoldi_init": [vp, C.c_int, C.c_int, C.POINTER(CostRecord), C.POINTER(vp)],
+            "ppa_arnoldi_extend": [vp, vp, C.c_int, C.POINTER(CostRecord)],
+            "ppa_arnoldi_info": [vp, _ip, _ip, _ip, C.POINTER(C.c_longlong), C.POINTER(vp)],
+            "ppa_arnoldi_get_H": [vp, vp],
+            "ppa_arnoldi_ritz": [vp, C.c_int, vp, vp, vp],
+            "ppa_arnoldi_harmonic": [vp, vp, vp],
+            "ppa_arnoldi_ritz_vector": [vp, C.c_int, C.c_int, vp, vp, _ip, C.POINTER(CostRecord)],
+            "ppa_arnoldi_restart": [vp, C.c_int, C.c_int, C.POINTER(CostRecord), _ip],
+            "ppa_spmv": [vp, vp, vp],
+            "ppa_cgs2_step": [vp, C.c_longlong, C.c_int, C.c_int, vp, vp, vp],
+            "ppa_ts_combine": [vp, C.c_longlong, C.c_int, C.c_int, vp, C.c_int, vp, C.c_longlong],
+            "ppa_solve": [vp, C.POINTER(_SolveConfigC), C.POINTER(_SolveResultC)],
+        }
+        for name, args in sigs.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = C.c_int
+        for name in ("ppa_host_csr_free", "ppa_op_free", "ppa_arnoldi_free"):
+            f = getattr(L, name)
+            f.argtypes = [vp]
+            f.restype = None
+        _lib = L
+    return _lib
+
+
+def _check(status: int) -> None:
+    if status == 0:
+        return
+    msg = lib().ppa_last_error().decode()
+    if status == 1:
+        raise ValueError(msg)
+    if status == 3:
+        raise LogicError(msg)
+    if status == 2:
+        raise RuntimeError(msg)
+    raise PPAError(f"[status {status}] {msg}")
+
+
+def _ptr(x) -> int:
+    """Device pointer of a torch tensor (or a raw int)."""
+    if x is None:
+        return 0
+    if isinstance(x, int):
+        return x
+    return int(x.data_ptr())
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _np_ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _roots(roots) -> tuple[np.ndarray, np.ndarray]:
+    r = np.asarray(roots, dtype=np.complex128).ravel()
+    return _f64(r.real), _f64(r.imag)
+
+
+def set_stream(stream) -> None:
+    """Launch subsequent kernels of this thread on `stream` (torch.cuda.Stream or handle)."""
+    h = getattr(stream, "cuda_stream", stream)
+    _check(lib().ppa_set_stream(C.c_void_p(int(h) if h else 0)))
+
+
+def synchronize() -> None:
+    _check(lib().ppa_synchronize())
+
+
+# --------------------------------------------------------------------- CSR --
+class CsrMatrix:
+    """Host CSR matrix (inc/operators.hpp:15-33), validated on construction."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.ppa_host_csr_free(self._h)
+            self._h = None
+
+    @classmethod
+    def from_arrays(cls, n, row_ptr, col_idx, values):
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int32)
+        ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+        v = _f64(values)
+        h = C.c_void_p()
+        _check(lib().ppa_host_csr_create(n, len(v), _np_ptr(rp), _np_ptr(ci), _np_ptr(v), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_triplets(cls, n, rows, cols, vals):
+        r = np.ascontiguousarray(rows, dtype=np.int32)
+        c = np.ascontiguousarray(cols, dtype=np.int32)
+        v = _f64(vals)
+        h = C.c_void_p()
+        _check(lib().ppa_host_csr_from_triplets(n, len(v), _np_ptr(r), _np_ptr(c), _np_ptr(v),
+                                                C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def _gen(cls, fn, *args):
+        h = C.c_void_p()
+        _check(fn(*args, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def config(cls, k: int):
+        return cls._gen(lib().ppa_gen_config, k)
+
+    @classmethod
+    def convection_diffusion(cls, grid_n: int):
+        """make_convection_diffusion (src/operators.cpp:190-244)."""
+        return cls._gen(lib().ppa_gen_convdiff_ref, grid_n)
+
+    @classmethod
+    def convection_diffusion_const(cls, grid_n: int, peclet: float = 0.5):
+        return cls._gen(lib().ppa_gen_convdiff_const, grid_n, C.c_double(peclet))
+
+    @classmethod
+    def laplacian_3d(cls, grid_n: int):
+        return cls._gen(lib().ppa_gen_laplacian_3d, grid_n)
+
+    @classmethod
+    def bidiagonal(cls, n: int):
+        return cls._gen(lib().ppa_gen_bidiagonal, n)
+
+    @classmethod
+    def random_poisson(cls, n: int, lam: float = 16.0, seed: int = 4):
+        return cls._gen(lib().ppa_gen_random_poisson, n, C.c_double(lam), C.c_ulonglong(seed))
+
+    def info(self):
+        n = C.c_int()
+        nnz = C.c_longlong()
+        fp = C.c_ulonglong()
+        _check(lib().ppa_host_csr_info(self._h, C.byref(n), C.byref(nnz), C.byref(fp)))
+        return n.value, nnz.value, fp.value
+
+    @property
+    def n(self):
+        return self.info()[0]
+
+    @property
+    def nnz(self):
+        return self.info()[1]
+
+    def fingerprint(self) -> int:
+        return self.info()[2]
+
+    def arrays(self):
+        """Copies of (row_ptr, col_idx, values)."""
+        n, nnz, _ = self.info()
+        rp, ci, v = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _check(lib().ppa_host_csr_arrays(self._h, C.byref(rp), C.byref(ci), C.byref(v)))
+        a = np.ctypeslib.as_array(C.cast(rp, C.POINTER(C.c_int)), (n + 1,)).copy()
+        b = np.ctypeslib.as_array(C.cast(ci, C.POINTER(C.c_int)), (max(nnz, 1),))[:nnz].copy()
+        c = np.ctypeslib.as_array(C.cast(v, C.POINTER(C.c_double)), (max(nnz, 1),))[:nnz].copy()
+        return a, b, c
+
+
+def normal_vector(n: int, seed: int, stream: int) -> np.ndarray:
+    out = np.empty(n, dtype=np.float64)
+    _check(lib().ppa_normal_vector(n, seed, stream, _np_ptr(out)))
+    return out
+
+
+# --------------------------------------------------------------- operators --
+class LinearOperator:
+    """OperatorPtr (inc/operators.hpp:49-78); vectors are device pointers."""
+
+    def __init__(self, handle, keep=()):
+        self._h = handle
+        self._keep = keep  # base operators must outlive wrappers
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.ppa_op_free(self._h)
+            self._h = None
+
+    def _info(self):
+        d, mv, k = C.c_int(), C.c_int(), C.c_int()
+        nz = C.c_double()
+        _check(lib().ppa_op_info(self._h, C.byref(d), C.byref(mv), C.byref(nz), C.byref(k)))
+        return d.value, mv.value, nz.value, KINDS[k.value]
+
+    def dim(self):
+        return self._info()[0]
+
+    def mvps_per_apply(self):
+        return self._info()[1]
+
+    def nnzr(self):
+        return self._info()[2]
+
+    def kind(self):
+        return self._info()[3]
+
+    def apply(self, x, y, rec: Optional[CostRecord] = None):
+        rec = rec if rec is not None else CostRecord()
+        _check(lib().ppa_op_apply(self._h, _ptr(x), _ptr(y), C.byref(rec)))
+        return rec
+
+    def apply_host(self, x: np.ndarray, rec: Optional[CostRecord] = None) -> np.ndarray:
+        x = _f64(x)
+        y = np.empty_like(x)
+        rec = rec if rec is not None else CostRecord()
+        _check(lib().ppa_op_apply_host(self._h, _np_ptr(x), _np_ptr(y), C.byref(rec)))
+        return y
+
+    def model_bytes(self):
+        b = C.c_double()
+        nnz = C.c_longlong()
+        _check(lib().ppa_csr_model_bytes(self._h, C.byref(b), C.byref(nnz)))
+        return b.value
+
+
+def make_csr_operator(m: CsrMatrix) -> LinearOperator:
+    h = C.c_void_p()
+    _check(lib().ppa_csr_operator(m._h, C.byref(h)))
+    return LinearOperator(h)
+
+
+def make_diagonal(diag) -> LinearOperator:
+    d = _f64(diag)
+    h = C.c_void_p()
+    _check(lib().ppa_diagonal_operator(len(d), _np_ptr(d), C.byref(h)))
+    return LinearOperator(h)
+
+
+def _poly_op(a: LinearOperator, roots, base_degree, complement):
+    re, im = _roots(roots)
+    h = C.c_void_p()
+    _check(lib().ppa_poly_operator(a._h, _np_ptr(re), _np_ptr(im), len(re), int(base_degree or 0),
+                                   int(complement), C.byref(h)))
+    return LinearOperator(h, keep=(a,))
+
+
+def make_poly_operator(a: LinearOperator, roots, base_degree=None) -> LinearOperator:
+    return _poly_op(a, roots, base_degree, False)
+
+
+def make_poly_complement_operator(a: LinearOperator, roots, base_degree=None) -> LinearOperator:
+    return _poly_op(a, roots, base_degree, True)
+
+
+def spmv(a: LinearOperator, x, y) -> None:
+    _check(lib().ppa_spmv(a._h, _ptr(x), _ptr(y)))
+
+
+# -------------------------------------------------------------- polynomial --
+def apply_poly(roots, a: LinearOperator, v, out, rec: Optional[CostRecord] = None):
+    re, im = _roots(roots)
+    rec = rec if rec is not None else CostRecord()
+    _check(lib().ppa_apply_poly(_np_ptr(re), _np_ptr(im), len(re), a._h, _ptr(v), _ptr(out),
+                                C.byref(rec)))
+    return rec
+
+
+def build_gmres_poly(a: LinearOperator, b, degree: int, rec: Optional[CostRecord] = None):
+    """Returns (roots complex128 in Leja order, truncated)."""
+    re = np.zeros(max(degree, 1))
+    im = np.zeros(max(degree, 1))
+    nr, tr = C.c_int(), C.c_int()
+    rec = rec if rec is not None else CostRecord()
+    _check(lib().ppa_build_gmres_poly(a._h, _ptr(b), degree, _np_ptr(re), _np_ptr(im),
+                                      C.byref(nr), C.byref(tr), C.byref(rec)))
+    return re[:nr.value] + 1j * im[:nr.value], bool(tr.value)
+
+
+def leja_order(roots) -> np.ndarray:
+    re, im = _roots(roots)
+    ore, oim = np.zeros_like(re), np.zeros_like(im)
+    _check(lib().ppa_leja_order(_np_ptr(re), _np_ptr(im), len(re), _np_ptr(ore), _np_ptr(oim)))
+    return ore + 1j * oim
+
+
+def compute_pof(roots):
+    """Returns dict(log10_pof, copies_needed, max_log10_pof, total_copies)."""
+    re, im = _roots(roots)
+    n = len(re)
+    lg = np.zeros(max(n, 1))
+    cp = np.zeros(max(n, 1), dtype=np.int32)
+    nd, tot = C.c_int(), C.c_int()
+    mx = C.c_double()
+    _check(lib().ppa_compute_pof(_np_ptr(re), _np_ptr(im), n, _np_ptr(lg), _np_ptr(cp),
+                                 C.byref(nd), C.byref(mx), C.byref(tot)))
+    return {"log10_pof": lg[:nd.value], "copies_needed": cp[:nd.value],
+            "max_log10_pof": mx.value, "total_copies": tot.value}
+
+
+def add_stability_roots(roots, base_degree=None, max_copies_per_root=1 << 20) -> np.ndarray:
+    re, im = _roots(roots)
+    cap = 8 * len(re) + 64
+    ore, oim = np.zeros(cap), np.zeros(cap)
+    on = C.c_int()
+    _check(lib().ppa_add_stability_roots(_np_ptr(re), _np_ptr(im), len(re),
+                                         int(base_degree or len(re)), int(max_copies_per_root),
+                                         cap, _np_ptr(ore), _np_ptr(oim), C.byref(on)))
+    return ore[:on.value] + 1j * oim[:on.value]
+
+
+def eval_poly(roots, z: complex) -> complex:
+    re, im = _roots(roots)
+    a, b = C.c_double(), C.c_double()
+    _check(lib().ppa_eval_poly(_np_ptr(re), _np_ptr(im), len(re), C.c_double(complex(z).real),
+                               C.c_double(complex(z).imag), C.byref(a), C.byref(b)))
+    return complex(a.value, b.value)
+
+
+# ----------------------------------------------------------------- Arnoldi --
+class ArnoldiState:
+    """ArnoldiState (inc/arnoldi.hpp:18-26); V lives in HBM."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.ppa_arnoldi_free(self._h)
+            self._h = None
+
+    def _info(self):
+        cur, mx, bd = C.c_int(), C.c_int(), C.c_int()
+        ld = C.c_longlong()
+        V = C.c_void_p()
+        _check(lib().ppa_arnoldi_info(self._h, C.byref(cur), C.byref(mx), C.byref(bd),
+                                      C.byref(ld), C.byref(V)))
+        return cur.value, mx.value, bool(bd.value), ld.value, V.value
+
+    @property
+    def cur_dim(self):
+        return self._info()[0]
+
+    @property
+    def max_dim(self):
+        return self._info()[1]
+
+    @property
+    def breakdown(self):
+        return self._info()[2]
+
+    @property
+    def ld(self):
+        return self._info()[3]
+
+    @property
+    def V_ptr(self):
+        return self._info()[4]
+
+    @property
+    def H(self) -> np.ndarray:
+        m = self.max_dim
+        h = np.zeros((m + 1) * m)
+        _check(lib().ppa_arnoldi_get_H(self._h, _np_ptr(h)))
+        return h.reshape((m, m + 1)).T.copy()
+
+    def extend(self, op: LinearOperator, to_dim: int, rec: Optional[CostRecord] = None):
+        rec = rec if rec is not None else CostRecord()
+        _check(lib().ppa_arnoldi_extend(self._h, op._h, to_dim, C.byref(rec)))
+        return rec
+
+    def ritz_pairs(self, ordering=SMALLEST_MAGNITUDE):
+        d = self.cur_dim
+        re, im, rs = np.zeros(d), np.zeros(d), np.zeros(d)
+        _check(lib().ppa_arnoldi_ritz(self._h, ordering, _np_ptr(re), _np_ptr(im), _np_ptr(rs)))
+        return re + 1j * im, rs
+
+    def harmonic_ritz_values(self):
+        d = self.cur_dim
+        re, im = np.zeros(d), np.zeros(d)
+        _check(lib().ppa_arnoldi_harmonic(self._h, _np_ptr(re), _np_ptr(im)))
+        return re + 1j * im
+
+    def ritz_vector(self, j, y_re, y_im=None, ordering=SMALLEST_MAGNITUDE, rec=None):
+        rec = rec if rec is not None else CostRecord()
+        cx = C.c_int()
+        _check(lib().ppa_arnoldi_ritz_vector(self._h, ordering, j, _ptr(y_re), _ptr(y_im),
+                                             C.byref(cx), C.byref(rec)))
+        return bool(cx.value)
+
+    def thick_restart(self, k: int, ordering=SMALLEST_MAGNITUDE, rec=None) -> int:
+        rec = rec if rec is not None else CostRecord()
+        kk = C.c_int()
+        _check(lib().ppa_arnoldi_restart(self._h, ordering, k, C.byref(rec), C.byref(kk)))
+        return kk.value
+
+
+def arnoldi_init(v0, n: int, m: int, rec: Optional[CostRecord] = None) -> ArnoldiState:
+    rec = rec if rec is not None else CostRecord()
+    h = C.c_void_p()
+    _check(lib().ppa_arnoldi_init(_ptr(v0), n, m, C.byref(rec), C.byref(h)))
+    return ArnoldiState(h)
+
+
+def cgs2_step(V, ld, n, c, w, Hcol, flag) -> None:
+    _check(lib().ppa_cgs2_step(_ptr(V), ld, n, c, _ptr(w), _ptr(Hcol), _ptr(flag)))
+
+
+def ts_combine(V, ldv, n, d, G, p, Out, ldo) -> None:
+    _check(lib().ppa_ts_combine(_ptr(V), ldv, n, d, _ptr(G), p, _ptr(Out), ldo))
+
+
+# ------------------------------------------------------------------ solver --
+@dataclass
+class SolveConfig:
+    """SolveConfig (inc/solver.hpp:21-58)."""
+
+    m: int = 50
+    k: int = 20
+    nev: int = 15
+    degree: int = 0
+    rtol_multiplier: float = 1e-8
+    rtol_absolute: Optional[float] = None
+    variant: str = "ritz"
+    stability: str = "off"
+    double_d1: int = 0
+    double_d2: int = 0
+    max_cycles: int = 100
+    seed: int = 1
+    allow_nev_above_k: bool = False
+    reference: Sequence[complex] = field(default_factory=list)
+
+    def _c(self, use_double: bool) -> _SolveConfigC:
+        return _SolveConfigC(self.m, self.k, self.nev, self.degree, self.rtol_multiplier,
+                             self.rtol_absolute or 0.0, 1 if self.variant == "harmonic" else 0,
+                             1 if self.stability == "pof_auto" else 0, self.double_d1,
+                             self.double_d2, 1 if use_double else 0, self.max_cycles, self.seed,
+                             1 if self.allow_nev_above_k else 0)
+
+
+def _solve(a: LinearOperator, cfg: SolveConfig, use_double: bool) -> dict:
+    cap_nev, cap_roots, cap_cyc = max(cfg.nev, 1), 4096, max(cfg.max_cycles, 1)
+    bufs = {k: np.zeros(cap_nev) for k in ("eig_re", "eig_im", "residuals")}
+    conv = np.zeros(cap_nev, dtype=np.int32)
+    roots = {k: np.zeros(cap_roots) for k in ("poly_re", "poly_im", "inner_re", "inner_im")}
+    cyc = np.zeros(cap_cyc)
+    r = _SolveResultC()
+    r.cap_nev, r.cap_roots, r.cap_cycles = cap_nev, cap_roots, cap_cyc
+    for k, v in {**bufs, **roots}.items():
+        setattr(r, k, v.ctypes.data_as(_dp))
+    r.converged_flags = conv.ctypes.data_as(_ip)
+    r.cycle_max_residual = cyc.ctypes.data_as(_dp)
+    c = cfg._c(use_double)
+    _check(lib().ppa_solve(a._h, C.byref(c), C.byref(r)))
+    ne = min(r.n_eig, cap_nev)
+    eig = bufs["eig_re"][:ne] + 1j * bufs["eig_im"][:ne]
+    out = {
+        "eigenvalues": eig,
+        "residuals": bufs["residuals"][:ne].copy(),
+        "converged_flags": conv[:ne].astype(bool),
+        "converged": bool(r.converged),
+        "cycles": r.cycles,
+        "composite_degree": r.composite_degree,
+        "poly": roots["poly_re"][:r.n_poly] + 1j * roots["poly_im"][:r.n_poly],
+        "poly_base_degree": r.poly_base_degree,
+        "inner_poly": roots["inner_re"][:r.n_inner] + 1j * roots["inner_im"][:r.n_inner],
+        "rtol": r.rtol,
+        "max_err": r.max_err,
+        "norm_estimate": r.norm_estimate,
+        "cost": {"mvps": r.cost.mvps, "dots": r.cost.dots, "vops": r.cost.vops,
+                 "nnzr": r.cost.nnzr},
+        "cycle_max_residual": cyc[:r.n_cycles].copy(),
+        "timing": {"total": r.t_total, "setup": r.t_setup, "extend": r.t_extend,
+                   "check": r.t_check, "restart": r.t_restart},
+    }
+    if cfg.reference:
+        ref = np.asarray(cfg.reference, dtype=np.complex128)
+        out["correct_count"] = int(sum(
+            1 for z, ok in zip(eig, out["converged_flags"])
+            if ok and np.any(np.abs(z - ref) <= 1e-6 * np.abs(ref))))
+    return out
+
+
+def solve(a: LinearOperator, cfg: SolveConfig) -> dict:
+    """solve (inc/solver.hpp:94)."""
+    return _solve(a, cfg, False)
+
+
+def solve_double(a: LinearOperator, cfg: SolveConfig) -> dict:
+    """solve_double (inc/solver.hpp:111)."""
+    return _solve(a, cfg, True)

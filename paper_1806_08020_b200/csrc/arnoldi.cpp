@@ -1,0 +1,357 @@
+// Thick-restarted Arnoldi with the basis on the device.
+// Reference: src/arnoldi.cpp (cited per function).
+
+#include "ppa/arnoldi.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <stdexcept>
+
+#include "ppa/kernels.hpp"
+
+namespace ppa {
+
+namespace {
+
+using cplx = std::complex<double>;
+
+constexpr double kPairTol = 1e-10;  // src/arnoldi.cpp:16
+
+bool conj_pair(const cplx& a, const cplx& b) {
+  return std::abs(a - std::conj(b)) <= kPairTol * std::max(1.0, std::abs(a));
+}
+
+double sort_key(const cplx& z, RitzOrdering ord) {
+  switch (ord) {
+    case RitzOrdering::smallest_magnitude: return std::abs(z);
+    case RitzOrdering::largest_magnitude: return -std::abs(z);
+    case RitzOrdering::target_one: return std::abs(1.0 - z);
+  }
+  return std::abs(z);
+}
+
+// Stable sort by key with conjugate mates pulled adjacent, +imag first
+// (src/arnoldi.cpp:40-95).
+void arrange_pairs(RitzSet& s) {
+  const int d = s.count();
+  std::vector<int> idx(d);
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
+    return sort_key(s.values[a], s.ordering) < sort_key(s.values[b], s.ordering);
+  });
+  std::vector<int> out;
+  out.reserve(d);
+  std::vector<char> used(d, 0);
+  for (int r = 0; r < d; ++r) {
+    const int i = idx[r];
+    if (used[i]) continue;
+    used[i] = 1;
+    if (!ritz_is_complex(s.values[i])) {
+      out.push_back(i);
+      continue;
+    }
+    int mate = -1;
+    for (int q = 0; q < d && mate < 0; ++q) {
+      const int j = idx[q];
+      if (!used[j] && conj_pair(s.values[i], s.values[j])) mate = j;
+    }
+    if (mate < 0) {
+      out.push_back(i);
+      continue;
+    }
+    used[mate] = 1;
+    if (s.values[i].imag() >= 0.0) {
+      out.push_back(i);
+      out.push_back(mate);
+    } else {
+      out.push_back(mate);
+      out.push_back(i);
+    }
+  }
+  std::vector<cplx> v(d);
+  std::vector<double> res(d);
+  dense::CMat g(s.vectors_h.rows, d);
+  for (int r = 0; r < d; ++r) {
+    v[r] = s.values[out[r]];
+    res[r] = s.residuals[out[r]];
+    for (int i = 0; i < g.rows; ++i) g(i, r) = s.vectors_h(i, out[r]);
+  }
+  s.values = std::move(v);
+  s.residuals = std::move(res);
+  s.vectors_h = std::move(g);
+}
+
+dense::Mat leading_block(const ArnoldiState& st, int d) {
+  dense::Mat M(d, d);
+  for (int j = 0; j < d; ++j)
+    for (int i = 0; i < d; ++i) M(i, j) = st.h(i, j);
+  return M;
+}
+
+// M + hsub^2 f e_d^T with f = Hd^{-T} e_d (src/arnoldi.cpp:183-198).
+dense::Mat harmonic_matrix(const ArnoldiState& st, const char* who) {
+  const int d = st.cur_dim;
+  dense::Mat M = leading_block(st, d);
+  const double hsub = st.h(d, d - 1);
+  if (hsub != 0.0) {
+    std::vector<double> ed(d, 0.0), f;
+    ed[d - 1] = 1.0;
+    if (!dense::solve_transpose_full_pivot(M, ed, f)) {
+      throw std::runtime_error(std::string(who) +
+                               ": singular projection (GMRES stagnation); "
+                               "try a different starting vector");
+    }
+    for (int i = 0; i < d; ++i) M(i, d - 1) += (hsub * hsub) * f[i];
+  }
+  return M;
+}
+
+long long round_ld(int n) { return (static_cast<long long>(n) + 31) / 32 * 32; }
+
+}  // namespace
+
+bool ritz_is_complex(const cplx& z) {
+  return std::abs(z.imag()) > kPairTol * std::max(1.0, std::abs(z));
+}
+
+ArnoldiState arnoldi_init(const double* v0, int n, int m, CostRecord& rec) {
+  if (m < 1) throw std::invalid_argument("arnoldi_init: m < 1");
+  if (n < m + 1) throw std::invalid_argument("arnoldi_init: m+1 exceeds dimension");
+  Context& ctx = current_context();
+  ArnoldiState st;
+  st.max_dim = m;
+  st.n = n;
+  st.ld = round_ld(n);
+  st.V.resize(static_cast<size_t>(st.ld) * (m + 1));
+  PPA_CUDA(cudaMemsetAsync(st.V.get(), 0, st.V.size() * sizeof(double), ctx.stream()));
+  st.H.assign(static_cast<size_t>(m + 1) * m, 0.0);
+  const double nb = ctx.nrm2_sync(v0, n);
+  ++rec.dots;
+  ++rec.vops;
+  if (nb == 0.0) throw std::invalid_argument("arnoldi_init: zero start");
+  kern::copy(v0, st.col(0), n, ctx.stream());
+  kern::scale(st.col(0), 1.0 / nb, n, ctx.stream());
+  ++rec.vops;
+  return st;
+}
+
+void arnoldi_extend(ArnoldiState& st, const LinearOperator& op, int to_dim, CostRecord& rec) {
+  if (to_dim > st.max_dim) throw std::invalid_argument("arnoldi_extend: to_dim > max_dim");
+  if (to_dim <= st.cur_dim) throw std::invalid_argument("arnoldi_extend: to_dim <= cur_dim");
+  if (op.dim() != st.n) throw std::invalid_argument("arnoldi_extend: dimension mismatch");
+  Context& ctx = current_context();
+  const cudaStream_t s = ctx.stream();
+  Scratch w(static_cast<size_t>(st.n));
+  Scratch hdev(static_cast<size_t>(st.max_dim) + 4);
+  double* Hcol = hdev.get();
+  int* flag = reinterpret_cast<int*>(hdev.get() + st.max_dim + 2);
+  double* host = ctx.pinned(static_cast<size_t>(st.max_dim) + 4);
+  for (int j = st.cur_dim; j < to_dim; ++j) {
+    op.apply(st.col(j), w.get(), rec);
+    const int c = j + 1;
+    kern::cgs2_step(st.V.get(), st.ld, st.n, c, w.get(), Hcol, flag, ctx.ws(), ctx.sm_count(), s);
+    PPA_CUDA(cudaMemcpyAsync(host, hdev.get(), (st.max_dim + 4) * sizeof(double),
+                             cudaMemcpyDeviceToHost, s));
+    ctx.sync();
+    for (int i = 0; i <= c; ++i) st.h(i, j) = host[i];
+    const int bd = *reinterpret_cast<const int*>(host + st.max_dim + 2);
+    // MGS2 charges (src/arnoldi.cpp:130-140): 2c dots+axpys, one norm.
+    rec.dots += 2LL * c + 1;
+    rec.vops += 4LL * c + 1;
+    st.cur_dim = j + 1;
+    if (bd == 2) throw std::runtime_error("arnoldi_extend: non-finite basis vector");
+    if (bd == 1) {
+      st.h(j + 1, j) = 0.0;
+      st.breakdown = true;
+      return;
+    }
+    ++rec.vops;  // the scaling (src/arnoldi.cpp:149-150)
+  }
+}
+
+RitzSet ritz_pairs(const ArnoldiState& st, RitzOrdering ordering) {
+  const int d = st.cur_dim;
+  if (d < 1) throw std::invalid_argument("ritz_pairs: empty state");
+  RitzSet set;
+  set.ordering = ordering;
+  if (!dense::eig(leading_block(st, d), set.values, &set.vectors_h)) {
+    throw std::runtime_error("ritz_pairs: Hessenberg eigensolver failed");
+  }
+  set.residuals.resize(d);
+  const double hsub = st.h(d, d - 1);
+  for (int i = 0; i < d; ++i) {
+    double nn = 0.0;
+    for (int r = 0; r < d; ++r) nn += std::norm(set.vectors_h(r, i));
+    const double nrm = std::sqrt(nn);
+    for (int r = 0; r < d; ++r) set.vectors_h(r, i) /= nrm;
+    set.residuals[i] = std::abs(hsub) * std::abs(set.vectors_h(d - 1, i));
+  }
+  arrange_pairs(set);
+  return set;
+}
+
+std::vector<cplx> harmonic_ritz_values(const ArnoldiState& st) {
+  if (st.cur_dim < 1) throw std::invalid_argument("harmonic_ritz_values: empty state");
+  const dense::Mat M = harmonic_matrix(st, "harmonic_ritz_values");
+  std::vector<cplx> vals;
+  if (!dense::eig(M, vals, nullptr)) {
+    throw std::runtime_error("harmonic_ritz_values: eigensolver failed");
+  }
+  return vals;
+}
+
+RitzSet harmonic_restart_selection(const ArnoldiState& st, RitzOrdering ordering) {
+  const int d = st.cur_dim;
+  if (d < 1) throw std::invalid_argument("harmonic_restart_selection: empty");
+  const dense::Mat M = harmonic_matrix(st, "harmonic_restart_selection");
+  const dense::Mat Hd = leading_block(st, d);
+  const double hsub = st.h(d, d - 1);
+  RitzSet set;
+  set.ordering = ordering;
+  set.harmonic = true;
+  if (!dense::eig(M, set.values, &set.vectors_h)) {
+    throw std::runtime_error("harmonic_restart_selection: eigensolver failed");
+  }
+  set.residuals.resize(d);
+  for (int i = 0; i < d; ++i) {
+    double nn = 0.0;
+    for (int r = 0; r < d; ++r) nn += std::norm(set.vectors_h(r, i));
+    const double nrm = std::sqrt(nn);
+    for (int r = 0; r < d; ++r) set.vectors_h(r, i) /= nrm;
+    // ||Hd g - theta g||^2 + |hsub g_d|^2 (src/arnoldi.cpp:242-246)
+    double top = 0.0;
+    for (int r = 0; r < d; ++r) {
+      cplx acc(0.0, 0.0);
+      for (int c = 0; c < d; ++c) acc += Hd(r, c) * set.vectors_h(c, i);
+      top += std::norm(acc - set.values[i] * set.vectors_h(r, i));
+    }
+    set.residuals[i] = std::sqrt(top + std::norm(hsub * set.vectors_h(d - 1, i)));
+  }
+  arrange_pairs(set);
+  return set;
+}
+
+DeviceComplexVector ritz_vector(const ArnoldiState& st, const RitzSet& set, int j,
+                                CostRecord& rec) {
+  const int d = set.vectors_h.rows;
+  if (j < 0 || j >= set.count()) throw std::invalid_argument("ritz_vector: index out of range");
+  Context& ctx = current_context();
+  const cudaStream_t s = ctx.stream();
+  double imn = 0.0;
+  for (int r = 0; r < d; ++r) imn += set.vectors_h(r, j).imag() * set.vectors_h(r, j).imag();
+  const bool cplx_vec = std::sqrt(imn) > 0.0;
+  const int p = cplx_vec ? 2 : 1;
+  std::vector<double> g(static_cast<size_t>(d) * p);
+  for (int r = 0; r < d; ++r) {
+    g[r] = set.vectors_h(r, j).real();
+    if (cplx_vec) g[d + r] = set.vectors_h(r, j).imag();
+  }
+  Scratch gdev(g.size());
+  PPA_CUDA(cudaMemcpyAsync(gdev.get(), g.data(), g.size() * sizeof(double),
+                           cudaMemcpyHostToDevice, s));
+  DeviceComplexVector y;
+  y.complex = cplx_vec;
+  const long long ldy = round_ld(st.n);
+  Scratch tmp(static_cast<size_t>(ldy) * p);
+  kern::ts_combine(st.V.get(), st.ld, st.n, d, gdev.get(), p, tmp.get(), ldy, s);
+  rec.vops += static_cast<long long>(p) * d;
+  double* sums = ctx.results();
+  kern::col_sumsq(tmp.get(), ldy, st.n, p, sums, ctx.ws(), ctx.sm_count(), s);
+  double* h = ctx.pinned(2);
+  PPA_CUDA(cudaMemcpyAsync(h, sums, p * sizeof(double), cudaMemcpyDeviceToHost, s));
+  ctx.sync();
+  const double nrm = std::sqrt(h[0] + (cplx_vec ? h[1] : 0.0));
+  y.re.resize(st.n);
+  kern::copy(tmp.get(), y.re.get(), st.n, s);
+  kern::div_value(y.re.get(), nrm, st.n, s);
+  if (cplx_vec) {
+    y.im.resize(st.n);
+    kern::copy(tmp.get() + ldy, y.im.get(), st.n, s);
+    kern::div_value(y.im.get(), nrm, st.n, s);
+  }
+  rec.dots += cplx_vec ? 2 : 1;
+  rec.vops += cplx_vec ? 4 : 2;
+  ctx.sync();  // gdev / tmp are released on return
+  return y;
+}
+
+int thick_restart(ArnoldiState& st, const RitzSet& keep, int k, CostRecord& rec) {
+  const int m = st.cur_dim;
+  if (m != st.max_dim) throw std::invalid_argument("thick_restart: cycle not at full dimension");
+  if (k <= 0 || k >= m) throw std::invalid_argument("thick_restart: bad k");
+  if (keep.count() < k) throw std::invalid_argument("thick_restart: selection smaller than k");
+  if (st.h(m, m - 1) == 0.0) {
+    throw std::runtime_error("thick_restart: no residual vector (breakdown)");
+  }
+  // Real basis of the kept span (src/arnoldi.cpp:285-299).
+  dense::Mat G(m, k);
+  int col = 0, j = 0;
+  while (col < k && j < keep.count()) {
+    if (!ritz_is_complex(keep.values[j])) {
+      for (int r = 0; r < m; ++r) G(r, col) = keep.vectors_h(r, j).real();
+      ++col;
+      j += 1;
+    } else {
+      if (col + 2 > k) break;
+      for (int r = 0; r < m; ++r) {
+        G(r, col) = keep.vectors_h(r, j).real();
+        G(r, col + 1) = keep.vectors_h(r, j).imag();
+      }
+      col += 2;
+      j += 2;
+    }
+  }
+  const int kk = col;
+  if (kk == 0) throw std::invalid_argument("thick_restart: k too small");
+  dense::Mat Gk(m, kk);
+  std::copy(G.a.begin(), G.a.begin() + static_cast<long>(m) * kk, Gk.a.begin());
+  const dense::Mat Q = dense::householder_q(Gk);
+  const dense::Mat Hm = leading_block(st, m);
+  dense::Mat Hk = dense::matmul_tn(Q, dense::matmul(Hm, Q));
+  std::vector<double> hrow(kk);
+  for (int c = 0; c < kk; ++c) hrow[c] = st.h(m, m - 1) * Q(m - 1, c);
+
+  Context& ctx = current_context();
+  const cudaStream_t s = ctx.stream();
+  Scratch qdev(Q.a.size());
+  PPA_CUDA(cudaMemcpyAsync(qdev.get(), Q.a.data(), Q.a.size() * sizeof(double),
+                           cudaMemcpyHostToDevice, s));
+  kern::ts_combine(st.V.get(), st.ld, st.n, m, qdev.get(), kk, st.V.get(), st.ld, s);
+  rec.vops += static_cast<long long>(m) * kk;
+  kern::copy(st.col(m), st.col(kk), st.n, s);
+
+  // Reorthogonalise the carried residual vector (one pass) and fold the
+  // corrections into H (src/arnoldi.cpp:313-333).
+  double* dres = ctx.results();
+  Scratch corr(static_cast<size_t>(kk) + 1);
+  kern::cgs1_pass(st.V.get(), st.ld, st.n, kk, st.col(kk), corr.get(), dres, ctx.ws(),
+                  ctx.sm_count(), s);
+  double* h = ctx.pinned(static_cast<size_t>(kk) + 1);
+  PPA_CUDA(cudaMemcpyAsync(h, corr.get(), kk * sizeof(double), cudaMemcpyDeviceToHost, s));
+  PPA_CUDA(cudaMemcpyAsync(h + kk, dres, sizeof(double), cudaMemcpyDeviceToHost, s));
+  ctx.sync();
+  std::vector<double> cvec(h, h + kk);
+  const double rn = h[kk];
+  rec.dots += kk;
+  rec.vops += 2LL * kk;
+  ++rec.dots;
+  ++rec.vops;
+  kern::scale(st.col(kk), 1.0 / rn, st.n, s);
+  ++rec.vops;
+  for (int c = 0; c < kk; ++c)
+    for (int r = 0; r < kk; ++r) Hk(r, c) += cvec[r] * hrow[c];
+
+  std::fill(st.H.begin(), st.H.end(), 0.0);
+  for (int c = 0; c < kk; ++c) {
+    for (int r = 0; r < kk; ++r) st.h(r, c) = Hk(r, c);
+    st.h(kk, c) = rn * hrow[c];
+  }
+  st.cur_dim = kk;
+  st.restart_k = kk;
+  ++st.cycle_count;
+  ctx.sync();  // qdev is released on return
+  return kk;
+}
+
+}  // namespace ppa

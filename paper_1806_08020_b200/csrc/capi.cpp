@@ -1,0 +1,570 @@
+// extern "C" boundary (include/ppa_b200.h).  Every entry catches and maps
+// the C++ exceptions of the ppa namespace to status codes.
+
+#include "ppa_b200.h"
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "ppa/arnoldi.hpp"
+#include "ppa/gmres_poly.hpp"
+#include "ppa/kernels.hpp"
+#include "ppa/operators.hpp"
+#include "ppa/rng.hpp"
+#include "ppa/solver.hpp"
+
+struct ppa_host_csr {
+  ppa::CsrMatrix m;
+};
+struct ppa_op {
+  ppa::OperatorPtr p;
+};
+struct ppa_arnoldi {
+  ppa::ArnoldiState s;
+};
+
+namespace {
+
+thread_local std::string t_err;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return PPA_OK;
+  } catch (const std::invalid_argument& e) {
+    t_err = e.what();
+    return PPA_INVALID_ARGUMENT;
+  } catch (const std::logic_error& e) {
+    t_err = e.what();
+    return PPA_LOGIC_ERROR;
+  } catch (const ppa::CudaError& e) {
+    t_err = e.what();
+    return PPA_CUDA_ERROR;
+  } catch (const std::runtime_error& e) {
+    t_err = e.what();
+    return PPA_RUNTIME_ERROR;
+  } catch (const std::exception& e) {
+    t_err = e.what();
+    return PPA_INTERNAL_ERROR;
+  } catch (...) {
+    t_err = "unknown error";
+    return PPA_INTERNAL_ERROR;
+  }
+}
+
+void add_cost(ppa_cost* c, const ppa::CostRecord& r) {
+  if (!c) return;
+  c->mvps += r.mvps;
+  c->dots += r.dots;
+  c->vops += r.vops;
+  if (r.nnzr > 0) c->nnzr = r.nnzr;
+  c->wall_seconds += r.wall_seconds;
+}
+
+std::vector<std::complex<double>> roots_of(const double* re, const double* im, int n) {
+  if (n < 0) throw std::invalid_argument("root list: negative length");
+  if (n > 0 && (!re || !im)) throw std::invalid_argument("root list: null pointer");
+  std::vector<std::complex<double>> r(n);
+  for (int i = 0; i < n; ++i) r[i] = {re[i], im[i]};
+  return r;
+}
+
+ppa::PolyPrecond poly_of(const double* re, const double* im, int n, int base_degree) {
+  ppa::PolyPrecond p;
+  p.roots = roots_of(re, im, n);
+  p.base_degree = base_degree > 0 ? base_degree : n;
+  p.multiplicity.resize(p.roots.size());
+  for (size_t i = 0; i < p.roots.size(); ++i)
+    p.multiplicity[i] = static_cast<int>(std::count(p.roots.begin(), p.roots.end(), p.roots[i]));
+  return p;
+}
+
+ppa_host_csr* wrap(ppa::CsrMatrix&& m) {
+  auto* h = new ppa_host_csr;
+  h->m = std::move(m);
+  return h;
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw std::invalid_argument(std::string(what) + ": null pointer");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ppa_last_error(void) { return t_err.c_str(); }
+int ppa_abi_version(void) { return 1; }
+
+int ppa_device_info(int* sm_count, double* l2_bytes) {
+  return guard([&] {
+    int dev = 0, sms = 0, l2 = 0;
+    PPA_CUDA(cudaGetDevice(&dev));
+    PPA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    PPA_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+    if (sm_count) *sm_count = sms;
+    if (l2_bytes) *l2_bytes = l2;
+  });
+}
+
+int ppa_set_stream(void* s) {
+  return guard([&] { ppa::set_current_stream(static_cast<cudaStream_t>(s)); });
+}
+
+int ppa_synchronize(void) {
+  return guard([&] { ppa::current_context().sync(); });
+}
+
+int ppa_host_csr_create(int n, long long nnz, const int* row_ptr, const int* col_idx,
+                        const double* values, ppa_host_csr** out) {
+  return guard([&] {
+    need(out, "ppa_host_csr_create");
+    if (n < 0 || nnz < 0) throw std::invalid_argument("CsrMatrix: negative dimension");
+    need(row_ptr, "ppa_host_csr_create");
+    if (nnz > 0) {
+      need(col_idx, "ppa_host_csr_create");
+      need(values, "ppa_host_csr_create");
+    }
+    ppa::CsrMatrix m;
+    m.n = n;
+    m.row_ptr.assign(row_ptr, row_ptr + n + 1);
+    m.col_idx.assign(col_idx, col_idx + nnz);
+    m.values.assign(values, values + nnz);
+    m.validate();
+    *out = wrap(std::move(m));
+  });
+}
+
+int ppa_host_csr_from_triplets(int n, long long count, const int* rows, const int* cols,
+                               const double* vals, ppa_host_csr** out) {
+  return guard([&] {
+    need(out, "ppa_host_csr_from_triplets");
+    std::vector<std::tuple<int, int, double>> t;
+    t.reserve(static_cast<size_t>(count));
+    for (long long i = 0; i < count; ++i) t.emplace_back(rows[i], cols[i], vals[i]);
+    *out = wrap(ppa::CsrMatrix::from_triplets(n, std::move(t)));
+  });
+}
+
+int ppa_gen_convdiff_ref(int grid_n, ppa_host_csr** out) {
+  return guard([&] { need(out, "gen"); *out = wrap(ppa::make_convection_diffusion(grid_n)); });
+}
+int ppa_gen_config(int config, ppa_host_csr** out) {
+  return guard([&] { need(out, "gen"); *out = wrap(ppa::make_config_matrix(config)); });
+}
+int ppa_gen_bidiagonal(int n, ppa_host_csr** out) {
+  return guard([&] { need(out, "gen"); *out = wrap(ppa::make_bidiagonal(n)); });
+}
+int ppa_gen_convdiff_const(int grid_n, double peclet, ppa_host_csr** out) {
+  return guard([&] {
+    need(out, "gen");
+    *out = wrap(ppa::make_convection_diffusion_const(grid_n, peclet));
+  });
+}
+int ppa_gen_laplacian_3d(int grid_n, ppa_host_csr** out) {
+  return guard([&] { need(out, "gen"); *out = wrap(ppa::make_laplacian_3d(grid_n)); });
+}
+int ppa_gen_random_poisson(int n, double lambda, unsigned long long seed, ppa_host_csr** out) {
+  return guard([&] { need(out, "gen"); *out = wrap(ppa::make_random_poisson(n, lambda, seed)); });
+}
+
+int ppa_host_csr_info(const ppa_host_csr* m, int* n, long long* nnz,
+                      unsigned long long* fingerprint) {
+  return guard([&] {
+    need(m, "ppa_host_csr_info");
+    if (n) *n = m->m.n;
+    if (nnz) *nnz = m->m.nnz();
+    if (fingerprint) *fingerprint = ppa::csr_fingerprint(m->m);
+  });
+}
+
+int ppa_host_csr_arrays(const ppa_host_csr* m, const int** row_ptr, const int** col_idx,
+                        const double** values) {
+  return guard([&] {
+    need(m, "ppa_host_csr_arrays");
+    if (row_ptr) *row_ptr = m->m.row_ptr.data();
+    if (col_idx) *col_idx = m->m.col_idx.data();
+    if (values) *values = m->m.values.data();
+  });
+}
+
+void ppa_host_csr_free(ppa_host_csr* m) { delete m; }
+
+int ppa_normal_vector(long long n, unsigned long long seed, unsigned long long stream,
+                      double* out) {
+  return guard([&] {
+    need(out, "ppa_normal_vector");
+    const uint64_t k = ppa::rng::key(seed, stream);
+    for (long long i = 0; i < n; ++i) out[i] = ppa::rng::normal_at(k, static_cast<uint64_t>(i));
+  });
+}
+
+int ppa_csr_operator(const ppa_host_csr* m, ppa_op** out) {
+  return guard([&] {
+    need(m, "ppa_csr_operator");
+    need(out, "ppa_csr_operator");
+    auto* o = new ppa_op;
+    try {
+      o->p = ppa::make_csr_operator(m->m);
+    } catch (...) {
+      delete o;
+      throw;
+    }
+    *out = o;
+  });
+}
+
+int ppa_diagonal_operator(int n, const double* diag, ppa_op** out) {
+  return guard([&] {
+    need(out, "ppa_diagonal_operator");
+    if (n > 0) need(diag, "ppa_diagonal_operator");
+    std::vector<double> d(diag, diag + std::max(0, n));
+    auto* o = new ppa_op;
+    try {
+      o->p = ppa::make_diagonal(std::move(d));
+    } catch (...) {
+      delete o;
+      throw;
+    }
+    *out = o;
+  });
+}
+
+int ppa_poly_operator(const ppa_op* base, const double* re, const double* im, int nroots,
+                      int base_degree, int complement, ppa_op** out) {
+  return guard([&] {
+    need(base, "ppa_poly_operator");
+    need(out, "ppa_poly_operator");
+    ppa::PolyPrecond p = poly_of(re, im, nroots, base_degree);
+    auto* o = new ppa_op;
+    try {
+      o->p = complement ? ppa::make_poly_complement_operator(base->p, std::move(p))
+                        : ppa::make_poly_operator(base->p, std::move(p));
+    } catch (...) {
+      delete o;
+      throw;
+    }
+    *out = o;
+  });
+}
+
+void ppa_op_free(ppa_op* op) { delete op; }
+
+int ppa_op_info(const ppa_op* op, int* dim, int* mvps, double* nnzr, int* kind) {
+  return guard([&] {
+    need(op, "ppa_op_info");
+    if (dim) *dim = op->p->dim();
+    if (mvps) *mvps = op->p->mvps_per_apply();
+    if (nnzr) *nnzr = op->p->nnzr();
+    if (kind) *kind = static_cast<int>(op->p->kind());
+  });
+}
+
+int ppa_op_apply(const ppa_op* op, const double* x, double* y, ppa_cost* cost) {
+  return guard([&] {
+    need(op, "ppa_op_apply");
+    ppa::CostRecord r;
+    op->p->apply(x, y, r);
+    add_cost(cost, r);
+  });
+}
+
+int ppa_op_apply_host(const ppa_op* op, const double* x, double* y, ppa_cost* cost) {
+  return guard([&] {
+    need(op, "ppa_op_apply_host");
+    need(x, "ppa_op_apply_host");
+    need(y, "ppa_op_apply_host");
+    ppa::Context& ctx = ppa::current_context();
+    const size_t bytes = static_cast<size_t>(op->p->dim()) * sizeof(double);
+    ppa::Scratch dx(op->p->dim()), dy(op->p->dim());
+    PPA_CUDA(cudaMemcpyAsync(dx.get(), x, bytes, cudaMemcpyHostToDevice, ctx.stream()));
+    ppa::CostRecord r;
+    op->p->apply(dx.get(), dy.get(), r);
+    PPA_CUDA(cudaMemcpyAsync(y, dy.get(), bytes, cudaMemcpyDeviceToHost, ctx.stream()));
+    ctx.sync();
+    add_cost(cost, r);
+  });
+}
+
+int ppa_csr_model_bytes(const ppa_op* op, double* bytes, long long* nnz) {
+  return guard([&] {
+    need(op, "ppa_csr_model_bytes");
+    const auto* c = dynamic_cast<const ppa::CsrOperator*>(op->p.get());
+    if (!c) throw std::invalid_argument("ppa_csr_model_bytes: not a CSR operator");
+    if (bytes) *bytes = c->model_bytes();
+    if (nnz) *nnz = c->nnz();
+  });
+}
+
+int ppa_apply_poly(const double* re, const double* im, int nroots, const ppa_op* a,
+                   const double* v, double* out, ppa_cost* cost) {
+  return guard([&] {
+    need(a, "ppa_apply_poly");
+    ppa::PolyPrecond p = poly_of(re, im, nroots, nroots);
+    ppa::CostRecord r;
+    ppa::apply_poly(p, *a->p, v, out, r);
+    add_cost(cost, r);
+  });
+}
+
+int ppa_build_gmres_poly(const ppa_op* a, const double* b, int degree, double* re, double* im,
+                         int* nroots, int* truncated, ppa_cost* cost) {
+  return guard([&] {
+    need(a, "ppa_build_gmres_poly");
+    need(re, "ppa_build_gmres_poly");
+    need(im, "ppa_build_gmres_poly");
+    ppa::CostRecord r;
+    const ppa::PolyPrecond p = ppa::build_gmres_poly(*a->p, b, degree, r);
+    for (size_t i = 0; i < p.roots.size(); ++i) {
+      re[i] = p.roots[i].real();
+      im[i] = p.roots[i].imag();
+    }
+    if (nroots) *nroots = p.effective_degree();
+    if (truncated) *truncated = p.truncated ? 1 : 0;
+    add_cost(cost, r);
+  });
+}
+
+int ppa_leja_order(const double* re, const double* im, int n, double* out_re, double* out_im) {
+  return guard([&] {
+    need(out_re, "ppa_leja_order");
+    need(out_im, "ppa_leja_order");
+    const auto o = ppa::leja_order(roots_of(re, im, n));
+    for (size_t i = 0; i < o.size(); ++i) {
+      out_re[i] = o[i].real();
+      out_im[i] = o[i].imag();
+    }
+  });
+}
+
+int ppa_compute_pof(const double* re, const double* im, int n, double* log10_pof, int* copies,
+                    int* ndistinct, double* max_log10, int* total) {
+  return guard([&] {
+    const ppa::PofReport rep = ppa::compute_pof(poly_of(re, im, n, n));
+    for (size_t i = 0; i < rep.log10_pof.size(); ++i) {
+      if (log10_pof) log10_pof[i] = rep.log10_pof[i];
+      if (copies) copies[i] = rep.copies_needed[i];
+    }
+    if (ndistinct) *ndistinct = static_cast<int>(rep.log10_pof.size());
+    if (max_log10) *max_log10 = rep.max_log10_pof;
+    if (total) *total = rep.total_copies;
+  });
+}
+
+int ppa_add_stability_roots(const double* re, const double* im, int n, int base_degree,
+                            int max_copies, int cap, double* out_re, double* out_im,
+                            int* out_n) {
+  return guard([&] {
+    need(out_re, "ppa_add_stability_roots");
+    need(out_im, "ppa_add_stability_roots");
+    const ppa::PolyPrecond p =
+        ppa::add_stability_roots(poly_of(re, im, n, base_degree), max_copies);
+    if (static_cast<int>(p.roots.size()) > cap) {
+      throw std::invalid_argument("ppa_add_stability_roots: output capacity too small");
+    }
+    for (size_t i = 0; i < p.roots.size(); ++i) {
+      out_re[i] = p.roots[i].real();
+      out_im[i] = p.roots[i].imag();
+    }
+    if (out_n) *out_n = p.effective_degree();
+  });
+}
+
+int ppa_eval_poly(const double* re, const double* im, int n, double zr, double zi, double* o_re,
+                  double* o_im) {
+  return guard([&] {
+    const std::complex<double> v = ppa::eval_poly(poly_of(re, im, n, n), {zr, zi});
+    if (o_re) *o_re = v.real();
+    if (o_im) *o_im = v.imag();
+  });
+}
+
+int ppa_arnoldi_init(const double* v0, int n, int m, ppa_cost* cost, ppa_arnoldi** out) {
+  return guard([&] {
+    need(out, "ppa_arnoldi_init");
+    need(v0, "ppa_arnoldi_init");
+    ppa::CostRecord r;
+    auto* st = new ppa_arnoldi;
+    try {
+      st->s = ppa::arnoldi_init(v0, n, m, r);
+    } catch (...) {
+      delete st;
+      throw;
+    }
+    *out = st;
+    add_cost(cost, r);
+  });
+}
+
+int ppa_arnoldi_extend(ppa_arnoldi* st, const ppa_op* op, int to_dim, ppa_cost* cost) {
+  return guard([&] {
+    need(st, "ppa_arnoldi_extend");
+    need(op, "ppa_arnoldi_extend");
+    ppa::CostRecord r;
+    try {
+      ppa::arnoldi_extend(st->s, *op->p, to_dim, r);
+    } catch (...) {
+      add_cost(cost, r);
+      throw;
+    }
+    add_cost(cost, r);
+  });
+}
+
+int ppa_arnoldi_info(const ppa_arnoldi* st, int* cur, int* maxd, int* bd, long long* ld,
+                     double** V) {
+  return guard([&] {
+    need(st, "ppa_arnoldi_info");
+    if (cur) *cur = st->s.cur_dim;
+    if (maxd) *maxd = st->s.max_dim;
+    if (bd) *bd = st->s.breakdown ? 1 : 0;
+    if (ld) *ld = st->s.ld;
+    if (V) *V = st->s.V.get();
+  });
+}
+
+int ppa_arnoldi_get_H(const ppa_arnoldi* st, double* H) {
+  return guard([&] {
+    need(st, "ppa_arnoldi_get_H");
+    need(H, "ppa_arnoldi_get_H");
+    std::memcpy(H, st->s.H.data(), st->s.H.size() * sizeof(double));
+  });
+}
+
+int ppa_arnoldi_ritz(const ppa_arnoldi* st, int ordering, double* re, double* im,
+                     double* resid) {
+  return guard([&] {
+    need(st, "ppa_arnoldi_ritz");
+    const ppa::RitzSet s = ppa::ritz_pairs(st->s, static_cast<ppa::RitzOrdering>(ordering));
+    for (int i = 0; i < s.count(); ++i) {
+      if (re) re[i] = s.values[i].real();
+      if (im) im[i] = s.values[i].imag();
+      if (resid) resid[i] = s.residuals[i];
+    }
+  });
+}
+
+int ppa_arnoldi_harmonic(const ppa_arnoldi* st, double* re, double* im) {
+  return guard([&] {
+    need(st, "ppa_arnoldi_harmonic");
+    const auto v = ppa::harmonic_ritz_values(st->s);
+    for (size_t i = 0; i < v.size(); ++i) {
+      if (re) re[i] = v[i].real();
+      if (im) im[i] = v[i].imag();
+    }
+  });
+}
+
+int ppa_arnoldi_ritz_vector(const ppa_arnoldi* st, int ordering, int j, double* yr, double* yi,
+                            int* is_complex, ppa_cost* cost) {
+  return guard([&] {
+    need(st, "ppa_arnoldi_ritz_vector");
+    need(yr, "ppa_arnoldi_ritz_vector");
+    const ppa::RitzSet s = ppa::ritz_pairs(st->s, static_cast<ppa::RitzOrdering>(ordering));
+    ppa::CostRecord r;
+    ppa::DeviceComplexVector y = ppa::ritz_vector(st->s, s, j, r);
+    const cudaStream_t str = ppa::current_context().stream();
+    ppa::kern::copy(y.re.get(), yr, st->s.n, str);
+    if (y.complex && yi) ppa::kern::copy(y.im.get(), yi, st->s.n, str);
+    ppa::current_context().sync();
+    if (is_complex) *is_complex = y.complex ? 1 : 0;
+    add_cost(cost, r);
+  });
+}
+
+int ppa_arnoldi_restart(ppa_arnoldi* st, int ordering, int k, ppa_cost* cost, int* kk) {
+  return guard([&] {
+    need(st, "ppa_arnoldi_restart");
+    const ppa::RitzSet s = ppa::ritz_pairs(st->s, static_cast<ppa::RitzOrdering>(ordering));
+    ppa::CostRecord r;
+    const int got = ppa::thick_restart(st->s, s, k, r);
+    if (kk) *kk = got;
+    add_cost(cost, r);
+  });
+}
+
+void ppa_arnoldi_free(ppa_arnoldi* st) { delete st; }
+
+int ppa_spmv(const ppa_op* a, const double* x, double* y) {
+  return guard([&] {
+    need(a, "ppa_spmv");
+    const auto* c = dynamic_cast<const ppa::CsrOperator*>(a->p.get());
+    if (!c) throw std::invalid_argument("ppa_spmv: not a CSR operator");
+    ppa::kern::spmv(c->device(), x, y, ppa::kern::EpiArgs{}, ppa::current_context().stream());
+  });
+}
+
+int ppa_cgs2_step(double* V, long long ld, int n, int c, double* w, double* Hcol, int* flag) {
+  return guard([&] {
+    ppa::Context& ctx = ppa::current_context();
+    ppa::kern::cgs2_step(V, ld, n, c, w, Hcol, flag, ctx.ws(), ctx.sm_count(), ctx.stream());
+  });
+}
+
+int ppa_ts_combine(const double* V, long long ldv, int n, int d, const double* G, int p,
+                   double* Out, long long ldo) {
+  return guard([&] {
+    ppa::kern::ts_combine(V, ldv, n, d, G, p, Out, ldo, ppa::current_context().stream());
+  });
+}
+
+int ppa_solve(const ppa_op* a, const ppa_solve_config* c, ppa_solve_result* res) {
+  return guard([&] {
+    need(a, "ppa_solve");
+    need(c, "ppa_solve");
+    need(res, "ppa_solve");
+    ppa::SolveConfig cfg;
+    cfg.m = c->m;
+    cfg.k = c->k;
+    cfg.nev = c->nev;
+    cfg.degree = c->degree;
+    cfg.rtol_multiplier = c->rtol_multiplier;
+    if (c->rtol_absolute > 0) cfg.rtol_absolute = c->rtol_absolute;
+    cfg.variant = c->variant ? ppa::RestartVariant::harmonic : ppa::RestartVariant::ritz;
+    cfg.stability = c->stability ? ppa::StabilityMode::pof_auto : ppa::StabilityMode::off;
+    cfg.double_d1 = c->double_d1;
+    cfg.double_d2 = c->double_d2;
+    cfg.max_cycles = c->max_cycles;
+    cfg.seed = c->seed;
+    cfg.allow_nev_above_k = c->allow_nev_above_k != 0;
+    const ppa::EigResult r = c->use_double ? ppa::solve_double(a->p, cfg) : ppa::solve(a->p, cfg);
+    res->n_eig = static_cast<int>(r.eigenvalues.size());
+    for (int i = 0; i < res->n_eig && i < res->cap_nev; ++i) {
+      if (res->eig_re) res->eig_re[i] = r.eigenvalues[i].real();
+      if (res->eig_im) res->eig_im[i] = r.eigenvalues[i].imag();
+      if (res->residuals) res->residuals[i] = r.residuals[i];
+      if (res->converged_flags) res->converged_flags[i] = r.converged_flags[i] ? 1 : 0;
+    }
+    res->n_poly = r.poly ? r.poly->effective_degree() : 0;
+    res->poly_base_degree = r.poly ? r.poly->base_degree : 0;
+    for (int i = 0; i < res->n_poly && i < res->cap_roots; ++i) {
+      if (res->poly_re) res->poly_re[i] = r.poly->roots[i].real();
+      if (res->poly_im) res->poly_im[i] = r.poly->roots[i].imag();
+    }
+    res->n_inner = r.inner_poly ? r.inner_poly->effective_degree() : 0;
+    for (int i = 0; i < res->n_inner && i < res->cap_roots; ++i) {
+      if (res->inner_re) res->inner_re[i] = r.inner_poly->roots[i].real();
+      if (res->inner_im) res->inner_im[i] = r.inner_poly->roots[i].imag();
+    }
+    res->n_cycles = static_cast<int>(r.history.size());
+    for (int i = 0; i < res->n_cycles && i < res->cap_cycles; ++i) {
+      if (res->cycle_max_residual) res->cycle_max_residual[i] = r.history[i].max_residual;
+    }
+    res->converged = r.converged ? 1 : 0;
+    res->cycles = r.cycles;
+    res->composite_degree = r.composite_degree;
+    res->rtol = r.rtol;
+    res->max_err = r.max_err;
+    res->norm_estimate = r.norm_estimate;
+    res->cost = ppa_cost{r.cost.mvps, r.cost.dots, r.cost.vops, r.cost.nnzr, r.cost.wall_seconds};
+    res->t_total = r.timing.total;
+    res->t_setup = r.timing.setup;
+    res->t_extend = r.timing.extend;
+    res->t_check = r.timing.check;
+    res->t_restart = r.timing.restart;
+  });
+}
+
+}  // extern "C"

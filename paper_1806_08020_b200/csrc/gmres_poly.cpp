@@ -1,0 +1,375 @@
+// GMRES polynomial: host-side root management + device pi(A)v.
+// Reference: src/gmres_poly.cpp (line numbers cited per function).
+
+#include "ppa/gmres_poly.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <limits>
+#include <stdexcept>
+
+namespace ppa {
+
+namespace {
+
+using cplx = std::complex<double>;
+
+// src/gmres_poly.cpp:13-18: relative tolerance below which a root counts as real.
+constexpr double kRootImagTol = 1e-13;
+constexpr double kLnFloor = -690.0;  // ln(1e-300), src/gmres_poly.cpp:14
+
+bool poly_root_complex(const cplx& z) { return std::abs(z.imag()) > kRootImagTol * std::abs(z); }
+
+bool conj_match(const cplx& a, const cplx& b) {
+  return std::abs(a - std::conj(b)) <= 1e-10 * std::abs(b);
+}
+
+// First-occurrence distinct roots (src/gmres_poly.cpp:20-26).
+std::vector<cplx> unique_in_order(const std::vector<cplx>& roots) {
+  std::vector<cplx> u;
+  for (const cplx& r : roots)
+    if (std::find(u.begin(), u.end(), r) == u.end()) u.push_back(r);
+  return u;
+}
+
+void recount(PolyPrecond& p) {  // src/gmres_poly.cpp:28-34
+  p.multiplicity.resize(p.roots.size());
+  for (size_t i = 0; i < p.roots.size(); ++i)
+    p.multiplicity[i] = static_cast<int>(std::count(p.roots.begin(), p.roots.end(), p.roots[i]));
+}
+
+}  // namespace
+
+double PofReport::max_pof() const { return std::pow(10.0, max_log10_pof); }
+
+std::vector<cplx> leja_order(const std::vector<cplx>& roots) {
+  const int d = static_cast<int>(roots.size());
+  if (d == 0) throw std::invalid_argument("leja_order: empty root list");
+  for (const cplx& r : roots)
+    if (r == cplx(0.0, 0.0)) throw std::invalid_argument("leja_order: zero root");
+
+  std::vector<char> taken(d, 0);
+  std::vector<cplx> order;
+  order.reserve(d);
+  auto push = [&](int i) {
+    taken[i] = 1;
+    order.push_back(roots[i]);
+    if (!poly_root_complex(roots[i])) return;
+    // A chosen complex root drags its conjugate along (first match wins;
+    // an unmatched root is tolerated, src/gmres_poly.cpp:52-63).
+    for (int k = 0; k < d; ++k) {
+      if (!taken[k] && k != i &&
+          std::abs(roots[k] - std::conj(roots[i])) <= 1e-10 * std::abs(roots[i])) {
+        taken[k] = 1;
+        order.push_back(roots[k]);
+        return;
+      }
+    }
+  };
+
+  int first = 0;  // maximal modulus, first index on ties
+  for (int i = 1; i < d; ++i)
+    if (std::abs(roots[i]) > std::abs(roots[first])) first = i;
+  push(first);
+
+  while (static_cast<int>(order.size()) < d) {
+    int pick = -1;
+    double best = -std::numeric_limits<double>::infinity();
+    for (int i = 0; i < d; ++i) {
+      if (taken[i]) continue;
+      double score = 0.0;
+      for (const cplx& c : order) {
+        const double dist = std::abs(roots[i] - c);
+        score += dist > 0.0 ? std::log(dist) : kLnFloor;
+      }
+      if (score > best) {
+        best = score;
+        pick = i;
+      }
+    }
+    push(pick);
+  }
+  return order;
+}
+
+PolyPrecond build_gmres_poly(const LinearOperator& a, const double* b, int degree,
+                             CostRecord& rec) {
+  if (degree < 1) throw std::invalid_argument("build_gmres_poly: degree < 1");
+  if (b == nullptr) throw std::invalid_argument("build_gmres_poly: dimension mismatch");
+  // Uncounted, like the reference's b.norm() guard (src/gmres_poly.cpp:101).
+  if (current_context().nrm2_sync(b, a.dim()) == 0.0) {
+    throw std::invalid_argument("build_gmres_poly: zero starting vector");
+  }
+  const int d = std::min(degree, a.dim());
+  ArnoldiState st = arnoldi_init(b, a.dim(), d, rec);
+  arnoldi_extend(st, a, d, rec);
+
+  PolyPrecond p;
+  p.roots = leja_order(harmonic_ritz_values(st));
+  p.base_degree = static_cast<int>(p.roots.size());
+  p.truncated = p.base_degree < degree;
+  recount(p);
+  return p;
+}
+
+std::vector<PolyFactor> factor_plan(const PolyPrecond& p) {
+  std::vector<PolyFactor> plan;
+  const size_t nr = p.roots.size();
+  for (size_t i = 0; i < nr;) {
+    const cplx th = p.roots[i];
+    PolyFactor f;
+    if (!poly_root_complex(th)) {
+      f.c0 = -1.0 / th.real();  // src/gmres_poly.cpp:130 (imaginary part dropped)
+      i += 1;
+    } else {
+      if (i + 1 >= nr || std::abs(p.roots[i + 1] - std::conj(th)) > 1e-10 * std::abs(th)) {
+        throw std::logic_error("apply_poly: complex root without adjacent conjugate");
+      }
+      const double inv_mod2 = 1.0 / std::norm(th);  // src/gmres_poly.cpp:138-139
+      const double two_re_inv = 2.0 * th.real() * inv_mod2;
+      f.pair = true;
+      f.c0 = inv_mod2;
+      f.c1 = -two_re_inv;
+      i += 2;
+    }
+    plan.push_back(f);
+  }
+  return plan;
+}
+
+namespace {
+
+// Fused chain for a CSR base operator.  Each real factor is one SpMV launch
+// y = x + c0 (A x) (ping-pong between two buffers); a conjugate pair is a
+// plain SpMV t1 = A x followed by y = (x + c1 t1) + c0 (A t1), in place when
+// x is a scratch buffer.  The buffer of each launch is chosen backwards from
+// the end so the last launch writes `dst` directly; `complement_base`, when
+// set, is folded into that last launch (tau = I - pi, y = base - pi(A)x).
+void apply_poly_csr(const std::vector<PolyFactor>& plan, const CsrOperator& a, const double* v,
+                    double* dst, const double* complement_base, CostRecord& rec) {
+  Context& ctx = current_context();
+  const cudaStream_t st = ctx.stream();
+  const long long n = a.dim();
+  const int K = static_cast<int>(plan.size());
+  if (K == 0) {
+    if (complement_base) {
+      kern::sub(complement_base, v, dst, n, st);
+    } else {
+      kern::copy(v, dst, n, st);
+    }
+    return;
+  }
+  bool any_pair = false;
+  int reals = 0;
+  for (const PolyFactor& f : plan) {
+    any_pair |= f.pair;
+    reals += f.pair ? 0 : 1;
+  }
+  Scratch other(static_cast<size_t>(n));
+  Scratch t1buf(any_pair ? static_cast<size_t>(n) : 1);
+  // Backward buffer assignment: 0 -> dst, 1 -> other.
+  std::vector<int> target(K);
+  int need = 0;
+  for (int k = K - 1; k >= 0; --k) {
+    target[k] = need;
+    if (!plan[k].pair) need ^= 1;
+  }
+  double* bufs[2] = {dst, other.get()};
+  const double* cur = v;
+  for (int k = 0; k < K; ++k) {
+    const PolyFactor& f = plan[k];
+    double* out = bufs[target[k]];
+    kern::EpiArgs ep;
+    ep.base = (k == K - 1) ? complement_base : nullptr;
+    if (!f.pair) {
+      ep.mode = kern::Epi::real;
+      ep.c0 = f.c0;
+      kern::spmv(a.device(), cur, out, ep, st);
+      rec.mvps += 1;
+      rec.vops += 1;
+    } else {
+      kern::spmv(a.device(), cur, t1buf.get(), kern::EpiArgs{}, st);
+      ep.mode = kern::Epi::pair;
+      ep.c0 = f.c0;
+      ep.c1 = f.c1;
+      ep.o = cur;
+      kern::spmv(a.device(), t1buf.get(), out, ep, st);
+      rec.mvps += 2;
+      rec.vops += 2;
+    }
+    cur = out;
+  }
+  (void)reals;
+}
+
+// Reference operation sequence over an arbitrary operator.
+void apply_poly_generic(const std::vector<PolyFactor>& plan, const LinearOperator& a,
+                        const double* v, double* out, CostRecord& rec) {
+  const cudaStream_t st = current_context().stream();
+  const long long n = a.dim();
+  kern::copy(v, out, n, st);
+  bool any_pair = false;
+  for (const PolyFactor& f : plan) any_pair |= f.pair;
+  Scratch t1(static_cast<size_t>(n));
+  Scratch t2(any_pair ? static_cast<size_t>(n) : 1);
+  for (const PolyFactor& f : plan) {
+    if (!f.pair) {
+      a.apply(out, t1.get(), rec);
+      kern::axpy(f.c0, t1.get(), out, n, st);
+      rec.vops += 1;
+    } else {
+      a.apply(out, t1.get(), rec);
+      a.apply(t1.get(), t2.get(), rec);
+      kern::axpy(f.c1, t1.get(), out, n, st);
+      kern::axpy(f.c0, t2.get(), out, n, st);
+      rec.vops += 2;
+    }
+  }
+}
+
+}  // namespace
+
+void apply_poly(const PolyPrecond& p, const LinearOperator& a, const double* v, double* out,
+                CostRecord& rec) {
+  if (v == nullptr || out == nullptr) throw std::invalid_argument("apply_poly: dimension mismatch");
+  if (v == out) throw std::invalid_argument("apply_poly: input and output alias");
+  const std::vector<PolyFactor> plan = factor_plan(p);
+  if (const auto* csr = dynamic_cast<const CsrOperator*>(&a)) {
+    apply_poly_csr(plan, *csr, v, out, nullptr, rec);
+  } else {
+    apply_poly_generic(plan, a, v, out, rec);
+  }
+}
+
+std::complex<double> eval_poly(const PolyPrecond& p, std::complex<double> z) {
+  cplx val(1.0, 0.0);
+  for (const cplx& th : p.roots) val *= (1.0 - z / th);
+  return val;
+}
+
+PofReport compute_pof(const PolyPrecond& p) {
+  const std::vector<cplx> base = unique_in_order(p.roots);
+  const int d = static_cast<int>(base.size());
+  if (d < 2) throw std::invalid_argument("compute_pof: needs at least two roots");
+  PofReport rep;
+  rep.log10_pof.assign(d, 0.0);
+  rep.copies_needed.assign(d, 0);
+  rep.max_log10_pof = -std::numeric_limits<double>::infinity();
+  for (int j = 0; j < d; ++j) {
+    double lg = 0.0;
+    for (int i = 0; i < d; ++i) {
+      if (i == j) continue;
+      const double f = std::abs(1.0 - base[j] / base[i]);
+      lg += f > 0.0 ? std::log10(f) : kLnFloor;
+    }
+    rep.log10_pof[j] = lg;
+    rep.copies_needed[j] = lg > 4.0 ? static_cast<int>(std::ceil((lg - 4.0) / 14.0)) : 0;
+    rep.total_copies += rep.copies_needed[j];
+    rep.max_log10_pof = std::max(rep.max_log10_pof, lg);
+  }
+  return rep;
+}
+
+PolyPrecond add_stability_roots(const PolyPrecond& p, int max_copies_per_root) {
+  const PofReport rep = compute_pof(p);
+  const std::vector<cplx> base = unique_in_order(p.roots);
+  PolyPrecond out = p;
+  std::vector<char> done(base.size(), 0);
+  for (size_t j = 0; j < base.size(); ++j) {
+    if (done[j]) continue;
+    done[j] = 1;
+    const int copies = std::min(rep.copies_needed[j], max_copies_per_root);
+    if (copies <= 0) continue;
+    const cplx th = base[j];
+    std::vector<cplx> group{th};
+    if (poly_root_complex(th)) {
+      for (size_t k = 0; k < base.size(); ++k) {
+        if (!done[k] && std::abs(base[k] - std::conj(th)) <= 1e-10 * std::abs(th)) {
+          done[k] = 1;
+          group.push_back(base[k]);
+          break;
+        }
+      }
+    }
+    // src/gmres_poly.cpp:207-222: first copy appended; copies r = 1..c-1 at
+    // jpos + round(r (L - jpos) / c), inserted from the back.
+    const long long L = static_cast<long long>(out.roots.size());
+    const long long jpos = std::find(out.roots.begin(), out.roots.end(), th) - out.roots.begin();
+    std::vector<long long> at;
+    for (int r = 1; r < copies; ++r)
+      at.push_back(jpos + static_cast<long long>(
+                              std::llround(double(r) * double(L - jpos) / double(copies))));
+    std::sort(at.begin(), at.end(), std::greater<long long>());
+    out.roots.insert(out.roots.end(), group.begin(), group.end());
+    for (long long pos : at) out.roots.insert(out.roots.begin() + pos, group.begin(), group.end());
+  }
+  recount(out);
+  return out;
+}
+
+namespace {
+
+class PolyOperator final : public LinearOperator {
+ public:
+  PolyOperator(OperatorPtr a, PolyPrecond p, bool complement)
+      : a_(std::move(a)), p_(std::move(p)), complement_(complement), plan_(factor_plan(p_)) {}
+  int dim() const override { return a_->dim(); }
+  OperatorKind kind() const override {
+    return complement_ ? OperatorKind::composite : OperatorKind::poly;
+  }
+  int mvps_per_apply() const override { return p_.effective_degree() * a_->mvps_per_apply(); }
+  double nnzr() const override { return a_->nnzr(); }
+
+  void apply(const double* x, double* y, CostRecord& rec) const override {
+    if (x == y) throw std::invalid_argument("PolyOperator::apply: x and y alias");
+    const auto* csr = dynamic_cast<const CsrOperator*>(a_.get());
+    if (csr) {
+      // The complement y = x - w folds into the last fused launch.
+      apply_poly_csr(plan_, *csr, x, y, complement_ ? x : nullptr, rec);
+      if (complement_) rec.vops += 1;
+      return;
+    }
+    if (!complement_) {
+      apply_poly_generic(plan_, *a_, x, y, rec);
+      return;
+    }
+    Scratch w(static_cast<size_t>(dim()));
+    apply_poly_generic(plan_, *a_, x, w.get(), rec);
+    kern::sub(x, w.get(), y, dim(), current_context().stream());
+    rec.vops += 1;
+  }
+
+ private:
+  OperatorPtr a_;
+  PolyPrecond p_;
+  bool complement_;
+  std::vector<PolyFactor> plan_;
+};
+
+}  // namespace
+
+OperatorPtr make_poly_operator(OperatorPtr a, PolyPrecond p) {
+  return std::make_shared<PolyOperator>(std::move(a), std::move(p), false);
+}
+
+OperatorPtr make_poly_complement_operator(OperatorPtr a, PolyPrecond p) {
+  return std::make_shared<PolyOperator>(std::move(a), std::move(p), true);
+}
+
+std::string poly_dump_csv(const PolyPrecond& p) {
+  std::string s = "index,re,im,multiplicity,pof\n";
+  const std::vector<cplx> base = unique_in_order(p.roots);
+  std::vector<double> lg(base.size(), 0.0);
+  if (base.size() >= 2) lg = compute_pof(p).log10_pof;
+  char line[160];
+  for (size_t i = 0; i < base.size(); ++i) {
+    const int mult = static_cast<int>(std::count(p.roots.begin(), p.roots.end(), base[i]));
+    std::snprintf(line, sizeof(line), "%zu,%.17g,%.17g,%d,%.17g\n", i, base[i].real(),
+                  base[i].imag(), mult, std::pow(10.0, lg[i]));
+    s += line;
+  }
+  return s;
+}
+
+}  // namespace ppa

@@ -1,0 +1,247 @@
+// Streaming CSR SpMV with the polynomial-factor epilogues fused in.
+//
+// Replaces CsrMatrix::multiply (src/operators.cpp:39-48) and the axpys of
+// apply_poly (src/gmres_poly.cpp:129-143) / PolyOperator complement
+// (src/gmres_poly.cpp:306-308).
+//
+// Layout: plain CSR in HBM (int32 row_ptr/col_idx, fp64 values), plus a
+// host-built row-block partition (<= 256 rows and <= 2048 nonzeros each).
+// One 256-thread CTA per row block:
+//   phase 1  the block's contiguous slice of (col_idx, values) is streamed
+//            with 8-/16-byte vector loads that bypass L1 (every byte of the
+//            matrix is read once per SpMV), x is gathered through the
+//            read-only path (x stays L2-resident: 33 MB at config 3), and
+//            the products are staged in shared memory;
+//   phase 2  thread t sums row t's products sequentially - the same
+//            left-to-right order, without FMA contraction, as the reference's
+//            scalar loop, so the SpMV is bit-identical to the CPU oracle -
+//            and applies the factor epilogue with one coalesced store.
+// A row longer than 2048 nonzeros gets a block of its own and a block-wide
+// reduction (not bit-identical; no BASELINE config has such rows).
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "ppa/kernels.hpp"
+
+namespace ppa {
+namespace kern {
+namespace {
+
+constexpr int T = kSpmvThreads;
+constexpr int MAXR = kSpmvMaxRows;
+constexpr int MAXNNZ = kSpmvMaxNnz;
+// Pairs a thread may own: the slice [p0 & ~1, p1) has <= MAXNNZ + 1 elements.
+constexpr int KPAIRS = ((MAXNNZ + 2) / 2 + T - 1) / T;
+
+template <int MODE, bool COMPL>
+__device__ __forceinline__ double epilogue(int r, double s, const double* __restrict__ x,
+                                           double c0, double c1, const double* o,
+                                           const double* base) {
+  double z;
+  if (MODE == 0) {
+    z = s;
+  } else if (MODE == 1) {
+    z = __dadd_rn(__ldg(x + r), __dmul_rn(c0, s));
+  } else {
+    z = __dadd_rn(__dadd_rn(o[r], __dmul_rn(c1, __ldg(x + r))), __dmul_rn(c0, s));
+  }
+  if (COMPL) z = __dsub_rn(base[r], z);
+  return z;
+}
+
+template <int MODE, bool COMPL>
+__global__ void __launch_bounds__(T) k_spmv_rowblock(
+    const int* __restrict__ row_ptr, const int* __restrict__ col_idx,
+    const double* __restrict__ vals, const int* __restrict__ blk_row,
+    const double* __restrict__ x, double* y, double c0, double c1, const double* o,
+    const double* base) {
+  __shared__ __align__(16) double prod[MAXNNZ + 2];
+  __shared__ int rp[MAXR + 1];
+  __shared__ double s_warp[T / 32];
+
+  const int r0 = blk_row[blockIdx.x];
+  const int r1 = blk_row[blockIdx.x + 1];
+  const int nr = r1 - r0;
+  for (int t = threadIdx.x; t <= nr; t += T) rp[t] = row_ptr[r0 + t];
+  __syncthreads();
+  const int p0 = rp[0];
+  const int p1 = rp[nr];
+
+  if (p1 - p0 <= MAXNNZ) {
+    const int q0 = p0 & ~1;
+    const int npairs = (p1 - q0 + 1) >> 1;
+    int2 c[KPAIRS];
+    double2 v[KPAIRS];
+#pragma unroll
+    for (int k = 0; k < KPAIRS; ++k) {
+      const int pi = threadIdx.x + k * T;
+      if (pi < npairs) {
+        c[k] = dev::ld_stream(reinterpret_cast<const int2*>(col_idx + q0) + pi);
+        v[k] = dev::ld_stream(reinterpret_cast<const double2*>(vals + q0) + pi);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < KPAIRS; ++k) {
+      const int pi = threadIdx.x + k * T;
+      if (pi < npairs) {
+        const int q = q0 + 2 * pi;
+        double a = 0.0, b = 0.0;
+        if (q >= p0) a = __dmul_rn(v[k].x, __ldg(x + c[k].x));
+        if (q + 1 < p1) b = __dmul_rn(v[k].y, __ldg(x + c[k].y));
+        reinterpret_cast<double2*>(prod)[pi] = make_double2(a, b);
+      }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < nr; t += T) {
+      const int a = rp[t] - q0;
+      const int b = rp[t + 1] - q0;
+      double s = 0.0;
+      for (int p = a; p < b; ++p) s = __dadd_rn(s, prod[p]);
+      y[r0 + t] = epilogue<MODE, COMPL>(r0 + t, s, x, c0, c1, o, base);
+    }
+  } else {
+    // One long row (nr == 1): block-strided partial sums + fixed-order tree.
+    double s = 0.0;
+    for (int p = p0 + threadIdx.x; p < p1; p += T) {
+      s = __dadd_rn(s, __dmul_rn(dev::ld_stream(vals + p), __ldg(x + col_idx[p])));
+    }
+    s = dev::warp_sum(s);
+    if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = 0.0;
+#pragma unroll
+      for (int w = 0; w < T / 32; ++w) tot += s_warp[w];
+      y[r0] = epilogue<MODE, COMPL>(r0, tot, x, c0, c1, o, base);
+    }
+  }
+}
+
+// SELL-32: one warp per 32-row slice.  Lane l owns row 32s+l; entry k of
+// the slice is one coalesced 128 B (col) + 256 B (value) request per warp,
+// and for stencil matrices the x gathers of a slice column are contiguous
+// too.  No shared memory and no barriers: every warp is independent, so the
+// SM keeps many more loads in flight than the row-block kernel.  Padding
+// entries (col < 0) are skipped, so each row is still summed left to right
+// with the CSR's own column order (bit-identical to the CPU loop).
+constexpr int SELL_WARPS = 8;
+constexpr int SELL_UNROLL = 8;
+
+template <int MODE, bool COMPL>
+__global__ void __launch_bounds__(SELL_WARPS * 32) k_spmv_sell32(
+    const long long* __restrict__ slice_ptr, const int* __restrict__ scol,
+    const double* __restrict__ sval, int n, int nslices, const double* __restrict__ x, double* y,
+    double c0, double c1, const double* o, const double* base) {
+  const int lane = threadIdx.x & 31;
+  const int s = blockIdx.x * SELL_WARPS + (threadIdx.x >> 5);
+  if (s >= nslices) return;
+  const long long b0 = slice_ptr[s];
+  const int width = static_cast<int>((slice_ptr[s + 1] - b0) >> 5);
+  const int* cp = scol + b0 + lane;
+  const double* vp = sval + b0 + lane;
+  double sum = 0.0;
+  for (int k0 = 0; k0 < width; k0 += SELL_UNROLL) {
+    int c[SELL_UNROLL];
+    double v[SELL_UNROLL];
+#pragma unroll
+    for (int u = 0; u < SELL_UNROLL; ++u) {
+      if (k0 + u < width) {
+        c[u] = __ldcs(cp + (k0 + u) * 32);
+        v[u] = __ldcs(vp + (k0 + u) * 32);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < SELL_UNROLL; ++u) {
+      if (k0 + u < width && c[u] >= 0) sum = __dadd_rn(sum, __dmul_rn(v[u], __ldg(x + c[u])));
+    }
+  }
+  const int r = s * 32 + lane;
+  if (r < n) y[r] = epilogue<MODE, COMPL>(r, sum, x, c0, c1, o, base);
+}
+
+template <int MODE, bool COMPL>
+void launch(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep, cudaStream_t st) {
+  if (a.sell_val) {
+    const int grid = (a.nslices + SELL_WARPS - 1) / SELL_WARPS;
+    k_spmv_sell32<MODE, COMPL><<<grid, SELL_WARPS * 32, 0, st>>>(
+        a.slice_ptr, a.sell_col, a.sell_val, a.n, a.nslices, x, y, ep.c0, ep.c1, ep.o, ep.base);
+    return;
+  }
+  k_spmv_rowblock<MODE, COMPL><<<a.nblocks, T, 0, st>>>(a.row_ptr, a.col_idx, a.values,
+                                                       a.blk_row, x, y, ep.c0, ep.c1, ep.o,
+                                                       ep.base);
+}
+
+}  // namespace
+
+void spmv(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep, cudaStream_t st) {
+  if (a.n == 0 || a.nblocks == 0) return;
+  const bool compl_ = ep.base != nullptr;
+  switch (ep.mode) {
+    case Epi::plain:
+      compl_ ? launch<0, true>(a, x, y, ep, st) : launch<0, false>(a, x, y, ep, st);
+      break;
+    case Epi::real:
+      compl_ ? launch<1, true>(a, x, y, ep, st) : launch<1, false>(a, x, y, ep, st);
+      break;
+    case Epi::pair:
+      compl_ ? launch<2, true>(a, x, y, ep, st) : launch<2, false>(a, x, y, ep, st);
+      break;
+  }
+  PPA_CUDA(cudaGetLastError());
+}
+
+bool build_sell32(const int* row_ptr, const int* col_idx, const double* values, int n,
+                  std::vector<long long>& slice_ptr, std::vector<int>& cols,
+                  std::vector<double>& vals) {
+  const int ns = (n + 31) / 32;
+  slice_ptr.assign(static_cast<size_t>(ns) + 1, 0);
+  long long total = 0;
+  for (int s = 0; s < ns; ++s) {
+    int w = 0;
+    for (int r = s * 32; r < std::min(n, s * 32 + 32); ++r) w = std::max(w, row_ptr[r + 1] - row_ptr[r]);
+    total += 32LL * w;
+    slice_ptr[s + 1] = total;
+  }
+  const long long nnz = row_ptr[n];
+  if (static_cast<double>(total) > kSellMaxPadding * static_cast<double>(nnz) + 32.0 * 64) {
+    slice_ptr.clear();
+    return false;
+  }
+  cols.assign(static_cast<size_t>(total), -1);
+  vals.assign(static_cast<size_t>(total), 0.0);
+  for (int s = 0; s < ns; ++s) {
+    const long long b0 = slice_ptr[s];
+    for (int l = 0; l < 32; ++l) {
+      const int r = s * 32 + l;
+      if (r >= n) break;
+      for (int p = row_ptr[r], k = 0; p < row_ptr[r + 1]; ++p, ++k) {
+        cols[b0 + 32LL * k + l] = col_idx[p];
+        vals[b0 + 32LL * k + l] = values[p];
+      }
+    }
+  }
+  return true;
+}
+
+void build_row_blocks(const int* row_ptr, int n, int max_rows, int max_nnz,
+                      std::vector<int>& blk_row) {
+  blk_row.clear();
+  blk_row.reserve(static_cast<size_t>(n) / 64 + 2);
+  blk_row.push_back(0);
+  int r = 0;
+  while (r < n) {
+    const int start = r;
+    const int base = row_ptr[start];
+    int e = start;
+    while (e < n && e - start < max_rows && row_ptr[e + 1] - base <= max_nnz) ++e;
+    if (e == start) e = start + 1;  // a single row longer than max_nnz
+    blk_row.push_back(e);
+    r = e;
+  }
+}
+
+}  // namespace kern
+}  // namespace ppa

@@ -1,0 +1,365 @@
+// Operators and matrix generators (reference: src/operators.cpp).
+
+#include "ppa/operators.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <stdexcept>
+
+#include "ppa/rng.hpp"
+
+namespace ppa {
+
+void CsrMatrix::validate() const {
+  if (n < 0) throw std::invalid_argument("CsrMatrix: negative dimension");
+  if (row_ptr.size() != static_cast<size_t>(n) + 1) {
+    throw std::invalid_argument("CsrMatrix: row_ptr length must be n+1");
+  }
+  if (row_ptr.front() != 0 || row_ptr.back() != nnz()) {
+    throw std::invalid_argument("CsrMatrix: row_ptr endpoints invalid");
+  }
+  if (col_idx.size() != values.size()) {
+    throw std::invalid_argument("CsrMatrix: col_idx/values size mismatch");
+  }
+  for (int i = 0; i < n; ++i) {
+    const int b = row_ptr[i], e = row_ptr[i + 1];
+    if (e < b) throw std::invalid_argument("CsrMatrix: row_ptr not nondecreasing");
+    for (int p = b; p < e; ++p) {
+      const int c = col_idx[p];
+      if (c < 0 || c >= n) throw std::invalid_argument("CsrMatrix: column index out of range");
+      if (p > b && c <= col_idx[p - 1]) {
+        throw std::invalid_argument("CsrMatrix: columns not strictly increasing within a row");
+      }
+    }
+  }
+}
+
+CsrMatrix CsrMatrix::from_triplets(int n, std::vector<std::tuple<int, int, double>> t) {
+  for (const auto& e : t) {
+    const int i = std::get<0>(e), j = std::get<1>(e);
+    if (i < 0 || i >= n || j < 0 || j >= n) {
+      throw std::invalid_argument("from_triplets: index out of range");
+    }
+  }
+  std::stable_sort(t.begin(), t.end(), [](const auto& a, const auto& b) {
+    if (std::get<0>(a) != std::get<0>(b)) return std::get<0>(a) < std::get<0>(b);
+    return std::get<1>(a) < std::get<1>(b);
+  });
+  CsrMatrix m;
+  m.n = n;
+  m.row_ptr.assign(static_cast<size_t>(n) + 1, 0);
+  m.col_idx.reserve(t.size());
+  m.values.reserve(t.size());
+  for (size_t p = 0; p < t.size(); ++p) {
+    const int i = std::get<0>(t[p]), j = std::get<1>(t[p]);
+    if (p > 0 && std::get<0>(t[p - 1]) == i && std::get<1>(t[p - 1]) == j) {
+      m.values.back() += std::get<2>(t[p]);
+      continue;
+    }
+    m.col_idx.push_back(j);
+    m.values.push_back(std::get<2>(t[p]));
+    ++m.row_ptr[static_cast<size_t>(i) + 1];
+  }
+  for (int i = 0; i < n; ++i) m.row_ptr[i + 1] += m.row_ptr[i];
+  m.validate();
+  return m;
+}
+
+// ------------------------------------------------------------ operator --
+
+CsrOperator::CsrOperator(const CsrMatrix& m, OperatorKind kind, std::vector<double> diag)
+    : kind_(kind), diag_(std::move(diag)) {
+  m.validate();
+  n_ = m.n;
+  nnz_ = m.nnz();
+  nnzr_ = m.nnzr();
+  std::vector<int> blk;
+  kern::build_row_blocks(m.row_ptr.data(), m.n, kern::kSpmvMaxRows, kern::kSpmvMaxNnz, blk);
+  const size_t nz = static_cast<size_t>(nnz_);
+  const size_t padded = nz + kern::kSpmvPad;
+  row_ptr_.resize(static_cast<size_t>(n_) + 1);
+  col_idx_.resize(padded);
+  values_.resize(padded);
+  blk_row_.resize(blk.size());
+  PPA_CUDA(cudaMemcpy(row_ptr_.get(), m.row_ptr.data(), (n_ + 1) * sizeof(int),
+                      cudaMemcpyHostToDevice));
+  PPA_CUDA(cudaMemset(col_idx_.get(), 0, padded * sizeof(int)));
+  PPA_CUDA(cudaMemset(values_.get(), 0, padded * sizeof(double)));
+  if (nz) {
+    PPA_CUDA(cudaMemcpy(col_idx_.get(), m.col_idx.data(), nz * sizeof(int),
+                        cudaMemcpyHostToDevice));
+    PPA_CUDA(cudaMemcpy(values_.get(), m.values.data(), nz * sizeof(double),
+                        cudaMemcpyHostToDevice));
+  }
+  PPA_CUDA(cudaMemcpy(blk_row_.get(), blk.data(), blk.size() * sizeof(int),
+                      cudaMemcpyHostToDevice));
+  dev_.n = n_;
+  dev_.nnz = nnz_;
+  dev_.row_ptr = row_ptr_.get();
+  dev_.col_idx = col_idx_.get();
+  dev_.values = values_.get();
+  dev_.blk_row = blk_row_.get();
+  dev_.nblocks = static_cast<int>(blk.size()) - 1;
+
+  std::vector<long long> sp;
+  std::vector<int> sc;
+  std::vector<double> sv;
+  if (!std::getenv("PPA_DISABLE_SELL") &&
+      kern::build_sell32(m.row_ptr.data(), m.col_idx.data(), m.values.data(), n_, sp, sc, sv)) {
+    slice_ptr_.resize(sp.size());
+    sell_col_.resize(sc.size() + 32);
+    sell_val_.resize(sv.size() + 32);
+    PPA_CUDA(cudaMemcpy(slice_ptr_.get(), sp.data(), sp.size() * sizeof(long long),
+                        cudaMemcpyHostToDevice));
+    if (!sc.empty()) {
+      PPA_CUDA(cudaMemcpy(sell_col_.get(), sc.data(), sc.size() * sizeof(int),
+                          cudaMemcpyHostToDevice));
+      PPA_CUDA(cudaMemcpy(sell_val_.get(), sv.data(), sv.size() * sizeof(double),
+                          cudaMemcpyHostToDevice));
+    }
+    dev_.slice_ptr = slice_ptr_.get();
+    dev_.sell_col = sell_col_.get();
+    dev_.sell_val = sell_val_.get();
+    dev_.nslices = static_cast<int>(sp.size()) - 1;
+    dev_.sell_entries = sp.back();
+  }
+}
+
+void CsrOperator::apply(const double* x, double* y, CostRecord& rec) const {
+  if (x == y) throw std::invalid_argument("CsrOperator::apply: x and y alias");
+  ++rec.mvps;
+  kern::spmv(dev_, x, y, kern::EpiArgs{}, current_context().stream());
+}
+
+OperatorPtr make_csr_operator(const CsrMatrix& matrix) {
+  return std::make_shared<CsrOperator>(matrix);
+}
+
+OperatorPtr make_diagonal(std::vector<double> d) {
+  if (d.empty()) throw std::invalid_argument("make_diagonal: empty diagonal");
+  CsrMatrix m;
+  m.n = static_cast<int>(d.size());
+  m.row_ptr.resize(d.size() + 1);
+  m.col_idx.resize(d.size());
+  m.values = d;
+  for (int i = 0; i <= m.n; ++i) m.row_ptr[i] = i;
+  for (int i = 0; i < m.n; ++i) m.col_idx[i] = i;
+  return std::make_shared<CsrOperator>(m, OperatorKind::diagonal, std::move(d));
+}
+
+// ---------------------------------------------------------- generators --
+
+CsrMatrix make_convection_diffusion(int grid_n) {
+  if (grid_n < 2) throw std::invalid_argument("make_convection_diffusion: grid_n < 2");
+  const int n = grid_n * grid_n;
+  const double h = 1.0 / (grid_n + 1);
+  CsrMatrix m;
+  m.n = n;
+  m.row_ptr.assign(static_cast<size_t>(n) + 1, 0);
+  m.col_idx.reserve(5ull * n);
+  m.values.reserve(5ull * n);
+  int pos = 0;
+  for (int iy = 0; iy < grid_n; ++iy) {
+    const double y = (iy + 1) * h;
+    const bool lower = y <= 0.5 + 1e-14;
+    const double eps = lower ? 1.0 : 100.0;
+    const double cc = lower ? 20.0 : 2000.0;
+    const double center = 4.0 * eps / (h * h);
+    const double east = -eps / (h * h) + cc / (2.0 * h);
+    const double west = -eps / (h * h) - cc / (2.0 * h);
+    const double ns = -eps / (h * h);
+    for (int ix = 0; ix < grid_n; ++ix) {
+      const int row = iy * grid_n + ix;
+      auto put = [&](int col, double v) {
+        m.col_idx.push_back(col);
+        m.values.push_back(v);
+        ++pos;
+      };
+      if (iy > 0) put(row - grid_n, ns);
+      if (ix > 0) put(row - 1, west);
+      put(row, center);
+      if (ix + 1 < grid_n) put(row + 1, east);
+      if (iy + 1 < grid_n) put(row + grid_n, ns);
+      m.row_ptr[static_cast<size_t>(row) + 1] = pos;
+    }
+  }
+  m.validate();
+  return m;
+}
+
+CsrMatrix make_convection_diffusion_const(int grid_n, double peclet) {
+  if (grid_n < 2) throw std::invalid_argument("make_convection_diffusion_const: grid_n < 2");
+  const long long nl = static_cast<long long>(grid_n) * grid_n;
+  if (nl > 2147483647LL) throw std::invalid_argument("make_convection_diffusion_const: too large");
+  const int n = static_cast<int>(nl);
+  const double h = 1.0 / (grid_n + 1);
+  const double beta = 2.0 * peclet / h;
+  const double center = 4.0 / (h * h);
+  const double east = -1.0 / (h * h) + beta / (2.0 * h);
+  const double west = -1.0 / (h * h) - beta / (2.0 * h);
+  const double ns = -1.0 / (h * h);
+  CsrMatrix m;
+  m.n = n;
+  m.row_ptr.assign(static_cast<size_t>(n) + 1, 0);
+  const size_t nnz = 5ull * n - 4ull * grid_n;
+  m.col_idx.resize(nnz);
+  m.values.resize(nnz);
+  size_t pos = 0;
+  for (int iy = 0; iy < grid_n; ++iy) {
+    for (int ix = 0; ix < grid_n; ++ix) {
+      const int row = iy * grid_n + ix;
+      auto put = [&](int col, double v) {
+        m.col_idx[pos] = col;
+        m.values[pos] = v;
+        ++pos;
+      };
+      if (iy > 0) put(row - grid_n, ns);
+      if (ix > 0) put(row - 1, west);
+      put(row, center);
+      if (ix + 1 < grid_n) put(row + 1, east);
+      if (iy + 1 < grid_n) put(row + grid_n, ns);
+      m.row_ptr[static_cast<size_t>(row) + 1] = static_cast<int>(pos);
+    }
+  }
+  m.validate();
+  return m;
+}
+
+CsrMatrix make_laplacian_3d(int grid_n) {
+  if (grid_n < 2) throw std::invalid_argument("make_laplacian_3d: grid_n < 2");
+  const long long nl = 1LL * grid_n * grid_n * grid_n;
+  if (nl > 2147483647LL / 7) throw std::invalid_argument("make_laplacian_3d: too large");
+  const int N = grid_n;
+  const int n = static_cast<int>(nl);
+  const double h = 1.0 / (grid_n + 1);
+  const double center = 6.0 / (h * h);
+  const double off = -1.0 / (h * h);
+  CsrMatrix m;
+  m.n = n;
+  m.row_ptr.assign(static_cast<size_t>(n) + 1, 0);
+  const size_t nnz = 7ull * n - 6ull * N * N;
+  m.col_idx.resize(nnz);
+  m.values.resize(nnz);
+  size_t pos = 0;
+  const int NN = N * N;
+  for (int iz = 0; iz < N; ++iz)
+    for (int iy = 0; iy < N; ++iy)
+      for (int ix = 0; ix < N; ++ix) {
+        const int row = (iz * N + iy) * N + ix;
+        auto put = [&](int col, double v) {
+          m.col_idx[pos] = col;
+          m.values[pos] = v;
+          ++pos;
+        };
+        if (iz > 0) put(row - NN, off);
+        if (iy > 0) put(row - N, off);
+        if (ix > 0) put(row - 1, off);
+        put(row, center);
+        if (ix + 1 < N) put(row + 1, off);
+        if (iy + 1 < N) put(row + N, off);
+        if (iz + 1 < N) put(row + NN, off);
+        m.row_ptr[static_cast<size_t>(row) + 1] = static_cast<int>(pos);
+      }
+  m.validate();
+  return m;
+}
+
+CsrMatrix make_bidiagonal(int n) {
+  if (n < 1) throw std::invalid_argument("make_bidiagonal: n < 1");
+  CsrMatrix m;
+  m.n = n;
+  m.row_ptr.resize(static_cast<size_t>(n) + 1);
+  m.col_idx.reserve(2ull * n);
+  m.values.reserve(2ull * n);
+  m.row_ptr[0] = 0;
+  for (int i = 0; i < n; ++i) {
+    m.col_idx.push_back(i);
+    m.values.push_back(static_cast<double>(i + 1));
+    if (i + 1 < n) {
+      m.col_idx.push_back(i + 1);
+      m.values.push_back(1.0);
+    }
+    m.row_ptr[i + 1] = static_cast<int>(m.col_idx.size());
+  }
+  m.validate();
+  return m;
+}
+
+CsrMatrix make_random_poisson(int n, double lambda, unsigned long long seed) {
+  if (n < 2) throw std::invalid_argument("make_random_poisson: n < 2");
+  const uint64_t mkey = rng::key(seed, rng::kMatrix);
+  const double elim = std::exp(-lambda);
+  CsrMatrix m;
+  m.n = n;
+  m.row_ptr.assign(static_cast<size_t>(n) + 1, 0);
+  m.col_idx.reserve(static_cast<size_t>(n) * static_cast<size_t>(lambda + 2));
+  m.values.reserve(m.col_idx.capacity());
+  std::vector<std::pair<int, double>> row;
+  for (int i = 0; i < n; ++i) {
+    rng::RowStream rs(mkey, static_cast<uint64_t>(i));
+    // Knuth's multiplicative Poisson sampler.
+    int L = 0;
+    double p = 1.0;
+    do {
+      p *= rs.uniform();
+      ++L;
+    } while (p > elim);
+    L = std::max(1, L - 1);
+    row.clear();
+    row.emplace_back(i, (static_cast<double>(i) + 1.0) / static_cast<double>(n) * 10.0);
+    for (int e = 0; e < L; ++e) {
+      int j;
+      do {
+        j = static_cast<int>(rs.uniform() * n);
+        if (j >= n) j = n - 1;
+      } while (j == i);
+      row.emplace_back(j, rs.normal() / 8.0);
+    }
+    std::stable_sort(row.begin(), row.end(),
+                     [](const auto& a, const auto& b) { return a.first < b.first; });
+    int last = -1;
+    for (const auto& e : row) {
+      if (e.first == last) {
+        m.values.back() += e.second;
+      } else {
+        m.col_idx.push_back(e.first);
+        m.values.push_back(e.second);
+        last = e.first;
+      }
+    }
+    m.row_ptr[static_cast<size_t>(i) + 1] = static_cast<int>(m.col_idx.size());
+  }
+  m.validate();
+  return m;
+}
+
+CsrMatrix make_config_matrix(int config) {
+  switch (config) {
+    case 1: return make_bidiagonal(5000);
+    case 2: return make_convection_diffusion_const(1000, 0.5);
+    case 3: return make_laplacian_3d(160);
+    case 4: return make_random_poisson(2000000, 16.0, 4);
+    case 5: return make_convection_diffusion_const(2048, 0.5);
+    default: throw std::invalid_argument("make_config_matrix: config must be 1..5");
+  }
+}
+
+unsigned long long csr_fingerprint(const CsrMatrix& m) {
+  uint64_t h = 0xcbf29ce484222325ull;
+  auto eat = [&](const void* p, size_t bytes) {
+    const unsigned char* c = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < bytes; ++i) {
+      h ^= c[i];
+      h *= 0x100000001b3ull;
+    }
+  };
+  eat(&m.n, sizeof(int));
+  eat(m.row_ptr.data(), m.row_ptr.size() * sizeof(int));
+  eat(m.col_idx.data(), m.col_idx.size() * sizeof(int));
+  eat(m.values.data(), m.values.size() * sizeof(double));
+  return h;
+}
+
+}  // namespace ppa

@@ -1,0 +1,135 @@
+#pragma once
+// Host-side launchers for the sm_100a kernels (csrc/kernels/*.cu).
+// Every launcher is asynchronous on the given stream; none synchronises.
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "ppa/device.hpp"
+
+namespace ppa {
+namespace kern {
+
+/// Device copy of a CsrMatrix plus the row-block partition used by the
+/// streaming SpMV.  Pointers are device pointers.
+struct CsrDevice {
+  int n = 0;
+  long long nnz = 0;
+  const int* row_ptr = nullptr;  // [n+1]
+  const int* col_idx = nullptr;  // [nnz (+pad)]
+  const double* values = nullptr;
+  const int* blk_row = nullptr;  // [nblocks+1] first row of each row block
+  int nblocks = 0;
+  // Sliced ELL (SELL-32) copy: slice s holds rows 32s..32s+31; entry k of
+  // lane l sits at slice_ptr[s] + 32k + l; padding has col = -1.  Used when
+  // the padding overhead is small (regular rows); nullptr otherwise.
+  const long long* slice_ptr = nullptr;  // [nslices+1]
+  const int* sell_col = nullptr;
+  const double* sell_val = nullptr;
+  int nslices = 0;
+  long long sell_entries = 0;
+};
+
+/// SELL-32 is used when its padded entry count is at most this factor of nnz.
+constexpr double kSellMaxPadding = 1.15;
+
+/// Host-side SELL-32 construction from CSR (returns false when padding
+/// exceeds kSellMaxPadding).
+bool build_sell32(const int* row_ptr, const int* col_idx, const double* values, int n,
+                  std::vector<long long>& slice_ptr, std::vector<int>& cols,
+                  std::vector<double>& vals);
+
+/// Row-block capacities of the streaming SpMV (must match spmv.cu).
+constexpr int kSpmvThreads = 256;
+constexpr int kSpmvMaxRows = 256;
+constexpr int kSpmvMaxNnz = 2048;
+/// Elements of padding after col_idx/values so vector loads never run off
+/// the allocation.
+constexpr int kSpmvPad = 8;
+
+/// Fused epilogues of the SpMV (s = (A x)[i]).  Each reproduces the
+/// reference's operation order (src/gmres_poly.cpp:129-143) without FMA
+/// contraction so the result is bit-identical to the scalar CPU loop:
+///   plain : y = s
+///   real  : y = x[i] + (c0 * s)                 real root, c0 = -1/theta
+///   pair  : y = (o[i] + (c1 * x[i])) + (c0 * s) conjugate pair, second
+///           product; x = t1, c1 = -2Re(theta)/|theta|^2, c0 = 1/|theta|^2
+/// Optionally, complement: y = base[i] - z (tau = I - pi, src/gmres_poly.cpp:306-308).
+enum class Epi : int { plain = 0, real = 1, pair = 2 };
+
+struct EpiArgs {
+  Epi mode = Epi::plain;
+  double c0 = 0.0;
+  double c1 = 0.0;
+  const double* o = nullptr;     // pair: running product (may alias y)
+  const double* base = nullptr;  // complement base (nullptr: no complement)
+};
+
+void spmv(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep, cudaStream_t st);
+
+/// Builds the row-block partition on the host from row_ptr.
+/// Returns the first row of each block (size nblocks+1).
+void build_row_blocks(const int* row_ptr_host, int n, int max_rows, int max_nnz,
+                      std::vector<int>& blk_row);
+
+// ---------------------------------------------------------------- blas1 ---
+void copy(const double* x, double* y, long long n, cudaStream_t st);
+void axpy(double a, const double* x, double* y, long long n, cudaStream_t st);  // y += a*x
+void scale(double* x, double a, long long n, cudaStream_t st);                  // x *= a
+void div_scale(double* x, const double* dev_a, long long n, cudaStream_t st);   // x /= *dev_a
+void div_value(double* x, double a, long long n, cudaStream_t st);               // x /= a
+void sub(const double* x, const double* w, double* y, long long n, cudaStream_t st);  // y = x - w
+void fill(double* x, double v, long long n, cudaStream_t st);
+
+/// out[0] = x . y  (deterministic two-stage reduction; device result)
+void dot(const double* x, const double* y, long long n, double* out, ReduceWorkspace& ws,
+         int sm_count, cudaStream_t st);
+/// out[0] = ||x||_2
+void nrm2(const double* x, long long n, double* out, ReduceWorkspace& ws, int sm_count,
+          cudaStream_t st);
+
+// ---------------------------------------------------------- tall-skinny ---
+/// out[j] = sum_i V[i,j] * w[i], j < c.  V column-major with leading dim ld.
+void ts_dot(const double* V, long long ld, int n, int c, const double* w, double* out,
+            ReduceWorkspace& ws, int sm_count, cudaStream_t st);
+
+/// One CGS2 orthogonalisation step of w against V[:,0:c] (three sweeps):
+///   h1 = V^T w;  w -= V h1;  h2 = V^T w, s = ||w||^2 (fused);
+///   hsub = sqrt(s - ||h2||^2);  V[:,c] = (w - V h2) / hsub (fused).
+/// Hcol[0..c] receives (h1 + h2, hsub) and *flag the breakdown test
+/// hsub <= 1e-14 * ||Hcol|| (src/arnoldi.cpp:140-148); on breakdown
+/// Hcol[c] = 0 and V[:,c] is not written.  All outputs stay on device.
+void cgs2_step(double* V, long long ld, int n, int c, double* w, double* Hcol, int* flag,
+               ReduceWorkspace& ws, int sm_count, cudaStream_t st);
+
+/// One classical Gram-Schmidt pass: c = V^T v; v -= V c; out_norm = ||v||.
+/// corr (device, c) receives the coefficients.
+void cgs1_pass(const double* V, long long ld, int n, int c, double* v, double* corr,
+               double* out_norm, ReduceWorkspace& ws, int sm_count, cudaStream_t st);
+
+/// Out[:,0:p] = V[:,0:d] * G, G column-major d x p on device.  In place
+/// (Out == V, same ld) is allowed when p <= d: every row block is staged in
+/// shared memory before it is overwritten.
+void ts_combine(const double* V, long long ldv, int n, int d, const double* G, int p,
+                double* Out, long long ldo, cudaStream_t st);
+
+/// out[j] = sum_i Y[i,j]^2 for j < p.
+void col_sumsq(const double* Y, long long ld, int n, int p, double* out, ReduceWorkspace& ws,
+               int sm_count, cudaStream_t st);
+
+/// Ritz-pair checks against A (solver convergence test).
+/// real:  out[0] = mu = y.Ay ; out[1] = ||Ay - mu y||
+void ritz_check_real(const double* y, const double* Ay, long long n, double* out,
+                     ReduceWorkspace& ws, int sm_count, cudaStream_t st);
+/// complex y = yr + i yi:  out[0..1] = mu (re, im), out[2] = ||Ay - mu y||
+void ritz_check_complex(const double* yr, const double* yi, const double* Ayr,
+                        const double* Ayi, long long n, double* out, ReduceWorkspace& ws,
+                        int sm_count, cudaStream_t st);
+
+/// Ensures the reduction workspace can host `blocks` partial rows of
+/// `width` values.
+void ensure_workspace(ReduceWorkspace& ws, int blocks, int width);
+
+}  // namespace kern
+}  // namespace ppa

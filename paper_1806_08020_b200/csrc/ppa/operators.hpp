@@ -1,0 +1,127 @@
+#pragma once
+// Operators: the reference's operator module (inc/operators.hpp) with
+// device-resident vectors.  Names, semantics, counters and exceptions follow
+// the reference; the one substitution is the vector type - apply() takes
+// device pointers of length dim() instead of Eigen::Ref<VectorXd> (SURVEY
+// §8b "Constraint": host vectors would force a 32 MB H2D/D2H per apply).
+
+#include <memory>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "ppa/cost.hpp"
+#include "ppa/device.hpp"
+#include "ppa/kernels.hpp"
+
+namespace ppa {
+
+/// Host CSR matrix (inc/operators.hpp:15-33): int32 row_ptr[n+1], int32
+/// col_idx strictly increasing per row, fp64 values.
+struct CsrMatrix {
+  int n = 0;
+  std::vector<int> row_ptr;
+  std::vector<int> col_idx;
+  std::vector<double> values;
+
+  long long nnz() const { return static_cast<long long>(values.size()); }
+  double nnzr() const { return n > 0 ? double(nnz()) / double(n) : 0.0; }
+
+  /// Structural invariants; throws std::invalid_argument with the
+  /// reference's messages (src/operators.cpp:12-37).
+  void validate() const;
+
+  /// Sort by (row, col), sum duplicates in input order, validate
+  /// (src/operators.cpp:50-78; the sort is stable here so duplicate sums
+  /// are deterministic).
+  static CsrMatrix from_triplets(int n, std::vector<std::tuple<int, int, double>> t);
+};
+
+enum class OperatorKind { csr, diagonal, shifted, block2, poly, composite };
+
+/// A counted action v -> Op v on device vectors (inc/operators.hpp:49-76).
+/// Kernels run on the calling thread's current context stream.
+class LinearOperator {
+ public:
+  virtual ~LinearOperator() = default;
+  virtual int dim() const = 0;
+  virtual OperatorKind kind() const = 0;
+  /// y = Op x (device pointers, length dim(), x != y).  Increments rec.mvps
+  /// by the base-matrix applications performed.
+  virtual void apply(const double* x, double* y, CostRecord& rec) const = 0;
+  virtual int mvps_per_apply() const = 0;
+  virtual const std::vector<double>* diagonal() const { return nullptr; }
+  virtual double nnzr() const = 0;
+};
+
+using OperatorPtr = std::shared_ptr<const LinearOperator>;
+
+/// CSR operator whose matrix lives in HBM (uploaded once at construction,
+/// validated on the host first; src/operators.cpp:113-130).
+class CsrOperator final : public LinearOperator {
+ public:
+  explicit CsrOperator(const CsrMatrix& m, OperatorKind kind = OperatorKind::csr,
+                       std::vector<double> diag = {});
+  int dim() const override { return n_; }
+  OperatorKind kind() const override { return kind_; }
+  int mvps_per_apply() const override { return 1; }
+  double nnzr() const override { return nnzr_; }
+  const std::vector<double>* diagonal() const override {
+    return kind_ == OperatorKind::diagonal ? &diag_ : nullptr;
+  }
+  void apply(const double* x, double* y, CostRecord& rec) const override;
+
+  const kern::CsrDevice& device() const { return dev_; }
+  long long nnz() const { return nnz_; }
+  bool uses_sell() const { return dev_.sell_val != nullptr; }
+  long long sell_entries() const { return dev_.sell_entries; }
+  /// Bytes one SpMV moves under the north-star model:
+  /// 12*nnz + 4*(n+1) + 8n (x) + 8n (y).
+  double model_bytes() const {
+    return 12.0 * double(nnz_) + 4.0 * double(n_ + 1) + 16.0 * double(n_);
+  }
+
+ private:
+  int n_ = 0;
+  long long nnz_ = 0;
+  double nnzr_ = 0.0;
+  OperatorKind kind_;
+  std::vector<double> diag_;
+  DBuffer<int> row_ptr_, col_idx_, blk_row_, sell_col_;
+  DBuffer<double> values_, sell_val_;
+  DBuffer<long long> slice_ptr_;
+  kern::CsrDevice dev_;
+};
+
+OperatorPtr make_csr_operator(const CsrMatrix& matrix);
+/// Diagonal operator (src/operators.cpp:89-111), stored as a diagonal CSR.
+OperatorPtr make_diagonal(std::vector<double> diag_values);
+
+// ------------------------------------------------------- generators -----
+// Deterministic synthetic matrices (BASELINE.json configs; DESIGN.md
+// "Generators").  Column order per row is ascending, as the reference's
+// generator emits it (src/operators.cpp:215-238).
+
+/// The reference's two-region convection-diffusion matrix
+/// (src/operators.cpp:190-244), restated bit-exactly.
+CsrMatrix make_convection_diffusion(int grid_n);
+/// Constant-coefficient -u_xx - u_yy + beta u_x on a grid_n^2 interior grid,
+/// h = 1/(grid_n+1), beta = 2*peclet/h (configs 2 and 5: peclet = 0.5).
+CsrMatrix make_convection_diffusion_const(int grid_n, double peclet);
+/// 7-point 3D Laplacian (1/h^2 scaling), grid_n^3 unknowns (config 3).
+CsrMatrix make_laplacian_3d(int grid_n);
+/// Upper bidiagonal a_ii = i (1-based), a_i,i+1 = 1 (config 1).
+CsrMatrix make_bidiagonal(int n);
+/// Random sparse: row i gets max(1, Poisson(lambda)) off-diagonal entries
+/// with uniform columns != i and N(0,1)/8 values, plus a_ii = (i+1)/n*10
+/// (config 4).  Duplicates are summed in draw order.
+CsrMatrix make_random_poisson(int n, double lambda, unsigned long long seed);
+
+/// BASELINE.json configs 1..5 (matrix only).
+CsrMatrix make_config_matrix(int config);
+
+/// FNV-1a over (n, row_ptr, col_idx, values) bytes - the bit-exactness
+/// fingerprint compared against the oracle's generator.
+unsigned long long csr_fingerprint(const CsrMatrix& m);
+
+}  // namespace ppa

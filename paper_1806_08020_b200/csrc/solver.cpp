@@ -1,0 +1,349 @@
+// PP-Arnoldi driver: solve / solve_double / operator_norm_estimate.
+// The reference declares these (inc/solver.hpp:57-116) without a body; the
+// cycle structure follows SPEC.md [MODULE] solver and PAPER.md:563-575
+// (Arnoldi(m,k) on pi(A), Ritz values ordered by |1 - nu|, convergence
+// tested with Rayleigh quotients and true residuals against A).
+
+#include "ppa/solver.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <limits>
+#include <stdexcept>
+
+#include "ppa/kernels.hpp"
+#include "ppa/rng.hpp"
+
+namespace ppa {
+
+namespace {
+
+using cplx = std::complex<double>;
+using Clock = std::chrono::steady_clock;
+
+double seconds_since(Clock::time_point t0) {
+  return std::chrono::duration<double>(Clock::now() - t0).count();
+}
+
+DBuffer<double> upload(const std::vector<double>& h) {
+  DBuffer<double> d(h.size());
+  PPA_CUDA(cudaMemcpy(d.get(), h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+  return d;
+}
+
+long long round_ld(int n) { return (static_cast<long long>(n) + 31) / 32 * 32; }
+
+struct CheckOutcome {
+  std::vector<cplx> mu;
+  std::vector<double> res;
+  int real_checks = 0;
+  int pair_checks = 0;
+};
+
+// True-residual test of the first nev Ritz pairs against A (
+// PAPER.md:569-571).  All Ritz vectors are formed by one V*G launch; each
+// check is an SpMV plus two fused reductions; one read-back at the end.
+// Counters per real check: ritz_vector's charge (src/arnoldi.cpp:260-263)
+// + 1 mvp + 2 dots + 3 vops; per conjugate pair: + 2 mvps + 6 dots + 10 vops
+// (DESIGN.md "Solver decisions").
+CheckOutcome check_pairs(const ArnoldiState& st, const RitzSet& set, int nev,
+                         const LinearOperator& a, CostRecord& rec) {
+  Context& ctx = current_context();
+  const cudaStream_t s = ctx.stream();
+  const int d = set.vectors_h.rows;
+  const int nchk = std::min(nev, set.count());
+  // Plan: columns of G and which checks are pairs.
+  struct Item {
+    int j;
+    bool pair;
+    int col;
+  };
+  std::vector<Item> items;
+  int p = 0;
+  for (int j = 0; j < nchk;) {
+    const bool pair = ritz_is_complex(set.values[j]) && j + 1 < set.count();
+    items.push_back({j, pair, p});
+    p += pair ? 2 : 1;
+    j += pair ? 2 : 1;
+  }
+  std::vector<double> g(static_cast<size_t>(d) * p);
+  for (const Item& it : items) {
+    for (int r = 0; r < d; ++r) {
+      g[static_cast<size_t>(it.col) * d + r] = set.vectors_h(r, it.j).real();
+      if (it.pair) g[static_cast<size_t>(it.col + 1) * d + r] = set.vectors_h(r, it.j).imag();
+    }
+  }
+  Scratch gdev(g.size());
+  PPA_CUDA(cudaMemcpyAsync(gdev.get(), g.data(), g.size() * sizeof(double),
+                           cudaMemcpyHostToDevice, s));
+  const long long ldy = round_ld(st.n);
+  Scratch Y(static_cast<size_t>(ldy) * p);
+  Scratch AY(static_cast<size_t>(ldy) * p);
+  kern::ts_combine(st.V.get(), st.ld, st.n, d, gdev.get(), p, Y.get(), ldy, s);
+  Scratch sums(static_cast<size_t>(p) + 3 * items.size() + 8);
+  kern::col_sumsq(Y.get(), ldy, st.n, p, sums.get(), ctx.ws(), ctx.sm_count(), s);
+  std::vector<double> hs(p);
+  PPA_CUDA(cudaMemcpyAsync(hs.data(), sums.get(), p * sizeof(double), cudaMemcpyDeviceToHost, s));
+  ctx.sync();
+  double* outs = sums.get() + p;
+  for (size_t t = 0; t < items.size(); ++t) {
+    const Item& it = items[t];
+    double* yr = Y.get() + static_cast<long long>(it.col) * ldy;
+    double* ar = AY.get() + static_cast<long long>(it.col) * ldy;
+    if (!it.pair) {
+      kern::div_value(yr, std::sqrt(hs[it.col]), st.n, s);
+      rec.vops += d;
+      rec.dots += 1;
+      rec.vops += 2;
+      a.apply(yr, ar, rec);
+      kern::ritz_check_real(yr, ar, st.n, outs + 3 * t, ctx.ws(), ctx.sm_count(), s);
+      rec.dots += 2;
+      rec.vops += 3;
+    } else {
+      double* yi = yr + ldy;
+      double* ai = ar + ldy;
+      const double nrm = std::sqrt(hs[it.col] + hs[it.col + 1]);
+      kern::div_value(yr, nrm, st.n, s);
+      kern::div_value(yi, nrm, st.n, s);
+      rec.vops += 2LL * d;
+      rec.dots += 2;
+      rec.vops += 4;
+      a.apply(yr, ar, rec);
+      a.apply(yi, ai, rec);
+      kern::ritz_check_complex(yr, yi, ar, ai, st.n, outs + 3 * t, ctx.ws(), ctx.sm_count(), s);
+      rec.dots += 6;
+      rec.vops += 10;
+    }
+  }
+  std::vector<double> ho(3 * items.size());
+  PPA_CUDA(cudaMemcpyAsync(ho.data(), outs, ho.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  ctx.sync();
+  CheckOutcome out;
+  out.mu.assign(nchk, cplx(0.0, 0.0));
+  out.res.assign(nchk, 0.0);
+  for (size_t t = 0; t < items.size(); ++t) {
+    const Item& it = items[t];
+    if (!it.pair) {
+      out.mu[it.j] = cplx(ho[3 * t], 0.0);
+      out.res[it.j] = ho[3 * t + 1];
+      ++out.real_checks;
+    } else {
+      const cplx mu(ho[3 * t], ho[3 * t + 1]);
+      out.mu[it.j] = mu;
+      out.res[it.j] = ho[3 * t + 2];
+      if (it.j + 1 < nchk) {
+        out.mu[it.j + 1] = std::conj(mu);
+        out.res[it.j + 1] = ho[3 * t + 2];
+      }
+      ++out.pair_checks;
+    }
+  }
+  return out;
+}
+
+// Cycle loop shared by solve and solve_double.
+void run_cycles(const LinearOperator& a, const LinearOperator& op, const SolveConfig& cfg,
+                RitzOrdering ordering, EigResult& res, CostRecord& rec) {
+  Context& ctx = current_context();
+  const int n = a.dim();
+  const std::vector<double> v0h = rng::normal_vector(n, cfg.seed, rng::kArnoldiStart);
+  DBuffer<double> v0 = upload(v0h);
+  ArnoldiState st = arnoldi_init(v0.get(), n, cfg.m, rec);
+  res.max_err = std::numeric_limits<double>::infinity();
+  for (int cycle = 1; cycle <= cfg.max_cycles; ++cycle) {
+    CycleStats cs;
+    cs.cycle = cycle;
+    cs.start_dim = st.cur_dim;
+    auto t0 = Clock::now();
+    arnoldi_extend(st, op, cfg.m, rec);
+    res.timing.extend += seconds_since(t0);
+    cs.end_dim = st.cur_dim;
+
+    t0 = Clock::now();
+    const RitzSet set = cfg.variant == RestartVariant::harmonic
+                            ? harmonic_restart_selection(st, ordering)
+                            : ritz_pairs(st, ordering);
+    CheckOutcome chk = check_pairs(st, set, cfg.nev, a, rec);
+    res.timing.check += seconds_since(t0);
+    cs.real_checks = chk.real_checks;
+    cs.pair_checks = chk.pair_checks;
+    double mx = 0.0;
+    bool all = static_cast<int>(chk.res.size()) == cfg.nev;
+    for (double r : chk.res) {
+      mx = std::max(mx, r);
+      all = all && r <= res.rtol;
+    }
+    cs.max_residual = mx;
+    res.cycles = cycle;
+    if (mx < res.max_err) res.max_err = mx;
+    res.eigenvalues = chk.mu;
+    res.residuals = chk.res;
+    res.converged_flags.assign(chk.res.size(), false);
+    for (size_t i = 0; i < chk.res.size(); ++i) res.converged_flags[i] = chk.res[i] <= res.rtol;
+    if (all || cycle == cfg.max_cycles || st.breakdown) {
+      res.converged = all;
+      res.history.push_back(cs);
+      break;
+    }
+    t0 = Clock::now();
+    cs.restart_k = thick_restart(st, set, cfg.k, rec);
+    res.timing.restart += seconds_since(t0);
+    res.history.push_back(cs);
+  }
+}
+
+}  // namespace
+
+void SolveConfig::validate() const {
+  if (m < 2) throw std::invalid_argument("SolveConfig: m must be >= 2");
+  if (k <= 0 || k >= m) throw std::invalid_argument("SolveConfig: need 0 < k < m");
+  if (nev <= 0) throw std::invalid_argument("SolveConfig: need nev > 0");
+  if (!allow_nev_above_k && nev > k) throw std::invalid_argument("SolveConfig: need nev <= k");
+  if (nev >= m) throw std::invalid_argument("SolveConfig: need nev < m");
+  if (degree < 0) throw std::invalid_argument("SolveConfig: degree < 0");
+  if (double_d1 < 0 || double_d2 < 0) throw std::invalid_argument("SolveConfig: double degree < 0");
+  if (max_cycles < 1) throw std::invalid_argument("SolveConfig: max_cycles < 1");
+  if (rtol_absolute && !(*rtol_absolute > 0.0)) {
+    throw std::invalid_argument("SolveConfig: rtol_absolute must be > 0");
+  }
+  if (!(rtol_multiplier > 0.0)) throw std::invalid_argument("SolveConfig: rtol_multiplier <= 0");
+}
+
+int EigResult::count_correct(const std::vector<cplx>& reference, double rel_tol) const {
+  int c = 0;
+  for (size_t i = 0; i < eigenvalues.size(); ++i) {
+    if (i < converged_flags.size() && !converged_flags[i]) continue;
+    for (const cplx& r : reference) {
+      if (std::abs(eigenvalues[i] - r) <= rel_tol * std::abs(r)) {
+        ++c;
+        break;
+      }
+    }
+  }
+  return c;
+}
+
+bool check_ideal_order(const std::vector<cplx>& mu, int nev) {
+  if (nev < 1 || nev > static_cast<int>(mu.size())) {
+    throw std::invalid_argument("check_ideal_order: need 1 <= nev <= size");
+  }
+  for (int j = 1; j < nev; ++j)
+    if (std::abs(mu[j]) < std::abs(mu[j - 1])) return false;
+  for (size_t j = nev; j < mu.size(); ++j)
+    if (!(std::abs(mu[nev - 1]) < std::abs(mu[j]))) return false;
+  return true;
+}
+
+double operator_norm_estimate(const LinearOperator& a, unsigned long long seed, CostRecord& rec) {
+  if (const std::vector<double>* d = a.diagonal()) {
+    double mx = 0.0;
+    for (double v : *d) mx = std::max(mx, std::abs(v));
+    return mx;
+  }
+  // Five counted power-iteration steps from a seeded N(0,1) vector
+  // (SPEC.md "one cycle of power iteration (5 mvps)").
+  Context& ctx = current_context();
+  const cudaStream_t s = ctx.stream();
+  const int n = a.dim();
+  DBuffer<double> x = upload(rng::normal_vector(n, seed, rng::kNormEstimate));
+  DBuffer<double> y(static_cast<size_t>(n));
+  double nx = ctx.nrm2_sync(x.get(), n);
+  ++rec.dots;
+  ++rec.vops;
+  if (nx == 0.0) return 0.0;
+  kern::scale(x.get(), 1.0 / nx, n, s);
+  ++rec.vops;
+  double est = 0.0;
+  for (int it = 0; it < 5; ++it) {
+    a.apply(x.get(), y.get(), rec);
+    est = ctx.nrm2_sync(y.get(), n);
+    ++rec.dots;
+    ++rec.vops;
+    if (est == 0.0) break;
+    if (it + 1 < 5) {
+      kern::copy(y.get(), x.get(), n, s);
+      kern::scale(x.get(), 1.0 / est, n, s);
+      ++rec.vops;
+    }
+  }
+  ctx.sync();
+  return est;
+}
+
+EigResult solve(const OperatorPtr& a, const SolveConfig& cfg) {
+  if (!a) throw std::invalid_argument("solve: null operator");
+  cfg.validate();
+  if (a->dim() < cfg.m + 1) throw std::invalid_argument("solve: dimension must be >= m+1");
+  const auto t_all = Clock::now();
+  EigResult res;
+  CostRecord rec;
+  rec.nnzr = a->nnzr();
+  auto t0 = Clock::now();
+  res.norm_estimate = operator_norm_estimate(*a, cfg.seed, rec);
+  res.rtol = cfg.rtol_absolute ? *cfg.rtol_absolute : cfg.rtol_multiplier * res.norm_estimate;
+
+  OperatorPtr op = a;
+  RitzOrdering ordering = RitzOrdering::smallest_magnitude;
+  if (cfg.degree > 0) {
+    DBuffer<double> b = upload(rng::normal_vector(a->dim(), cfg.seed, rng::kPolyStart));
+    PolyPrecond p = build_gmres_poly(*a, b.get(), cfg.degree, rec);
+    if (cfg.stability == StabilityMode::pof_auto && p.roots.size() >= 2) {
+      p = add_stability_roots(p);
+    }
+    res.composite_degree = p.effective_degree();
+    op = make_poly_operator(a, p);
+    res.poly = p;
+    ordering = RitzOrdering::target_one;
+  }
+  current_context().sync();
+  res.timing.setup = seconds_since(t0);
+  run_cycles(*a, *op, cfg, ordering, res, rec);
+  current_context().sync();
+  res.timing.total = seconds_since(t_all);
+  rec.wall_seconds = res.timing.total;
+  res.cost = rec;
+  if (!cfg.reference.empty()) res.correct_count = res.count_correct(cfg.reference);
+  return res;
+}
+
+EigResult solve_double(const OperatorPtr& a, const SolveConfig& cfg) {
+  if (!a) throw std::invalid_argument("solve_double: null operator");
+  cfg.validate();
+  if (cfg.double_d1 < 1 || cfg.double_d2 < 1) {
+    throw std::invalid_argument("solve_double: d1, d2 must be >= 1");
+  }
+  if (a->dim() < cfg.m + 1) throw std::invalid_argument("solve_double: dimension must be >= m+1");
+  const auto t_all = Clock::now();
+  EigResult res;
+  CostRecord rec;
+  rec.nnzr = a->nnzr();
+  auto t0 = Clock::now();
+  res.norm_estimate = operator_norm_estimate(*a, cfg.seed, rec);
+  res.rtol = cfg.rtol_absolute ? *cfg.rtol_absolute : cfg.rtol_multiplier * res.norm_estimate;
+  const int n = a->dim();
+  DBuffer<double> b1 = upload(rng::normal_vector(n, cfg.seed, rng::kPolyStart));
+  PolyPrecond p1 = build_gmres_poly(*a, b1.get(), cfg.double_d1, rec);
+  p1.provenance = PolyProvenance::composite_stage;
+  OperatorPtr tau = make_poly_complement_operator(a, p1);
+  DBuffer<double> b2 = upload(rng::normal_vector(n, cfg.seed, rng::kPoly2Start));
+  PolyPrecond p2 = build_gmres_poly(*tau, b2.get(), cfg.double_d2, rec);
+  if (cfg.stability == StabilityMode::pof_auto && p2.roots.size() >= 2) {
+    p2 = add_stability_roots(p2);
+  }
+  res.composite_degree = p1.effective_degree() * p2.effective_degree();
+  OperatorPtr op = make_poly_operator(tau, p2);
+  res.inner_poly = p1;
+  res.poly = p2;
+  current_context().sync();
+  res.timing.setup = seconds_since(t0);
+  run_cycles(*a, *op, cfg, RitzOrdering::target_one, res, rec);
+  current_context().sync();
+  res.timing.total = seconds_since(t_all);
+  rec.wall_seconds = res.timing.total;
+  res.cost = rec;
+  if (!cfg.reference.empty()) res.correct_count = res.count_correct(cfg.reference);
+  return res;
+}
+
+}  // namespace ppa
