@@ -107,6 +107,23 @@ def dist_setup(gpus):
     return ws, rank, local
 
 
+def reduce_max(value: float, ws: int, device=None) -> float:
+    """Max over ranks (device-timed numbers; nccl on GPU, gloo on CPU)."""
+    if ws <= 1:
+        return value
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_gbs(bytes_per_step: float, ms_per_step: float, ws: int) -> float:
+    """Weak-scaling aggregate: every replica moves bytes_per_step per step."""
+    return ws * bytes_per_step / (ms_per_step * 1e-3) / 1e9
+
+
 def load_golden_poly():
     with open(os.path.join(ROOT, "tests", "golden", "c3_poly.json")) as f:
         g = json.load(f)
@@ -141,7 +158,8 @@ def run_reference(args):
     A = O.csr_operator(csr)
     roots = load_golden_poly()
     bspmv = 12.0 * nnz + 4.0 * (n + 1) + 16.0 * n
-    # size the per-step sample: ~3 s of CPU work
+    # size the per-step sample: ~3 s of CPU work (after one warm call)
+    O.time_poly_factors(A, roots, 1, 1)
     t1 = O.time_poly_factors(A, roots, 1, 1)
     nf = int(max(1, min(len(roots), 3.0 / max(t1, 1e-3))))
     for _ in range(args.warmup):
@@ -175,6 +193,7 @@ def cpu_baseline_port(roots):
     n, nnz, _ = csr.info()
     A = O.csr_operator(csr)
     bspmv = 12.0 * nnz + 4.0 * (n + 1) + 16.0 * n
+    O.time_poly_factors(A, roots, 1, 1)
     t1 = O.time_poly_factors(A, roots, 1, 1)
     nf = int(max(1, min(len(roots), 10.0 / max(t1, 1e-3))))
     t = O.time_poly_factors(A, roots, nf, 1)
@@ -229,13 +248,11 @@ def run_b200(args):
         e1.record(stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
+    ms = reduce_max(ms, ws, "cuda")
     if ws > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
         dist.barrier()
     ms_step = ms / args.steps
-    value = ws * step_bytes / (ms_step * 1e-3) / 1e9
+    value = whole_job_gbs(step_bytes, ms_step, ws)
     avg_launch_ms = ms_step / launches
     achieved = bspmv / (avg_launch_ms * 1e-3) / 1e9
     peak, peak_kind = hbm_peak()
@@ -267,33 +284,36 @@ def run_b200(args):
     f1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = f0.elapsed_time(f1) / ke
-    if ws > 1:
-        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e_val = ws * step_bytes / (e2e_ms * 1e-3) / 1e9
+    e2e_ms = reduce_max(e2e_ms, ws, "cuda")
+    e2e_val = whole_job_gbs(step_bytes, e2e_ms, ws)
     e2e_match = bool(np.array_equal(yh.numpy(), out.cpu().numpy()))
 
-    # CGS2 sweep bandwidth at basis size c = 40 (config 3's m)
+    # CGS2 step at basis size c = 40 (config 3's m) on a real Arnoldi basis of
+    # A: w = A v_39 orthogonalised against V[:,0:40] (3 sweeps, V[:,40] written).
     c = 40
-    ld = (n + 31) // 32 * 32
-    V = torch.randn((c + 1) * ld, dtype=torch.float64, device="cuda")
-    w = torch.randn(n, dtype=torch.float64, device="cuda")
+    st = ppa.arnoldi_init(v, n, c)
+    st.extend(A, c)
+    ld = st.ld
+    Vt = torch.empty(0, dtype=torch.float64, device="cuda")
+    w0 = torch.empty(n, dtype=torch.float64, device="cuda")
+    ppa.spmv(A, st.V_ptr + 8 * ld * (c - 1), w0)
+    w = torch.empty_like(w0)
     Hc = torch.empty(c + 2, dtype=torch.float64, device="cuda")
     flag = torch.zeros(2, dtype=torch.int32, device="cuda")
-    for _ in range(3):
-        ppa.cgs2_step(V, ld, n, c, w, Hc, flag)
-    g0 = torch.cuda.Event(enable_timing=True)
-    g1 = torch.cuda.Event(enable_timing=True)
     reps = 10
-    g0.record(stream)
-    for _ in range(reps):
-        ppa.cgs2_step(V, ld, n, c, w, Hc, flag)
-    g1.record(stream)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(reps + 3)]
+    for i, (g0, g1) in enumerate(evs):
+        w.copy_(w0)
+        g0.record(stream)
+        ppa.cgs2_step(st.V_ptr, ld, n, c, w, Hc, flag)
+        g1.record(stream)
     torch.cuda.synchronize()
-    cgs_ms = g0.elapsed_time(g1) / reps
+    cgs_ms = float(np.mean([g0.elapsed_time(g1) for g0, g1 in evs[3:]]))
+    cgs_flag = int(flag[0].item())
     cgs_gbs = 8.0 * n * (3 * c + 7) / (cgs_ms * 1e-3) / 1e9
-    del V, w
+    cgs_phys = 8.0 * n * (3 * c + 5) / (cgs_ms * 1e-3) / 1e9
+    del st, Vt
 
     # time to nev converged eigenpairs (config 3, matrix already on device)
     solve_info = None
@@ -337,7 +357,9 @@ def run_b200(args):
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "cgs2": {"c": c, "gbs_model": round(cgs_gbs, 2), "ms": round(cgs_ms, 4),
-                     "frac": round(cgs_gbs / peak, 4), "bytes_model": "8n(3c+7)"},
+                     "frac": round(cgs_gbs / peak, 4), "bytes_model": "8n(3c+7)",
+                     "gbs_moved": round(cgs_phys, 2), "bytes_moved": "8n(3c+5)",
+                     "breakdown_flag": cgs_flag},
             "time_to_nev": solve_info,
             "setup_seconds": round(setup_s, 3),
         }

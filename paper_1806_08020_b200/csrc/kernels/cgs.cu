@@ -1,0 +1,474 @@
+// CGS2 orthogonalisation and the other tall-skinny reductions over the
+// Krylov basis, as TMA-pipelined kernels.
+//
+// Replaces the MGS2 loop of arnoldi_extend (src/arnoldi.cpp:129-150), the
+// reorthogonalisation of thick_restart (src/arnoldi.cpp:317-324) and the
+// norms of ritz_vector (src/arnoldi.cpp:261).
+//
+// V is column-major in HBM (ld a multiple of 32 doubles) and is described to
+// the TMA unit by a 2D tensor map {rows = n, cols = c}.  A persistent CTA
+// (256 threads; 1-2 per SM by shared-memory footprint) walks a contiguous
+// range of 128-row tiles.  Thread 0 is the producer: one
+// cp.async.bulk.tensor.2d per tile moves the whole 128 x c block (rows past n
+// are zero-filled by the TMA) plus one 1 KB bulk copy of w into a
+// shared-memory stage, completing on the stage's mbarrier; `stages` tiles
+// stay in flight, so HBM never waits on the consumers.  The consumers (all 8
+// warps) read the tile from shared memory:
+//   dot     warp g owns columns j = g, g+8, ...; lanes walk rows
+//   update  row sums s = V h over two thread halves (fixed-order combine),
+//           then w -= s and the pass-2 dots / the norm / the V[:,c] store
+// Per-CTA partials are reduced in block order by the last CTA (ticket), so
+// every result is deterministic.  HBM bytes per CGS2 step at basis size c:
+// 3 sweeps over V[:,0:c] + w read 3x and written once + V[:,c] written once
+// = 8n(3c + 5) (the north-star model charges 8n(3c + 7)).
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "common.cuh"
+#include "ppa/kernels.hpp"
+#include "ws_layout.cuh"
+
+namespace ppa {
+namespace kern {
+namespace {
+
+constexpr int TR = 128;  // rows per tile
+constexpr int NT = 256;  // threads per CTA
+constexpr int NWARP = NT / 32;
+constexpr size_t kSmemPerSm = 200 * 1024;
+
+enum Mode : int { kDot = 0, kSumSq = 1, kUpd2 = 2, kUpd1 = 3, kStore = 4 };
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+struct PipeArgs {
+  const double* V;
+  long long ld;
+  int n;
+  int c;
+  double* w;        // dot: read; update: read + write
+  const double* h;  // update/store coefficients (device, c)
+  double* out;      // dot/sumsq: c results; upd1: the norm
+  int tiles_per_cta;
+  int stages;
+  double* partials;
+  unsigned int* ticket;
+  double* scal;  // upd2 finalisation / store hsub
+  double* Hcol;
+  int* flag;
+};
+
+__device__ __forceinline__ bool finish_grid(const double* s_col, int width, double* partials,
+                                            unsigned int* ticket, double* s_final) {
+  __shared__ unsigned int s_last;
+  for (int k = threadIdx.x; k < width; k += NT) {
+    partials[static_cast<size_t>(blockIdx.x) * width + k] = s_col[k];
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int t = atomicAdd(ticket, 1u);
+    s_last = (t == gridDim.x - 1) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!s_last) return false;
+  __threadfence();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = warp; k < width; k += NWARP) {
+    double acc = 0.0;
+    for (int b = lane; b < static_cast<int>(gridDim.x); b += 32) {
+      acc += __ldcg(partials + static_cast<size_t>(b) * width + k);
+    }
+    acc = dev::warp_sum(acc);
+    if (lane == 0) s_final[k] = acc;
+  }
+  if (threadIdx.x == 0) *ticket = 0u;
+  __syncthreads();
+  return true;
+}
+
+template <int MODE, int CPW>
+__global__ void __launch_bounds__(NT) k_tspipe(const __grid_constant__ CUtensorMap vmap,
+                                               PipeArgs a) {
+  constexpr bool kNeedW = MODE != kSumSq;
+  constexpr int MAXC = NWARP * CPW;
+  constexpr int RQ = TR / 32;  // rows per lane in the column-owner mapping
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ double s_h[MAXC];
+  __shared__ double s_part[2][TR];
+  __shared__ double s_col[MAXC + 1];
+  __shared__ double s_final[MAXC + 1];
+  __shared__ double s_red[NWARP];
+
+  if (MODE == kStore && *a.flag) return;
+  const int tid = threadIdx.x, lane = tid & 31, g = tid >> 5;
+  const int c = a.c;
+  const int ntiles = (a.n + TR - 1) / TR;
+  const int t_begin = blockIdx.x * a.tiles_per_cta;
+  const int count = max(0, min(ntiles, t_begin + a.tiles_per_cta) - t_begin);
+  const int S = a.stages;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  double* stage0 = reinterpret_cast<double*>(smem + 128);
+  // stage layout: V tile [c][TR] then w [TR]; 1 KB aligned
+  const size_t stage_elems = static_cast<size_t>(c + 1) * TR;
+
+  if (MODE == kUpd2 || MODE == kUpd1 || MODE == kStore) {
+    for (int j = tid; j < MAXC; j += NT) s_h[j] = j < c ? a.h[j] : 0.0;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const uint64_t policy = evict_first_policy();
+  auto issue = [&](int i) {
+    const int s = i % S;
+    const int row0 = (t_begin + i) * TR;
+    const bool wfull = kNeedW && row0 + TR <= a.n;
+    double* st = stage0 + s * stage_elems;
+    mbar_expect_tx(&bar[s], static_cast<uint32_t>(TR * c * 8 + (wfull ? TR * 8 : 0)));
+    tma_load_2d(st, &vmap, row0, 0, &bar[s], policy);
+    if (wfull) bulk_load(st + c * TR, a.w + row0, TR * 8, &bar[s], policy);
+  };
+  if (tid == 0) {
+    for (int i = 0; i < min(S, count); ++i) issue(i);
+  }
+
+  double acc[CPW];
+#pragma unroll
+  for (int jj = 0; jj < CPW; ++jj) acc[jj] = 0.0;
+  double nrm = 0.0;
+  const int half = tid >> 7;  // row-sum split over two halves of the columns
+  const int hr = tid & (TR - 1);
+  const int ch = (c + 1) >> 1;
+  const int jlo = half ? ch : 0;
+  const int jhi = half ? c : ch;
+  double* dstcol = const_cast<double*>(a.V) + static_cast<long long>(c) * a.ld;
+
+  for (int i = 0; i < count; ++i) {
+    const int s = i % S;
+    mbar_wait(&bar[s], (i / S) & 1);
+    const double* T = stage0 + s * stage_elems;
+    const int row0 = (t_begin + i) * TR;
+    const int rows = min(TR, a.n - row0);
+    const bool full = rows == TR;
+    const double* W = T + c * TR;
+
+    if (MODE == kDot || MODE == kSumSq) {
+      // rows beyond n are zero in the tile (TMA OOB fill) and w is zeroed here
+      double wr[RQ];
+#pragma unroll
+      for (int q = 0; q < RQ; ++q) {
+        const int r = lane + 32 * q;
+        wr[q] = MODE == kDot ? (full ? W[r] : (r < rows ? a.w[row0 + r] : 0.0)) : 0.0;
+      }
+#pragma unroll
+      for (int jj = 0; jj < CPW; ++jj) {
+        const int j = g + NWARP * jj;
+        if (j < c) {
+          const double* col = T + j * TR + lane;
+#pragma unroll
+          for (int q = 0; q < RQ; ++q) {
+            const double v = col[32 * q];
+            acc[jj] = MODE == kDot ? fma(v, wr[q], acc[jj]) : fma(v, v, acc[jj]);
+          }
+        }
+      }
+    } else {
+      // phase A: partial row sums over this thread's half of the columns
+      double sp = 0.0;
+      const double* col = T + hr;
+      for (int j = jlo; j < jhi; ++j) sp = fma(col[j * TR], s_h[j], sp);
+      s_part[half][hr] = sp;
+      __syncthreads();
+      if (MODE == kUpd2) {
+#pragma unroll
+        for (int q = 0; q < RQ; ++q) {
+          const int r = lane + 32 * q;
+          const double wo = full ? W[r] : (r < rows ? a.w[row0 + r] : 0.0);
+          const double wn = r < rows ? wo - (s_part[0][r] + s_part[1][r]) : 0.0;
+#pragma unroll
+          for (int jj = 0; jj < CPW; ++jj) {
+            const int j = g + NWARP * jj;
+            if (j < c) acc[jj] = fma(T[j * TR + r], wn, acc[jj]);
+          }
+          if (g == 0 && r < rows) {
+            nrm = fma(wn, wn, nrm);
+            a.w[row0 + r] = wn;
+          }
+        }
+      } else if (tid < rows) {
+        const double wo = full ? W[tid] : a.w[row0 + tid];
+        const double wn = wo - (s_part[0][tid] + s_part[1][tid]);
+        if (MODE == kUpd1) {
+          nrm = fma(wn, wn, nrm);
+          a.w[row0 + tid] = wn;
+        } else {  // kStore: V[:,c] = (w - V h2) / hsub
+          dstcol[row0 + tid] = wn / a.scal[kScalHsub];
+        }
+      }
+    }
+    __syncthreads();  // stage s and s_part are free again
+    if (tid == 0 && i + S < count) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(i + S);
+    }
+  }
+
+  if (MODE == kStore) return;
+  int width = 1;
+  if (MODE == kDot || MODE == kSumSq || MODE == kUpd2) {
+#pragma unroll
+    for (int jj = 0; jj < CPW; ++jj) {
+      const int j = g + NWARP * jj;
+      if (j < c) {
+        const double t = dev::warp_sum(acc[jj]);
+        if (lane == 0) s_col[j] = t;
+      }
+    }
+    width = MODE == kUpd2 ? c + 1 : c;
+  }
+  if (MODE == kUpd2 || MODE == kUpd1) {
+    const double t = dev::warp_sum(nrm);
+    if (lane == 0) s_red[g] = t;
+    __syncthreads();
+    if (tid == 0) {
+      double tot = 0.0;
+      for (int k = 0; k < NWARP; ++k) tot += s_red[k];
+      s_col[width - 1] = tot;
+    }
+  }
+  __syncthreads();
+  if (!finish_grid(s_col, width, a.partials, a.ticket, s_final)) return;
+
+  if (MODE == kDot || MODE == kSumSq) {
+    for (int j = tid; j < c; j += NT) a.out[j] = s_final[j];
+    return;
+  }
+  if (MODE == kUpd1) {
+    if (tid == 0) *a.out = sqrt(s_final[0]);
+    return;
+  }
+  // kUpd2: s_final[0..c) = h2, s_final[c] = ||w||^2 -> Hessenberg column,
+  // hsub (Pythagoras: ||w - V h2||^2 = ||w||^2 - ||h2||^2 for orthonormal V)
+  // and the breakdown test of src/arnoldi.cpp:143-148.
+  for (int j = tid; j < c; j += NT) a.scal[kScalH2 + j] = s_final[j];
+  if (tid == 0) {
+    double sq = 0.0;
+    for (int j = 0; j < c; ++j) sq += s_final[j] * s_final[j];
+    const double d2 = s_final[c] - sq;
+    const double hsub = d2 > 0.0 ? sqrt(d2) : 0.0;
+    a.scal[kScalHsub] = hsub;
+    a.scal[kScalHsub + 1] = sqrt(s_final[c]);
+    double cn = 0.0;
+    for (int j = 0; j < c; ++j) {
+      const double hj = s_h[j] + s_final[j];
+      a.Hcol[j] = hj;
+      cn += hj * hj;
+    }
+    cn += hsub * hsub;
+    const double colnorm = sqrt(cn);
+    int bd = 0;
+    if (!isfinite(hsub) || !isfinite(colnorm)) {
+      bd = 2;
+    } else if (hsub <= 1e-14 * colnorm) {
+      bd = 1;
+    }
+    a.Hcol[c] = bd ? 0.0 : hsub;
+    *a.flag = bd;
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    PPA_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) {
+      throw CudaError("cuTensorMapEncodeTiled entry point unavailable");
+    }
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// 2D map of the first c columns of V: dim0 = rows (n, contiguous), dim1 =
+// columns (stride ld); box = 128 rows x c columns.
+CUtensorMap basis_map(const double* V, long long ld, int n, int c) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(c)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * sizeof(double)};
+  const cuuint32_t box[2] = {TR, static_cast<cuuint32_t>(c)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(V),
+                               dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return m;
+}
+
+template <int MODE, int CPW>
+void launch_pipe(PipeArgs a, ReduceWorkspace& ws, int sm_count, cudaStream_t st) {
+  const size_t stage_bytes = static_cast<size_t>(a.c + 1) * TR * sizeof(double);
+  // two CTAs per SM when two double-buffered CTAs fit, else one deeper CTA
+  const int per_sm = 4 * stage_bytes <= kSmemPerSm ? 2 : 1;
+  const size_t budget = kSmemPerSm / per_sm;
+  const int stages =
+      static_cast<int>(std::max<size_t>(2, std::min<size_t>(6, budget / stage_bytes)));
+  const size_t smem = 128 + stage_bytes * stages;
+  static size_t configured = 0;
+  if (smem > configured) {
+    PPA_CUDA(cudaFuncSetAttribute(k_tspipe<MODE, CPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(std::max<size_t>(smem, 48 * 1024))));
+    configured = std::max<size_t>(smem, 48 * 1024);
+  }
+  const int ntiles = (a.n + TR - 1) / TR;
+  const int grid0 = std::max(1, std::min(ntiles, sm_count * per_sm));
+  a.tiles_per_cta = (ntiles + grid0 - 1) / grid0;
+  const int grid = (ntiles + a.tiles_per_cta - 1) / a.tiles_per_cta;
+  a.stages = stages;
+  ensure_workspace(ws, grid, NWARP * CPW + 1);
+  a.partials = ws.partials.get();
+  a.ticket = ws.tickets.get();
+  const CUtensorMap map = basis_map(a.V, a.ld, a.n, a.c);
+  k_tspipe<MODE, CPW><<<grid, NT, smem, st>>>(map, a);
+  PPA_CUDA(cudaGetLastError());
+}
+
+template <int MODE>
+void dispatch(const PipeArgs& a, ReduceWorkspace& ws, int sm_count, cudaStream_t st) {
+  if (a.c <= 8) return launch_pipe<MODE, 1>(a, ws, sm_count, st);
+  if (a.c <= 16) return launch_pipe<MODE, 2>(a, ws, sm_count, st);
+  if (a.c <= 32) return launch_pipe<MODE, 4>(a, ws, sm_count, st);
+  if (a.c <= 64) return launch_pipe<MODE, 8>(a, ws, sm_count, st);
+  return launch_pipe<MODE, 16>(a, ws, sm_count, st);
+}
+
+void check_aligned(const void* p, const char* who) {
+  if (reinterpret_cast<uintptr_t>(p) % 16 != 0) {
+    throw std::invalid_argument(std::string(who) + ": vectors must be 16-byte aligned");
+  }
+}
+
+void check_basis(const double* V, long long ld, int n, int c, const char* who) {
+  check_cols(c, who);
+  check_aligned(V, who);
+  if (ld % 2 || ld < n) {
+    throw std::invalid_argument(std::string(who) + ": leading dimension must be even and >= n");
+  }
+}
+
+PipeArgs base_args(const double* V, long long ld, int n, int c) {
+  PipeArgs a{};
+  a.V = V;
+  a.ld = ld;
+  a.n = n;
+  a.c = c;
+  return a;
+}
+
+}  // namespace
+
+void ts_dot(const double* V, long long ld, int n, int c, const double* w, double* out,
+            ReduceWorkspace& ws, int sm_count, cudaStream_t st) {
+  if (n <= 0) return;
+  check_basis(V, ld, n, c, "ts_dot");
+  check_aligned(w, "ts_dot");
+  PipeArgs a = base_args(V, ld, n, c);
+  a.w = const_cast<double*>(w);
+  a.out = out;
+  dispatch<kDot>(a, ws, sm_count, st);
+}
+
+void col_sumsq(const double* Y, long long ld, int n, int p, double* out, ReduceWorkspace& ws,
+               int sm_count, cudaStream_t st) {
+  if (n <= 0) return;
+  check_basis(Y, ld, n, p, "col_sumsq");
+  PipeArgs a = base_args(Y, ld, n, p);
+  a.out = out;
+  dispatch<kSumSq>(a, ws, sm_count, st);
+}
+
+void cgs2_step(double* V, long long ld, int n, int c, double* w, double* Hcol, int* flag,
+               ReduceWorkspace& ws, int sm_count, cudaStream_t st) {
+  check_basis(V, ld, n, c, "cgs2_step");
+  check_aligned(w, "cgs2_step");
+  double* scal = ws.scalars.get();
+  ts_dot(V, ld, n, c, w, scal + kScalH1, ws, sm_count, st);
+  PipeArgs a = base_args(V, ld, n, c);
+  a.w = w;
+  a.h = scal + kScalH1;
+  a.scal = scal;
+  a.Hcol = Hcol;
+  a.flag = flag;
+  dispatch<kUpd2>(a, ws, sm_count, st);
+  PipeArgs b = base_args(V, ld, n, c);
+  b.w = w;
+  b.h = scal + kScalH2;
+  b.scal = scal;
+  b.flag = flag;
+  dispatch<kStore>(b, ws, sm_count, st);
+}
+
+void cgs1_pass(const double* V, long long ld, int n, int c, double* v, double* corr,
+               double* out_norm, ReduceWorkspace& ws, int sm_count, cudaStream_t st) {
+  check_basis(V, ld, n, c, "cgs1_pass");
+  check_aligned(v, "cgs1_pass");
+  ts_dot(V, ld, n, c, v, corr, ws, sm_count, st);
+  PipeArgs a = base_args(V, ld, n, c);
+  a.w = v;
+  a.h = corr;
+  a.out = out_norm;
+  dispatch<kUpd1>(a, ws, sm_count, st);
+}
+
+}  // namespace kern
+}  // namespace ppa

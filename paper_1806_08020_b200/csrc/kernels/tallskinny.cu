@@ -16,18 +16,12 @@
 #include <string>
 
 #include "common.cuh"
+#include "ws_layout.cuh"
 #include "ppa/kernels.hpp"
 
 namespace ppa {
 namespace kern {
 
-// Layout of ReduceWorkspace::scalars (device doubles).
-constexpr int kScalH1 = 0;
-constexpr int kScalH2 = 256;
-constexpr int kScalHsub = 512;
-constexpr int kScalTmp = 520;   // ritz checks
-constexpr int kScalCount = 1024;
-constexpr int kMaxCols = 128;
 
 void ensure_workspace(ReduceWorkspace& ws, int blocks, int width) {
   if (!ws.tickets.get()) {
@@ -189,308 +183,6 @@ __global__ void k_fill(double* x, double v, long long n) {
 
 inline int ew_grid(long long n) { return std::max(1, std::min(ceil_div(n, 256), 148 * 16)); }
 
-// ------------------------------------------------------------------------
-// CGS2 sweeps: "warp = column group" layout.
-//
-// A 256-thread CTA is 8 warps; column j of V belongs to warp j % 8 (slot
-// j / 8, at most CPW columns per warp).  Lanes walk row PAIRS with 16-byte
-// loads (a warp reads 512 contiguous bytes of one column per request), so
-// per-thread state is CPW accumulators (+ the cached V tile in sweep 2):
-// low registers, many resident warps, every HBM byte coalesced.  Row sums
-// that need all columns (w - V h) are combined across the 8 warps through
-// shared memory in a fixed order, so results are deterministic.
-// ------------------------------------------------------------------------
-
-constexpr int NW = 8;           // warps per CTA
-constexpr int TS = NW * 32;     // threads per CTA
-
-__device__ __forceinline__ double2 ld_pair(const double* p, int r, int n) {
-  if (r + 1 < n) return __ldg(reinterpret_cast<const double2*>(p + r));
-  if (r < n) return make_double2(__ldg(p + r), 0.0);
-  return make_double2(0.0, 0.0);
-}
-
-// Per-column block partials already unique per column (s_col[0..width)):
-// write the block's row, the last CTA sums rows in block order.
-__device__ __forceinline__ bool grid_finish(const double* s_col, int width, double* partials,
-                                            unsigned int* ticket, double* s_final) {
-  __shared__ unsigned int s_last;
-  for (int k = threadIdx.x; k < width; k += blockDim.x) {
-    partials[static_cast<size_t>(blockIdx.x) * width + k] = s_col[k];
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned int t = atomicAdd(ticket, 1u);
-    s_last = (t == gridDim.x - 1) ? 1u : 0u;
-  }
-  __syncthreads();
-  if (!s_last) return false;
-  __threadfence();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  for (int k = warp; k < width; k += nwarp) {
-    double acc = 0.0;
-    for (int b = lane; b < static_cast<int>(gridDim.x); b += 32) {
-      acc += __ldcg(partials + static_cast<size_t>(b) * width + k);
-    }
-    acc = dev::warp_sum(acc);
-    if (lane == 0) s_final[k] = acc;
-  }
-  if (threadIdx.x == 0) *ticket = 0u;
-  __syncthreads();
-  return true;
-}
-
-// out[j] = sum_i V[i,j] * w[i]  (SQ: sum_i V[i,j]^2), j < c.
-template <int CPW, int QP, bool SQ>
-__global__ void __launch_bounds__(TS) k_mdot(const double* __restrict__ V, long long ld, int n,
-                                             int c, const double* __restrict__ w, int rpb,
-                                             double* partials, unsigned int* ticket,
-                                             double* out) {
-  __shared__ double s_col[NW * CPW];
-  __shared__ double s_final[NW * CPW];
-  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
-  double acc[CPW];
-#pragma unroll
-  for (int jj = 0; jj < CPW; ++jj) acc[jj] = 0.0;
-  const int r0 = blockIdx.x * rpb;
-  const int r1 = min(n, r0 + rpb);
-  for (int t0 = r0; t0 < r1; t0 += 64 * QP) {
-    double2 wv[QP];
-#pragma unroll
-    for (int q = 0; q < QP; ++q) {
-      const int r = t0 + 64 * q + 2 * lane;
-      wv[q] = SQ ? make_double2(0.0, 0.0) : (r < r1 ? ld_pair(w, r, r1) : make_double2(0.0, 0.0));
-    }
-#pragma unroll
-    for (int jj = 0; jj < CPW; ++jj) {
-      const int j = g + NW * jj;
-      if (j < c) {
-        const double* col = V + static_cast<long long>(j) * ld;
-#pragma unroll
-        for (int q = 0; q < QP; ++q) {
-          const int r = t0 + 64 * q + 2 * lane;
-          const double2 v = r < r1 ? ld_pair(col, r, r1) : make_double2(0.0, 0.0);
-          if (SQ) {
-            acc[jj] = fma(v.x, v.x, acc[jj]);
-            acc[jj] = fma(v.y, v.y, acc[jj]);
-          } else {
-            acc[jj] = fma(v.x, wv[q].x, acc[jj]);
-            acc[jj] = fma(v.y, wv[q].y, acc[jj]);
-          }
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int jj = 0; jj < CPW; ++jj) {
-    const int j = g + NW * jj;
-    if (j < c) {
-      const double t = dev::warp_sum(acc[jj]);
-      if (lane == 0) s_col[j] = t;
-    }
-  }
-  __syncthreads();
-  if (grid_finish(s_col, c, partials, ticket, s_final)) {
-    for (int j = threadIdx.x; j < c; j += TS) out[j] = s_final[j];
-  }
-}
-
-// w -= V h (h device); optionally h2 = V^T w and ||w||^2 (DOT); the CGS2
-// finalisation (Hessenberg column, hsub, breakdown flag) runs in the last CTA.
-// MODE 0: CGS2 sweep 2.  MODE 1: single-pass reorth (norm only).
-template <int CPW, int QP, int MODE>
-__global__ void __launch_bounds__(TS) k_cgs_update(const double* __restrict__ V, long long ld,
-                                                   int n, int c, double* __restrict__ w,
-                                                   const double* __restrict__ h1, int rpb,
-                                                   double* partials, unsigned int* ticket,
-                                                   double* scal, double* Hcol, int* flag,
-                                                   double* out_norm) {
-  __shared__ double s_h[NW * CPW];
-  __shared__ __align__(16) double s_part[2][NW][64 * QP];
-  __shared__ double s_col[NW * CPW + 1];
-  __shared__ double s_final[NW * CPW + 1];
-  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
-  for (int j = threadIdx.x; j < NW * CPW; j += TS) s_h[j] = j < c ? h1[j] : 0.0;
-  __syncthreads();
-  double acc[CPW];
-#pragma unroll
-  for (int jj = 0; jj < CPW; ++jj) acc[jj] = 0.0;
-  double nrm = 0.0;
-  const int r0 = blockIdx.x * rpb;
-  const int r1 = min(n, r0 + rpb);
-  int par = 0;
-  for (int t0 = r0; t0 < r1; t0 += 64 * QP, par ^= 1) {
-    double2 vr[QP][MODE == 0 ? CPW : 1];
-    double2 part[QP];
-#pragma unroll
-    for (int q = 0; q < QP; ++q) part[q] = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int jj = 0; jj < CPW; ++jj) {
-      const int j = g + NW * jj;
-      if (j < c) {
-        const double* col = V + static_cast<long long>(j) * ld;
-        const double hj = s_h[j];
-#pragma unroll
-        for (int q = 0; q < QP; ++q) {
-          const int r = t0 + 64 * q + 2 * lane;
-          const double2 v = r < r1 ? ld_pair(col, r, r1) : make_double2(0.0, 0.0);
-          if (MODE == 0) vr[q][jj] = v;
-          part[q].x = fma(v.x, hj, part[q].x);
-          part[q].y = fma(v.y, hj, part[q].y);
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < QP; ++q) {
-      reinterpret_cast<double2*>(s_part[par][g])[32 * q + lane] = part[q];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < QP; ++q) {
-      const int r = t0 + 64 * q + 2 * lane;
-      if (r >= r1) continue;
-      double2 sum = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int k = 0; k < NW; ++k) {
-        const double2 pk = reinterpret_cast<const double2*>(s_part[par][k])[32 * q + lane];
-        sum.x += pk.x;
-        sum.y += pk.y;
-      }
-      const double2 wo = ld_pair(w, r, r1);
-      const double2 wn = make_double2(wo.x - sum.x, wo.y - sum.y);
-      if (MODE == 0) {
-#pragma unroll
-        for (int jj = 0; jj < CPW; ++jj) {
-          if (g + NW * jj < c) {
-            acc[jj] = fma(vr[q][jj].x, wn.x, acc[jj]);
-            acc[jj] = fma(vr[q][jj].y, wn.y, acc[jj]);
-          }
-        }
-      }
-      if (g == 0) {
-        nrm = fma(wn.x, wn.x, nrm);
-        if (r + 1 < r1) {
-          nrm = fma(wn.y, wn.y, nrm);
-          *reinterpret_cast<double2*>(w + r) = wn;
-        } else {
-          w[r] = wn.x;
-        }
-      }
-    }
-  }
-  const int width = MODE == 0 ? c + 1 : 1;
-  if (MODE == 0) {
-#pragma unroll
-    for (int jj = 0; jj < CPW; ++jj) {
-      const int j = g + NW * jj;
-      if (j < c) {
-        const double t = dev::warp_sum(acc[jj]);
-        if (lane == 0) s_col[j] = t;
-      }
-    }
-  }
-  if (g == 0) {
-    const double t = dev::warp_sum(nrm);
-    if (lane == 0) s_col[width - 1] = t;
-  }
-  __syncthreads();
-  if (!grid_finish(s_col, width, partials, ticket, s_final)) return;
-  if (MODE == 1) {
-    if (threadIdx.x == 0) *out_norm = sqrt(s_final[0]);
-    return;
-  }
-  for (int j = threadIdx.x; j < c; j += TS) scal[kScalH2 + j] = s_final[j];
-  if (threadIdx.x == 0) {
-    double sq = 0.0;
-    for (int j = 0; j < c; ++j) sq += s_final[j] * s_final[j];
-    const double d2 = s_final[c] - sq;
-    const double hsub = d2 > 0.0 ? sqrt(d2) : 0.0;
-    scal[kScalHsub] = hsub;
-    scal[kScalHsub + 1] = sqrt(s_final[c]);
-    double cn = 0.0;
-    for (int j = 0; j < c; ++j) {
-      const double hj = s_h[j] + s_final[j];
-      Hcol[j] = hj;
-      cn += hj * hj;
-    }
-    cn += hsub * hsub;
-    const double colnorm = sqrt(cn);
-    int bd = 0;
-    if (!isfinite(hsub) || !isfinite(colnorm)) {
-      bd = 2;
-    } else if (hsub <= 1e-14 * colnorm) {
-      bd = 1;
-    }
-    Hcol[c] = bd ? 0.0 : hsub;
-    *flag = bd;
-  }
-}
-
-// Sweep 3: V[:,c] = (w - V h2) / hsub, skipped on breakdown.
-template <int CPW, int QP>
-__global__ void __launch_bounds__(TS) k_cgs_store(double* V, long long ld, int n, int c,
-                                                  const double* __restrict__ w, int rpb,
-                                                  const double* __restrict__ scal,
-                                                  const int* flag) {
-  if (*flag) return;
-  __shared__ double s_h[NW * CPW];
-  __shared__ __align__(16) double s_part[2][NW][64 * QP];
-  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
-  for (int j = threadIdx.x; j < NW * CPW; j += TS) s_h[j] = j < c ? scal[kScalH2 + j] : 0.0;
-  const double hsub = scal[kScalHsub];
-  __syncthreads();
-  double* out = V + static_cast<long long>(c) * ld;
-  const int r0 = blockIdx.x * rpb;
-  const int r1 = min(n, r0 + rpb);
-  int par = 0;
-  for (int t0 = r0; t0 < r1; t0 += 64 * QP, par ^= 1) {
-    double2 part[QP];
-#pragma unroll
-    for (int q = 0; q < QP; ++q) part[q] = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int jj = 0; jj < CPW; ++jj) {
-      const int j = g + NW * jj;
-      if (j < c) {
-        const double* col = V + static_cast<long long>(j) * ld;
-        const double hj = s_h[j];
-#pragma unroll
-        for (int q = 0; q < QP; ++q) {
-          const int r = t0 + 64 * q + 2 * lane;
-          const double2 v = r < r1 ? ld_pair(col, r, r1) : make_double2(0.0, 0.0);
-          part[q].x = fma(v.x, hj, part[q].x);
-          part[q].y = fma(v.y, hj, part[q].y);
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < QP; ++q) {
-      reinterpret_cast<double2*>(s_part[par][g])[32 * q + lane] = part[q];
-    }
-    __syncthreads();
-    if (g < QP) {
-      const int q = g;
-      const int r = t0 + 64 * q + 2 * lane;
-      if (r < r1) {
-        double2 sum = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int k = 0; k < NW; ++k) {
-          const double2 pk = reinterpret_cast<const double2*>(s_part[par][k])[32 * q + lane];
-          sum.x += pk.x;
-          sum.y += pk.y;
-        }
-        const double2 wo = ld_pair(w, r, r1);
-        const double a = (wo.x - sum.x) / hsub;
-        if (r + 1 < r1) {
-          *reinterpret_cast<double2*>(out + r) = make_double2(a, (wo.y - sum.y) / hsub);
-        } else {
-          out[r] = a;
-        }
-      }
-    }
-  }
-}
-
 // Out[:,0:p] = V[:,0:d] * G, one row per thread, the block's rows staged
 // in shared memory first (so Out may alias V).
 constexpr int kCombineRows = 128;
@@ -518,81 +210,13 @@ __global__ void __launch_bounds__(kCombineRows) k_ts_combine(const double* V, lo
   }
 }
 
-template <typename K>
-int occupancy_of(K kernel) {
-  int o = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, TS, 0);
-  return std::max(1, o);
-}
-
-// Row partition: `blocks` CTAs, each a contiguous range of whole 128-row tiles.
-struct Part {
-  int grid, rpb;
-};
-Part partition(int n, int sm_count, int occ) {
-  const int tiles = ceil_div(n, 128);
-  const int blocks = std::max(1, std::min(tiles, sm_count * occ));
-  const int rpb = ceil_div(tiles, blocks) * 128;
-  return {std::max(1, ceil_div(n, rpb)), rpb};
-}
-
-void check_aligned(const void* p, const char* who) {
-  if (reinterpret_cast<uintptr_t>(p) % 16 != 0) {
-    throw std::invalid_argument(std::string(who) + ": vectors must be 16-byte aligned");
-  }
-}
-
-template <int CPW>
-void launch_mdot(const double* V, long long ld, int n, int c, const double* w, double* out,
-                 bool sq, ReduceWorkspace& ws, int sm_count, cudaStream_t st) {
-  constexpr int QP = CPW <= 4 ? 4 : 2;
-  auto kern = sq ? k_mdot<CPW, QP, true> : k_mdot<CPW, QP, false>;
-  static const int occ_t = occupancy_of(k_mdot<CPW, QP, false>);
-  const Part pt = partition(n, sm_count, occ_t);
-  ensure_workspace(ws, pt.grid, NW * CPW + 1);
-  kern<<<pt.grid, TS, 0, st>>>(V, ld, n, c, w, pt.rpb, ws.partials.get(), ws.tickets.get(), out);
-  PPA_CUDA(cudaGetLastError());
-}
-
-template <int CPW>
-void launch_cgs2(double* V, long long ld, int n, int c, double* w, double* Hcol, int* flag,
-                 ReduceWorkspace& ws, int sm_count, cudaStream_t st) {
-  constexpr int QP = CPW <= 4 ? 2 : 1;
-  launch_mdot<CPW>(V, ld, n, c, w, ws.scalars.get() + kScalH1, false, ws, sm_count, st);
-  static const int occ_u = occupancy_of(k_cgs_update<CPW, QP, 0>);
-  const Part pu = partition(n, sm_count, occ_u);
-  ensure_workspace(ws, pu.grid, NW * CPW + 1);
-  double* scal = ws.scalars.get();
-  k_cgs_update<CPW, QP, 0><<<pu.grid, TS, 0, st>>>(V, ld, n, c, w, scal + kScalH1, pu.rpb,
-                                                   ws.partials.get(), ws.tickets.get(), scal,
-                                                   Hcol, flag, nullptr);
-  static const int occ_s = occupancy_of(k_cgs_store<CPW, QP>);
-  const Part ps = partition(n, sm_count, occ_s);
-  k_cgs_store<CPW, QP><<<ps.grid, TS, 0, st>>>(V, ld, n, c, w, ps.rpb, scal, flag);
-  PPA_CUDA(cudaGetLastError());
-}
-
-template <int CPW>
-void launch_cgs1(const double* V, long long ld, int n, int c, double* v, double* corr,
-                 double* out_norm, ReduceWorkspace& ws, int sm_count, cudaStream_t st) {
-  constexpr int QP = CPW <= 4 ? 2 : 1;
-  launch_mdot<CPW>(V, ld, n, c, v, corr, false, ws, sm_count, st);
-  static const int occ_u = occupancy_of(k_cgs_update<CPW, QP, 1>);
-  const Part pu = partition(n, sm_count, occ_u);
-  ensure_workspace(ws, pu.grid, NW * CPW + 1);
-  k_cgs_update<CPW, QP, 1><<<pu.grid, TS, 0, st>>>(V, ld, n, c, v, corr, pu.rpb,
-                                                   ws.partials.get(), ws.tickets.get(), nullptr,
-                                                   nullptr, nullptr, out_norm);
-  PPA_CUDA(cudaGetLastError());
-}
+}  // namespace
 
 void check_cols(int c, const char* who) {
   if (c < 1 || c > kMaxCols) {
     throw std::invalid_argument(std::string(who) + ": column count out of range [1,128]");
   }
 }
-
-}  // namespace
 
 // ------------------------------------------------------------------------
 // launchers
@@ -655,55 +279,6 @@ void ritz_check_complex(const double* yr, const double* yi, const double* ar, co
                         cudaStream_t st) {
   run_reduce<4>(n, OpCplxDots{yr, yi, ar, ai, out}, ws, sm_count, st);
   run_reduce<1>(n, OpCplxResid{yr, yi, ar, ai, out}, ws, sm_count, st);
-}
-
-#define PPA_CPW_DISPATCH(c, CALL) \
-  do {                                  \
-    if ((c) <= 8) { CALL(1); }          \
-    else if ((c) <= 16) { CALL(2); }    \
-    else if ((c) <= 32) { CALL(4); }    \
-    else if ((c) <= 64) { CALL(8); }    \
-    else { CALL(16); }                  \
-  } while (0)
-
-void ts_dot(const double* V, long long ld, int n, int c, const double* w, double* out,
-            ReduceWorkspace& ws, int sm_count, cudaStream_t st) {
-  check_cols(c, "ts_dot");
-  check_aligned(V, "ts_dot");
-  check_aligned(w, "ts_dot");
-#define CALL(K) launch_mdot<K>(V, ld, n, c, w, out, false, ws, sm_count, st)
-  PPA_CPW_DISPATCH(c, CALL);
-#undef CALL
-}
-
-void cgs2_step(double* V, long long ld, int n, int c, double* w, double* Hcol, int* flag,
-               ReduceWorkspace& ws, int sm_count, cudaStream_t st) {
-  check_cols(c, "cgs2_step");
-  check_aligned(V, "cgs2_step");
-  check_aligned(w, "cgs2_step");
-  if (ld % 2) throw std::invalid_argument("cgs2_step: ld must be even");
-#define CALL(K) launch_cgs2<K>(V, ld, n, c, w, Hcol, flag, ws, sm_count, st)
-  PPA_CPW_DISPATCH(c, CALL);
-#undef CALL
-}
-
-void cgs1_pass(const double* V, long long ld, int n, int c, double* v, double* corr,
-               double* out_norm, ReduceWorkspace& ws, int sm_count, cudaStream_t st) {
-  check_cols(c, "cgs1_pass");
-  check_aligned(V, "cgs1_pass");
-  check_aligned(v, "cgs1_pass");
-#define CALL(K) launch_cgs1<K>(V, ld, n, c, v, corr, out_norm, ws, sm_count, st)
-  PPA_CPW_DISPATCH(c, CALL);
-#undef CALL
-}
-
-void col_sumsq(const double* Y, long long ld, int n, int p, double* out, ReduceWorkspace& ws,
-               int sm_count, cudaStream_t st) {
-  check_cols(p, "col_sumsq");
-  check_aligned(Y, "col_sumsq");
-#define CALL(K) launch_mdot<K>(Y, ld, n, p, nullptr, out, true, ws, sm_count, st)
-  PPA_CPW_DISPATCH(p, CALL);
-#undef CALL
 }
 
 void ts_combine(const double* V, long long ldv, int n, int d, const double* G, int p, double* Out,

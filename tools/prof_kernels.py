@@ -22,16 +22,23 @@ if what in ("all", "spmv"):
     for _ in range(3):
         ppa.apply_poly(roots, A, v, out)
 if what in ("all", "cgs"):
+    # real Arnoldi basis so every sweep (incl. the V[:,c] store) runs
     c = 40
-    ld = (n + 31) // 32 * 32
-    V = torch.randn((c + 1) * ld, dtype=torch.float64, device="cuda")
-    w = torch.randn(n, dtype=torch.float64, device="cuda")
+    st = ppa.arnoldi_init(v, n, c)
+    st.extend(A, c)
+    ld = st.ld
+    w0 = torch.empty(n, dtype=torch.float64, device="cuda")
+    ppa.spmv(A, st.V_ptr + 8 * ld * (c - 1), w0)
+    w = torch.empty_like(w0)
     Hc = torch.empty(c + 2, dtype=torch.float64, device="cuda")
     flag = torch.zeros(2, dtype=torch.int32, device="cuda")
     for _ in range(3):
-        ppa.cgs2_step(V, ld, n, c, w, Hc, flag)
+        w.copy_(w0)
+        ppa.cgs2_step(st.V_ptr, ld, n, c, w, Hc, flag)
+    assert int(flag[0].item()) == 0
     G = torch.randn(c * 20, dtype=torch.float64, device="cuda")
+    Y = torch.empty(20 * ld, dtype=torch.float64, device="cuda")
     for _ in range(2):
-        ppa.ts_combine(V, ld, n, c, G, 20, V, ld)
+        ppa.ts_combine(st.V_ptr, ld, n, c, G, 20, Y, ld)
 torch.cuda.synchronize()
 print("done")
