@@ -196,8 +196,8 @@ int ppa_normal_vector(long long n, unsigned long long seed, unsigned long long s
                       double* out) {
   return guard([&] {
     need(out, "ppa_normal_vector");
-    const uint64_t k = ppa::rng::key(seed, stream);
-    for (long long i = 0; i < n; ++i) out[i] = ppa::rng::normal_at(k, static_cast<uint64_t>(i));
+    const std::vector<double> v = ppa::rng::normal_vector(n, seed, stream);
+    std::copy(v.begin(), v.end(), out);
   });
 }
 

@@ -79,7 +79,7 @@ CheckOutcome check_pairs(const ArnoldiState& st, const RitzSet& set, int nev,
                            cudaMemcpyHostToDevice, s));
   const long long ldy = round_ld(st.n);
   Scratch Y(static_cast<size_t>(ldy) * p);
-  Scratch AY(static_cast<size_t>(ldy) * p);
+  Scratch AY(static_cast<size_t>(ldy) * 2);  // A y for one real check or one pair
   kern::ts_combine(st.V.get(), st.ld, st.n, d, gdev.get(), p, Y.get(), ldy, s);
   Scratch sums(static_cast<size_t>(p) + 3 * items.size() + 8);
   kern::col_sumsq(Y.get(), ldy, st.n, p, sums.get(), ctx.ws(), ctx.sm_count(), s);
@@ -90,7 +90,7 @@ CheckOutcome check_pairs(const ArnoldiState& st, const RitzSet& set, int nev,
   for (size_t t = 0; t < items.size(); ++t) {
     const Item& it = items[t];
     double* yr = Y.get() + static_cast<long long>(it.col) * ldy;
-    double* ar = AY.get() + static_cast<long long>(it.col) * ldy;
+    double* ar = AY.get();  // reuse is ordered on the stream
     if (!it.pair) {
       kern::div_value(yr, std::sqrt(hs[it.col]), st.n, s);
       rec.vops += d;
