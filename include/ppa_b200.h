@@ -102,6 +102,11 @@ int ppa_op_info(const ppa_op* op, int* dim, int* mvps_per_apply, double* nnzr, i
 int ppa_op_apply(const ppa_op* op, const double* x_dev, double* y_dev, ppa_cost* cost);
 /* Same with host vectors: H2D of x, apply, D2H of y (the end-to-end call) */
 int ppa_op_apply_host(const ppa_op* op, const double* x, double* y, ppa_cost* cost);
+/* Batch of `count` host vectors (X, Y: count x dim, vector i at X + i*dim).
+   H2D of vector i+1 and D2H of vector i-1 overlap the apply of vector i
+   (double-buffered, three streams).  Pinned X/Y give full PCIe bandwidth. */
+int ppa_op_apply_host_batch(const ppa_op* op, int count, const double* X, double* Y,
+                            ppa_cost* cost);
 /* CSR operators: bytes of one SpMV under the north-star byte model */
 int ppa_csr_model_bytes(const ppa_op* op, double* bytes, long long* nnz);
 

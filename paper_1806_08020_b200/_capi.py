@@ -105,6 +105,7 @@ def lib():
             "ppa_op_info": [vp, _ip, _ip, _dp, _ip],
             "ppa_op_apply": [vp, vp, vp, C.POINTER(CostRecord)],
             "ppa_op_apply_host": [vp, vp, vp, C.POINTER(CostRecord)],
+            "ppa_op_apply_host_batch": [vp, C.c_int, vp, vp, C.POINTER(CostRecord)],
             "ppa_csr_model_bytes": [vp, _dp, C.POINTER(C.c_longlong)],
             "ppa_apply_poly": [vp, vp, C.c_int, vp, vp, vp, C.POINTER(CostRecord)],
             "ppa_build_gmres_poly": [vp, vp, C.c_int, vp, vp, _ip, _ip, C.POINTER(CostRecord)],
@@ -321,6 +322,22 @@ class LinearOperator:
         rec = rec if rec is not None else CostRecord()
         _check(lib().ppa_op_apply_host(self._h, _np_ptr(x), _np_ptr(y), C.byref(rec)))
         return y
+
+    def apply_host_batch(self, X, Y=None, rec: Optional[CostRecord] = None):
+        """Apply to each row of X (count x dim, host) with H2D/compute/D2H
+        overlapped across rows.  X/Y may be numpy arrays or pinned torch CPU
+        tensors; returns Y."""
+        rec = rec if rec is not None else CostRecord()
+        if hasattr(X, "data_ptr"):
+            count = X.shape[0]
+            _check(lib().ppa_op_apply_host_batch(self._h, count, C.c_void_p(X.data_ptr()),
+                                                 C.c_void_p(Y.data_ptr()), C.byref(rec)))
+            return Y
+        X = np.ascontiguousarray(X, dtype=np.float64)
+        Y = np.empty_like(X) if Y is None else Y
+        _check(lib().ppa_op_apply_host_batch(self._h, X.shape[0], _np_ptr(X), _np_ptr(Y),
+                                             C.byref(rec)))
+        return Y
 
     def model_bytes(self):
         b = C.c_double()

@@ -288,6 +288,68 @@ int ppa_op_apply_host(const ppa_op* op, const double* x, double* y, ppa_cost* co
   });
 }
 
+int ppa_op_apply_host_batch(const ppa_op* op, int count, const double* X, double* Y,
+                            ppa_cost* cost) {
+  return guard([&] {
+    need(op, "ppa_op_apply_host_batch");
+    if (count < 0) throw std::invalid_argument("ppa_op_apply_host_batch: negative count");
+    if (count == 0) return;
+    need(X, "ppa_op_apply_host_batch");
+    need(Y, "ppa_op_apply_host_batch");
+    ppa::Context& ctx = ppa::current_context();
+    const cudaStream_t cs = ctx.stream();
+    const long long n = op->p->dim();
+    const size_t bytes = static_cast<size_t>(n) * sizeof(double);
+    // Double-buffered pipeline: H2D of vector i+1 and D2H of vector i-1 run on
+    // their own streams (PCIe copy engines) while the SMs apply the operator
+    // to vector i; events order the buffer reuse.
+    static thread_local cudaStream_t hin = nullptr, hout = nullptr;
+    if (!hin) {
+      PPA_CUDA(cudaStreamCreateWithFlags(&hin, cudaStreamNonBlocking));
+      PPA_CUDA(cudaStreamCreateWithFlags(&hout, cudaStreamNonBlocking));
+    }
+    ppa::Scratch din0(n), din1(n), dout0(n), dout1(n);
+    double* din[2] = {din0.get(), din1.get()};
+    double* dout[2] = {dout0.get(), dout1.get()};
+    cudaEvent_t ev[3][2];
+    for (auto& row : ev)
+      for (auto& e : row) PPA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    enum { kIn = 0, kComp = 1, kOut = 2 };
+    // buffers come from the stream-ordered pool of `cs`: make the copy streams wait
+    cudaEvent_t ready;
+    PPA_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    PPA_CUDA(cudaEventRecord(ready, cs));
+    PPA_CUDA(cudaStreamWaitEvent(hin, ready, 0));
+    PPA_CUDA(cudaStreamWaitEvent(hout, ready, 0));
+    ppa::CostRecord r;
+    for (int i = 0; i < count; ++i) {
+      const int b = i & 1;
+      if (i >= 2) PPA_CUDA(cudaStreamWaitEvent(hin, ev[kComp][b], 0));
+      PPA_CUDA(cudaMemcpyAsync(din[b], X + static_cast<size_t>(i) * n, bytes,
+                               cudaMemcpyHostToDevice, hin));
+      PPA_CUDA(cudaEventRecord(ev[kIn][b], hin));
+      PPA_CUDA(cudaStreamWaitEvent(cs, ev[kIn][b], 0));
+      if (i >= 2) PPA_CUDA(cudaStreamWaitEvent(cs, ev[kOut][b], 0));
+      op->p->apply(din[b], dout[b], r);
+      PPA_CUDA(cudaEventRecord(ev[kComp][b], cs));
+      PPA_CUDA(cudaStreamWaitEvent(hout, ev[kComp][b], 0));
+      PPA_CUDA(cudaMemcpyAsync(Y + static_cast<size_t>(i) * n, dout[b], bytes,
+                               cudaMemcpyDeviceToHost, hout));
+      PPA_CUDA(cudaEventRecord(ev[kOut][b], hout));
+    }
+    PPA_CUDA(cudaStreamSynchronize(hin));
+    PPA_CUDA(cudaStreamSynchronize(hout));
+    // the scratch buffers are released on `cs`: order that after the copies
+    PPA_CUDA(cudaEventRecord(ready, hout));
+    PPA_CUDA(cudaStreamWaitEvent(cs, ready, 0));
+    ctx.sync();
+    for (auto& row : ev)
+      for (auto& e : row) cudaEventDestroy(e);
+    cudaEventDestroy(ready);
+    add_cost(cost, r);
+  });
+}
+
 int ppa_csr_model_bytes(const ppa_op* op, double* bytes, long long* nnz) {
   return guard([&] {
     need(op, "ppa_csr_model_bytes");

@@ -119,24 +119,29 @@ __global__ void __launch_bounds__(T) k_spmv_rowblock(
   }
 }
 
-// SELL-32: one warp per 32-row slice.  Lane l owns row 32s+l; entry k of
-// the slice is one coalesced 128 B (col) + 256 B (value) request per warp,
-// and for stencil matrices the x gathers of a slice column are contiguous
-// too.  No shared memory and no barriers: every warp is independent, so the
-// SM keeps many more loads in flight than the row-block kernel.  Padding
-// entries (col < 0) are skipped, so each row is still summed left to right
-// with the CSR's own column order (bit-identical to the CPU loop).
+// SELL-32(-sigma): one warp per 32-row slice.  Lane l owns slice row 32s+l
+// (original row perm[32s+l] when the rows were sorted by length inside
+// sigma-windows, else 32s+l itself); entry k of the slice is one coalesced
+// 128 B (col) + 256 B (value) request per warp, and for stencil matrices the
+// x gathers of a slice column are contiguous too.  No shared memory and no
+// barriers: every warp is independent, so the SM keeps many more loads in
+// flight than the row-block kernel.  Padding entries (col < 0) are skipped,
+// so each row is still summed left to right in the CSR's own column order
+// (bit-identical to the CPU loop).
 constexpr int SELL_WARPS = 8;
 constexpr int SELL_UNROLL = 8;
 
-template <int MODE, bool COMPL>
+template <int MODE, bool COMPL, bool PERM>
 __global__ void __launch_bounds__(SELL_WARPS * 32) k_spmv_sell32(
     const long long* __restrict__ slice_ptr, const int* __restrict__ scol,
-    const double* __restrict__ sval, int n, int nslices, const double* __restrict__ x, double* y,
-    double c0, double c1, const double* o, const double* base) {
+    const double* __restrict__ sval, const int* __restrict__ perm, int n, int nslices,
+    const double* __restrict__ x, double* y, double c0, double c1, const double* o,
+    const double* base) {
   const int lane = threadIdx.x & 31;
   const int s = blockIdx.x * SELL_WARPS + (threadIdx.x >> 5);
   if (s >= nslices) return;
+  const int idx = s * 32 + lane;
+  const int r = (PERM && idx < n) ? __ldg(perm + idx) : idx;
   const long long b0 = slice_ptr[s];
   const int width = static_cast<int>((slice_ptr[s + 1] - b0) >> 5);
   const int* cp = scol + b0 + lane;
@@ -157,16 +162,22 @@ __global__ void __launch_bounds__(SELL_WARPS * 32) k_spmv_sell32(
       if (k0 + u < width && c[u] >= 0) sum = __dadd_rn(sum, __dmul_rn(v[u], __ldg(x + c[u])));
     }
   }
-  const int r = s * 32 + lane;
-  if (r < n) y[r] = epilogue<MODE, COMPL>(r, sum, x, c0, c1, o, base);
+  if (idx < n) y[r] = epilogue<MODE, COMPL>(r, sum, x, c0, c1, o, base);
 }
 
 template <int MODE, bool COMPL>
 void launch(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep, cudaStream_t st) {
   if (a.sell_val) {
     const int grid = (a.nslices + SELL_WARPS - 1) / SELL_WARPS;
-    k_spmv_sell32<MODE, COMPL><<<grid, SELL_WARPS * 32, 0, st>>>(
-        a.slice_ptr, a.sell_col, a.sell_val, a.n, a.nslices, x, y, ep.c0, ep.c1, ep.o, ep.base);
+    if (a.sell_perm) {
+      k_spmv_sell32<MODE, COMPL, true><<<grid, SELL_WARPS * 32, 0, st>>>(
+          a.slice_ptr, a.sell_col, a.sell_val, a.sell_perm, a.n, a.nslices, x, y, ep.c0, ep.c1,
+          ep.o, ep.base);
+    } else {
+      k_spmv_sell32<MODE, COMPL, false><<<grid, SELL_WARPS * 32, 0, st>>>(
+          a.slice_ptr, a.sell_col, a.sell_val, nullptr, a.n, a.nslices, x, y, ep.c0, ep.c1, ep.o,
+          ep.base);
+    }
     return;
   }
   k_spmv_rowblock<MODE, COMPL><<<a.nblocks, T, 0, st>>>(a.row_ptr, a.col_idx, a.values,
@@ -193,21 +204,36 @@ void spmv(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep, cud
   PPA_CUDA(cudaGetLastError());
 }
 
-bool build_sell32(const int* row_ptr, const int* col_idx, const double* values, int n,
+bool build_sell32(const int* row_ptr, const int* col_idx, const double* values, int n, int sigma,
                   std::vector<long long>& slice_ptr, std::vector<int>& cols,
-                  std::vector<double>& vals) {
+                  std::vector<double>& vals, std::vector<int>& perm) {
   const int ns = (n + 31) / 32;
+  auto len = [&](int r) { return row_ptr[r + 1] - row_ptr[r]; };
+  perm.clear();
+  if (sigma > 1) {
+    // sort rows by decreasing length inside each sigma-window (stable, so
+    // the layout is deterministic); rows never leave their window
+    perm.resize(n);
+    for (int i = 0; i < n; ++i) perm[i] = i;
+    for (int w0 = 0; w0 < n; w0 += sigma) {
+      const int w1 = std::min(n, w0 + sigma);
+      std::stable_sort(perm.begin() + w0, perm.begin() + w1,
+                       [&](int a, int b) { return len(a) > len(b); });
+    }
+  }
+  auto row_of = [&](int idx) { return perm.empty() ? idx : perm[idx]; };
   slice_ptr.assign(static_cast<size_t>(ns) + 1, 0);
   long long total = 0;
   for (int s = 0; s < ns; ++s) {
     int w = 0;
-    for (int r = s * 32; r < std::min(n, s * 32 + 32); ++r) w = std::max(w, row_ptr[r + 1] - row_ptr[r]);
+    for (int i = s * 32; i < std::min(n, s * 32 + 32); ++i) w = std::max(w, len(row_of(i)));
     total += 32LL * w;
     slice_ptr[s + 1] = total;
   }
   const long long nnz = row_ptr[n];
   if (static_cast<double>(total) > kSellMaxPadding * static_cast<double>(nnz) + 32.0 * 64) {
     slice_ptr.clear();
+    perm.clear();
     return false;
   }
   cols.assign(static_cast<size_t>(total), -1);
@@ -215,8 +241,9 @@ bool build_sell32(const int* row_ptr, const int* col_idx, const double* values, 
   for (int s = 0; s < ns; ++s) {
     const long long b0 = slice_ptr[s];
     for (int l = 0; l < 32; ++l) {
-      const int r = s * 32 + l;
-      if (r >= n) break;
+      const int i = s * 32 + l;
+      if (i >= n) break;
+      const int r = row_of(i);
       for (int p = row_ptr[r], k = 0; p < row_ptr[r + 1]; ++p, ++k) {
         cols[b0 + 32LL * k + l] = col_idx[p];
         vals[b0 + 32LL * k + l] = values[p];

@@ -104,10 +104,20 @@ CsrOperator::CsrOperator(const CsrMatrix& m, OperatorKind kind, std::vector<doub
   dev_.nblocks = static_cast<int>(blk.size()) - 1;
 
   std::vector<long long> sp;
-  std::vector<int> sc;
+  std::vector<int> sc, perm;
   std::vector<double> sv;
-  if (!std::getenv("PPA_DISABLE_SELL") &&
-      kern::build_sell32(m.row_ptr.data(), m.col_idx.data(), m.values.data(), n_, sp, sc, sv)) {
+  bool sell = false;
+  int sigma = 1;
+  if (!std::getenv("PPA_DISABLE_SELL")) {
+    sell = kern::build_sell32(m.row_ptr.data(), m.col_idx.data(), m.values.data(), n_, 1, sp, sc,
+                              sv, perm);
+    if (!sell && !std::getenv("PPA_DISABLE_SIGMA")) {
+      sigma = kern::kSellSigma;
+      sell = kern::build_sell32(m.row_ptr.data(), m.col_idx.data(), m.values.data(), n_, sigma,
+                                sp, sc, sv, perm);
+    }
+  }
+  if (sell) {
     slice_ptr_.resize(sp.size());
     sell_col_.resize(sc.size() + 32);
     sell_val_.resize(sv.size() + 32);
@@ -119,11 +129,18 @@ CsrOperator::CsrOperator(const CsrMatrix& m, OperatorKind kind, std::vector<doub
       PPA_CUDA(cudaMemcpy(sell_val_.get(), sv.data(), sv.size() * sizeof(double),
                           cudaMemcpyHostToDevice));
     }
+    if (!perm.empty()) {
+      sell_perm_.resize(perm.size());
+      PPA_CUDA(cudaMemcpy(sell_perm_.get(), perm.data(), perm.size() * sizeof(int),
+                          cudaMemcpyHostToDevice));
+      dev_.sell_perm = sell_perm_.get();
+    }
     dev_.slice_ptr = slice_ptr_.get();
     dev_.sell_col = sell_col_.get();
     dev_.sell_val = sell_val_.get();
     dev_.nslices = static_cast<int>(sp.size()) - 1;
     dev_.sell_entries = sp.back();
+    dev_.sell_sigma = sigma;
   }
 }
 

@@ -27,18 +27,24 @@ struct CsrDevice {
   const long long* slice_ptr = nullptr;  // [nslices+1]
   const int* sell_col = nullptr;
   const double* sell_val = nullptr;
+  const int* sell_perm = nullptr;  // slice row -> matrix row (nullptr: identity)
   int nslices = 0;
+  int sell_sigma = 1;
   long long sell_entries = 0;
 };
 
 /// SELL-32 is used when its padded entry count is at most this factor of nnz.
 constexpr double kSellMaxPadding = 1.15;
 
-/// Host-side SELL-32 construction from CSR (returns false when padding
-/// exceeds kSellMaxPadding).
-bool build_sell32(const int* row_ptr, const int* col_idx, const double* values, int n,
+/// Sorting window used when unsorted SELL-32 pads too much (irregular rows).
+constexpr int kSellSigma = 16384;
+
+/// Host-side SELL-32 construction from CSR.  sigma > 1 sorts rows by length
+/// inside sigma-row windows and returns the slice-row -> row permutation.
+/// Returns false when the padding exceeds kSellMaxPadding.
+bool build_sell32(const int* row_ptr, const int* col_idx, const double* values, int n, int sigma,
                   std::vector<long long>& slice_ptr, std::vector<int>& cols,
-                  std::vector<double>& vals);
+                  std::vector<double>& vals, std::vector<int>& perm);
 
 /// Row-block capacities of the streaming SpMV (must match spmv.cu).
 constexpr int kSpmvThreads = 256;

@@ -75,6 +75,7 @@ class CsrOperator final : public LinearOperator {
   long long nnz() const { return nnz_; }
   bool uses_sell() const { return dev_.sell_val != nullptr; }
   long long sell_entries() const { return dev_.sell_entries; }
+  int sell_sigma() const { return dev_.sell_sigma; }
   /// Bytes one SpMV moves under the north-star model:
   /// 12*nnz + 4*(n+1) + 8n (x) + 8n (y).
   double model_bytes() const {
@@ -87,7 +88,7 @@ class CsrOperator final : public LinearOperator {
   double nnzr_ = 0.0;
   OperatorKind kind_;
   std::vector<double> diag_;
-  DBuffer<int> row_ptr_, col_idx_, blk_row_, sell_col_;
+  DBuffer<int> row_ptr_, col_idx_, blk_row_, sell_col_, sell_perm_;
   DBuffer<double> values_, sell_val_;
   DBuffer<long long> slice_ptr_;
   kern::CsrDevice dev_;

@@ -48,6 +48,24 @@ def test_spmv_bit_exact(cuda, name, gen):
     assert np.array_equal(host(y), Ao.apply(x))
 
 
+@pytest.mark.parametrize("name,gen", MATRICES)
+@pytest.mark.parametrize("layout", ["csr_rowblock", "sell_unsorted_only"])
+def test_spmv_other_layouts_bit_exact(cuda, monkeypatch, name, gen, layout):
+    # the CSR row-block kernel (PPA_DISABLE_SELL) and SELL without sigma
+    # sorting (PPA_DISABLE_SIGMA: irregular rows fall back to the row-block path)
+    monkeypatch.setenv("PPA_DISABLE_SELL" if layout == "csr_rowblock" else "PPA_DISABLE_SIGMA", "1")
+    P, Q = gen(ppa.CsrMatrix), gen(O.Csr)
+    A = ppa.make_csr_operator(P)
+    x = O.normal_vector(P.n, 4, 9)
+    y = cuda.empty(P.n, dtype=cuda.float64, device="cuda")
+    A.apply(dev(cuda, x), y)
+    assert np.array_equal(host(y), O.csr_operator(Q).apply(x))
+    roots = _roots_mixed()
+    out = cuda.empty(P.n, dtype=cuda.float64, device="cuda")
+    ppa.apply_poly(roots, A, dev(cuda, x), out)
+    assert np.array_equal(host(out), O.apply_poly(roots, O.csr_operator(Q), x))
+
+
 def test_spmv_long_rows(cuda):
     # rows longer than one row block (2048 nnz) take the block-reduction path
     n = 6000
@@ -162,6 +180,18 @@ def test_apply_host_e2e(cuda):
     y = op.apply_host(x)
     ref = O.apply_poly(roots, O.csr_operator(O.Csr.laplacian_3d(10)), x)
     assert np.array_equal(y, ref)
+    # batched host API: H2D / compute / D2H overlapped across vectors
+    X = np.stack([O.normal_vector(P.n, 2, s) for s in range(5)])
+    rec = ppa.CostRecord()
+    Y = op.apply_host_batch(X, rec=rec)
+    assert rec.mvps == 5 * len(roots)
+    Ao = O.csr_operator(O.Csr.laplacian_3d(10))
+    for i in range(5):
+        assert np.array_equal(Y[i], O.apply_poly(roots, Ao, X[i]))
+    XT = cuda.from_numpy(X).pin_memory()
+    YT = cuda.empty_like(XT).pin_memory()
+    op.apply_host_batch(XT, YT)
+    assert np.array_equal(YT.numpy(), Y)
 
 
 @pytest.mark.parametrize("gen,deg", [(lambda M: M.laplacian_3d(14), 20),
