@@ -202,6 +202,43 @@ def test_arnoldi_relation_orthonormality():
     assert np.linalg.norm(D @ V[:, :30] - V @ H) <= 1e-9 * max(1, np.linalg.norm(H))
 
 
+def test_harmonic_one_step_kat():
+    # 1-step Arnoldi: the harmonic Ritz value is the root of the
+    # degree-1 GMRES polynomial, argmin_theta ||(I - A/theta) b||, i.e.
+    # theta = ||Ab||^2 / (b . Ab) (n >= m+1: diag[1,2,5])
+    d = np.array([1.0, 2.0, 5.0])
+    b = np.array([0.3, 0.5, 0.8])
+    r = O.arnoldi(O.diagonal_operator(d), b, 1)
+    theta = O.harmonic_from_H(r["H"], 1)[0]
+    Ab = d * b
+    assert theta.real == pytest.approx(Ab @ Ab / (b @ Ab), rel=1e-13)
+    ts = np.linspace(theta.real * 0.9, theta.real * 1.1, 2001)
+    res = [np.linalg.norm(b - Ab / t) for t in ts]
+    assert abs(ts[int(np.argmin(res))] - theta.real) < 1e-3 * theta.real
+
+
+def test_harmonic_reciprocal_rayleigh_ritz_kat():
+    # diag[1..10], d = 4: harmonic Ritz values are reciprocals of
+    # the Rayleigh-Ritz values of A^-1 on A K_d(A, b) (explicit projection)
+    d = np.arange(1.0, 11.0)
+    b = O.normal_vector(10, 5, 2)
+    r = O.arnoldi(O.diagonal_operator(d), b, 4)
+    hv = np.sort(O.harmonic_from_H(r["H"], 4).real)
+    K = np.stack([d ** k * b for k in range(1, 5)], axis=1)  # A K_4
+    Q, _ = np.linalg.qr(K)
+    ev = np.linalg.eigvals(Q.T @ np.diag(1.0 / d) @ Q)
+    assert np.allclose(hv, np.sort(1.0 / ev.real), rtol=1e-9)
+
+
+def test_arnoldi_invariant_subspace_spectrum():
+    # SPEC.md:152 (n >= m+1 form): diag[1,2,3,4] from (1,1,1,0)/sqrt3 spans an
+    # invariant 3-dim space; H_3 has eigenvalues {1,2,3} to 1e-12
+    r = O.arnoldi(O.diagonal_operator([1.0, 2.0, 3.0, 4.0]), np.array([1.0, 1, 1, 0]) / np.sqrt(3), 3)
+    ev = np.sort(np.linalg.eigvals(r["H"][:3, :3]).real)
+    assert np.allclose(ev, [1.0, 2.0, 3.0], atol=1e-12)
+    assert np.allclose(r["H"][:3, :3], r["H"][:3, :3].T, atol=1e-12)  # symmetric op -> tridiagonal
+
+
 def test_harmonic_full_dimension_equals_eigenvalues():
     # d = n: harmonic Ritz values are the exact eigenvalues
     d = np.array([1.0, 2.5, 4.0, 7.0, 11.0, 13.0])
