@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <limits>
 #include <stdexcept>
 
@@ -140,12 +141,17 @@ std::vector<PolyFactor> factor_plan(const PolyPrecond& p) {
 
 namespace {
 
-// Fused chain for a CSR base operator.  Each real factor is one SpMV launch
-// y = x + c0 (A x) (ping-pong between two buffers); a conjugate pair is a
-// plain SpMV t1 = A x followed by y = (x + c1 t1) + c0 (A t1), in place when
-// x is a scratch buffer.  The buffer of each launch is chosen backwards from
-// the end so the last launch writes `dst` directly; `complement_base`, when
-// set, is folded into that last launch (tau = I - pi, y = base - pi(A)x).
+// Fused chain for a CSR base operator.  The factors are grouped into passes:
+//   single real root : one SpMV launch, y = x + c0 (A x)
+//   conjugate pair   : t1 = A x, then y = (x + c1 t1) + c0 (A t1)
+//   two real roots   : when the matrix qualifies (banded SELL-32), one
+//                      matrix-powers launch applies both (kernels/mpk.cu)
+// A pair also runs as one matrix-powers launch when the matrix qualifies.
+// Every pass maps the current vector to a new buffer; buffers are assigned
+// backwards from the end so the last pass writes `dst` directly, and
+// `complement_base`, when set, is folded into that last pass (tau = I - pi,
+// y = base - pi(A) x).  Counters charge the reference's per-factor
+// increments (src/gmres_poly.cpp:129-143).
 void apply_poly_csr(const std::vector<PolyFactor>& plan, const CsrOperator& a, const double* v,
                     double* dst, const double* complement_base, CostRecord& rec) {
   Context& ctx = current_context();
@@ -160,47 +166,74 @@ void apply_poly_csr(const std::vector<PolyFactor>& plan, const CsrOperator& a, c
     }
     return;
   }
-  bool any_pair = false;
-  int reals = 0;
-  for (const PolyFactor& f : plan) {
-    any_pair |= f.pair;
-    reals += f.pair ? 0 : 1;
+  // Matrix-powers fusion is opt-in: it is bit-exact and halves HBM traffic
+  // (L2 reuse), but its cross-CTA waits make it slower than two plain
+  // launches on B200.
+  const char* mpk_env = std::getenv("PPA_ENABLE_MPK");
+  const bool mp = mpk_env && mpk_env[0] == '1' && kern::mp2_supported(a.device());
+  struct Pass {
+    int first;
+    int count;  // factors in the pass (1 or 2 real roots, or 1 pair)
+  };
+  std::vector<Pass> passes;
+  bool any_two = false;
+  for (int k = 0; k < K;) {
+    if (plan[k].pair) {
+      passes.push_back({k, 1});
+      any_two = true;
+      k += 1;
+    } else if (mp && k + 1 < K && !plan[k + 1].pair) {
+      passes.push_back({k, 2});
+      any_two = true;
+      k += 2;
+    } else {
+      passes.push_back({k, 1});
+      k += 1;
+    }
   }
+  const int P = static_cast<int>(passes.size());
   Scratch other(static_cast<size_t>(n));
-  Scratch t1buf(any_pair ? static_cast<size_t>(n) : 1);
-  // Backward buffer assignment: 0 -> dst, 1 -> other.
-  std::vector<int> target(K);
-  int need = 0;
-  for (int k = K - 1; k >= 0; --k) {
-    target[k] = need;
-    if (!plan[k].pair) need ^= 1;
-  }
+  Scratch t1buf(any_two ? static_cast<size_t>(n) : 1);
   double* bufs[2] = {dst, other.get()};
   const double* cur = v;
-  for (int k = 0; k < K; ++k) {
-    const PolyFactor& f = plan[k];
-    double* out = bufs[target[k]];
-    kern::EpiArgs ep;
-    ep.base = (k == K - 1) ? complement_base : nullptr;
-    if (!f.pair) {
+  for (int q = 0; q < P; ++q) {
+    const Pass& ps = passes[q];
+    double* out = bufs[(P - 1 - q) & 1];  // the last pass lands in dst
+    const double* base = (q == P - 1) ? complement_base : nullptr;
+    const PolyFactor& f = plan[ps.first];
+    if (ps.count == 2 || (f.pair && mp)) {
+      kern::Mp2Pass m;
+      m.pair = f.pair;
+      if (f.pair) {
+        m.a0 = f.c0;
+        m.a1 = f.c1;
+      } else {
+        m.a0 = f.c0;
+        m.b0 = plan[ps.first + 1].c0;
+      }
+      kern::spmv_mp2(a.device(), m, cur, t1buf.get(), out, base, ctx.mp_work(), ctx.sm_count(),
+                     st);
+    } else if (!f.pair) {
+      kern::EpiArgs ep;
+      ep.base = base;
       ep.mode = kern::Epi::real;
       ep.c0 = f.c0;
       kern::spmv(a.device(), cur, out, ep, st);
-      rec.mvps += 1;
-      rec.vops += 1;
     } else {
       kern::spmv(a.device(), cur, t1buf.get(), kern::EpiArgs{}, st);
+      kern::EpiArgs ep;
+      ep.base = base;
       ep.mode = kern::Epi::pair;
       ep.c0 = f.c0;
       ep.c1 = f.c1;
       ep.o = cur;
       kern::spmv(a.device(), t1buf.get(), out, ep, st);
-      rec.mvps += 2;
-      rec.vops += 2;
     }
+    const int mv = f.pair ? 2 : ps.count;
+    rec.mvps += mv;
+    rec.vops += mv;
     cur = out;
   }
-  (void)reals;
 }
 
 // Reference operation sequence over an arbitrary operator.

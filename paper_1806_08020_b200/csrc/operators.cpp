@@ -102,6 +102,11 @@ CsrOperator::CsrOperator(const CsrMatrix& m, OperatorKind kind, std::vector<doub
   dev_.values = values_.get();
   dev_.blk_row = blk_row_.get();
   dev_.nblocks = static_cast<int>(blk.size()) - 1;
+  int bw = 0;
+  for (int i = 0; i < n_; ++i) {
+    for (int p = m.row_ptr[i]; p < m.row_ptr[i + 1]; ++p) bw = std::max(bw, std::abs(m.col_idx[p] - i));
+  }
+  dev_.bandwidth = bw;
 
   std::vector<long long> sp;
   std::vector<int> sc, perm;

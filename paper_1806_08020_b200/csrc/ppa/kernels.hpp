@@ -31,7 +31,23 @@ struct CsrDevice {
   int nslices = 0;
   int sell_sigma = 1;
   long long sell_entries = 0;
+  int bandwidth = -1;  // max |col - row| over the entries (-1: unknown)
 };
+
+/// Two polynomial factors fused into one matrix-powers pass (mpk.cu):
+///   pair = false: y1 = x + a0 (A x),  y2 = y1 + b0 (A y1)   (two real roots)
+///   pair = true : t = A x (into y1),  y2 = (x + a1 t) + a0 (A t)  (conjugate pair)
+struct Mp2Pass {
+  bool pair = false;
+  double a0 = 0.0, a1 = 0.0, b0 = 0.0;
+};
+
+/// True when the fused two-level kernel applies: SELL-32 without row
+/// permutation and a bandwidth small against n.
+bool mp2_supported(const CsrDevice& a);
+/// One fused pass; x, y1, y2 distinct; `base` folds the complement into y2.
+void spmv_mp2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y1, double* y2,
+              const double* base, MpWork& w, int sm_count, cudaStream_t st);
 
 /// SELL-32 is used when its padded entry count is at most this factor of nnz.
 constexpr double kSellMaxPadding = 1.15;

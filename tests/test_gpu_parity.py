@@ -114,6 +114,38 @@ def test_apply_poly_bit_exact(cuda, kind):
     assert (rec.mvps, rec.vops) == (int(cost[0]), int(cost[2]))
 
 
+@pytest.mark.parametrize("kind", ["real_even", "real_odd", "mixed", "pairs_only"])
+@pytest.mark.parametrize("complement", [False, True])
+@pytest.mark.parametrize("mpk", ["1", "0"])
+def test_matrix_powers_fused_bit_exact(cuda, monkeypatch, kind, complement, mpk):
+    # n >= 65536 and small bandwidth: with PPA_ENABLE_MPK=1 consecutive factors
+    # run as fused two-level matrix-powers passes (kernels/mpk.cu); fused and
+    # plain chains must both equal the oracle bit for bit
+    monkeypatch.setenv("PPA_ENABLE_MPK", mpk)
+    gens = {"real_even": lambda M: M.laplacian_3d(48), "real_odd": lambda M: M.laplacian_3d(48),
+            "mixed": lambda M: M.convection_diffusion(300),
+            "pairs_only": lambda M: M.convection_diffusion_const(260, 0.5)}
+    roots = {"real_even": _roots_real(10, 10.0, 60000.0), "real_odd": _roots_real(9, 10.0, 60000.0),
+             "mixed": O.leja_order([4.5e6, 2e6 + 3e5j, 2e6 - 3e5j, 9e5, 1.2e5 + 4e4j,
+                                    1.2e5 - 4e4j, 1.5e4, 3e6, 6e5]),
+             "pairs_only": [3e5 + 2e4j, 3e5 - 2e4j, 5e4 + 5e3j, 5e4 - 5e3j]}[kind]
+    P, Q = gens[kind](ppa.CsrMatrix), gens[kind](O.Csr)
+    assert P.n >= 65536
+    mk = ppa.make_poly_complement_operator if complement else ppa.make_poly_operator
+    op = mk(ppa.make_csr_operator(P), roots)
+    opo = O.poly_operator(O.csr_operator(Q), roots, complement)
+    x = O.normal_vector(P.n, 6, 6)
+    y = cuda.empty(P.n, dtype=cuda.float64, device="cuda")
+    rec = op.apply(dev(cuda, x), y)
+    cost = np.zeros(3)
+    ref = opo.apply(x, cost)
+    assert np.array_equal(host(y), ref), rel(host(y), ref)
+    assert (rec.mvps, rec.vops) == (int(cost[0]), int(cost[2]))
+    # repeated applies reuse the per-context flags (epochs): still exact
+    op.apply(dev(cuda, x), y)
+    assert np.array_equal(host(y), ref)
+
+
 def test_apply_poly_eigvec_matches_eval(cuda):
     # SPEC.md gmres_poly invariant: on eigenvectors of a diagonal A, apply = eval
     d = np.arange(1.0, 201.0)
