@@ -154,6 +154,10 @@ void ppa_arnoldi_free(ppa_arnoldi* st);
 /* ---- raw device kernels -------------------------------------------------- */
 /* y = A x with a CSR operator (src/operators.cpp:39-48) */
 int ppa_spmv(const ppa_op* a, const double* x_dev, double* y_dev);
+/* AY = A Y for p column-major device vectors (multi-RHS SELL SpMM; each column
+   bit-identical to ppa_spmv); the solver's batched convergence check */
+int ppa_spmm(const ppa_op* a, const double* Y_dev, long long ldy, int p, double* AY_dev,
+             long long ldo);
 /* One CGS2 step (replaces MGS2 of src/arnoldi.cpp:129-150); Hcol_dev c+1, flag_dev int */
 int ppa_cgs2_step(double* V_dev, long long ld, int n, int c, double* w_dev, double* Hcol_dev,
                   int* flag_dev);

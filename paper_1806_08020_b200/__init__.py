@@ -39,6 +39,7 @@ from ._capi import (  # noqa: F401
     cgs2_step,
     ts_combine,
     spmv,
+    spmm,
     STREAM_NORM,
     STREAM_POLY,
     STREAM_ARNOLDI,

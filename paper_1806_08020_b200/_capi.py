@@ -122,6 +122,7 @@ def lib():
             "ppa_arnoldi_ritz_vector": [vp, C.c_int, C.c_int, vp, vp, _ip, C.POINTER(CostRecord)],
             "ppa_arnoldi_restart": [vp, C.c_int, C.c_int, C.POINTER(CostRecord), _ip],
             "ppa_spmv": [vp, vp, vp],
+            "ppa_spmm": [vp, vp, C.c_longlong, C.c_int, vp, C.c_longlong],
             "ppa_cgs2_step": [vp, C.c_longlong, C.c_int, C.c_int, vp, vp, vp],
             "ppa_ts_combine": [vp, C.c_longlong, C.c_int, C.c_int, vp, C.c_int, vp, C.c_longlong],
             "ppa_solve": [vp, C.POINTER(_SolveConfigC), C.POINTER(_SolveResultC)],
@@ -377,6 +378,11 @@ def make_poly_complement_operator(a: LinearOperator, roots, base_degree=None) ->
 
 def spmv(a: LinearOperator, x, y) -> None:
     _check(lib().ppa_spmv(a._h, _ptr(x), _ptr(y)))
+
+
+def spmm(a: LinearOperator, Y, ldy: int, p: int, AY, ldo: int) -> None:
+    """AY[:, j] = A Y[:, j], j < p (column-major device storage)."""
+    _check(lib().ppa_spmm(a._h, _ptr(Y), ldy, p, _ptr(AY), ldo))
 
 
 # -------------------------------------------------------------- polynomial --

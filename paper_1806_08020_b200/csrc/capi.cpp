@@ -558,6 +558,15 @@ int ppa_spmv(const ppa_op* a, const double* x, double* y) {
   });
 }
 
+int ppa_spmm(const ppa_op* a, const double* Y, long long ldy, int p, double* AY, long long ldo) {
+  return guard([&] {
+    need(a, "ppa_spmm");
+    const auto* c = dynamic_cast<const ppa::CsrOperator*>(a->p.get());
+    if (!c) throw std::invalid_argument("ppa_spmm: not a CSR operator");
+    ppa::kern::spmm(c->device(), Y, ldy, p, AY, ldo, ppa::current_context().stream());
+  });
+}
+
 int ppa_cgs2_step(double* V, long long ld, int n, int c, double* w, double* Hcol, int* flag) {
   return guard([&] {
     ppa::Context& ctx = ppa::current_context();

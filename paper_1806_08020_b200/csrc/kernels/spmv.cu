@@ -204,6 +204,72 @@ void spmv(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep, cud
   PPA_CUDA(cudaGetLastError());
 }
 
+namespace {
+
+// Multi-RHS SELL-32 (convergence check): each slice entry is
+// loaded once and applied to PB right-hand sides; per column the row sum is
+// the same left-to-right sequence as k_spmv_sell32.
+constexpr int SPMM_PB = 8;
+
+template <bool PERM>
+__global__ void __launch_bounds__(SELL_WARPS * 32) k_spmm_sell32(
+    const long long* __restrict__ slice_ptr, const int* __restrict__ scol,
+    const double* __restrict__ sval, const int* __restrict__ perm, int n, int nslices,
+    const double* __restrict__ Y, long long ldy, int p, double* __restrict__ AY, long long ldo) {
+  const int lane = threadIdx.x & 31;
+  const int s = blockIdx.x * SELL_WARPS + (threadIdx.x >> 5);
+  if (s >= nslices) return;
+  const int idx = s * 32 + lane;
+  const int r = (PERM && idx < n) ? __ldg(perm + idx) : idx;
+  const long long b0 = slice_ptr[s];
+  const int width = static_cast<int>((slice_ptr[s + 1] - b0) >> 5);
+  double sum[SPMM_PB];
+#pragma unroll
+  for (int j = 0; j < SPMM_PB; ++j) sum[j] = 0.0;
+  for (int k = 0; k < width; ++k) {
+    const int c = __ldcs(scol + b0 + 32LL * k + lane);
+    const double v = __ldcs(sval + b0 + 32LL * k + lane);
+    if (c < 0) continue;
+#pragma unroll
+    for (int j = 0; j < SPMM_PB; ++j) {
+      if (j < p) sum[j] = __dadd_rn(sum[j], __dmul_rn(v, __ldg(Y + c + j * ldy)));
+    }
+  }
+  if (idx < n) {
+#pragma unroll
+    for (int j = 0; j < SPMM_PB; ++j) {
+      if (j < p) AY[r + j * ldo] = sum[j];
+    }
+  }
+}
+
+}  // namespace
+
+void spmm(const CsrDevice& a, const double* Y, long long ldy, int p, double* AY, long long ldo,
+          cudaStream_t st) {
+  if (a.n == 0 || p <= 0) return;
+  if (!a.sell_val) {
+    for (int j = 0; j < p; ++j) spmv(a, Y + j * ldy, AY + j * ldo, EpiArgs{}, st);
+    return;
+  }
+  const int grid = (a.nslices + SELL_WARPS - 1) / SELL_WARPS;
+  for (int j0 = 0; j0 < p; j0 += SPMM_PB) {
+    const int pb = std::min(SPMM_PB, p - j0);
+    if (a.sell_perm) {
+      k_spmm_sell32<true><<<grid, SELL_WARPS * 32, 0, st>>>(a.slice_ptr, a.sell_col, a.sell_val,
+                                                            a.sell_perm, a.n, a.nslices,
+                                                            Y + j0 * ldy, ldy, pb, AY + j0 * ldo,
+                                                            ldo);
+    } else {
+      k_spmm_sell32<false><<<grid, SELL_WARPS * 32, 0, st>>>(a.slice_ptr, a.sell_col, a.sell_val,
+                                                             nullptr, a.n, a.nslices,
+                                                             Y + j0 * ldy, ldy, pb,
+                                                             AY + j0 * ldo, ldo);
+    }
+  }
+  PPA_CUDA(cudaGetLastError());
+}
+
 bool build_sell32(const int* row_ptr, const int* col_idx, const double* values, int n, int sigma,
                   std::vector<long long>& slice_ptr, std::vector<int>& cols,
                   std::vector<double>& vals, std::vector<int>& perm) {

@@ -90,6 +90,12 @@ struct EpiArgs {
 
 void spmv(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep, cudaStream_t st);
 
+/// AY[:,j] = A Y[:,j] for j < p (column-major, leading dims ldy / ldo):
+/// one matrix read per 8 columns with SELL-32, per-column SpMV otherwise.
+/// Every column is bit-identical to spmv() of that column.
+void spmm(const CsrDevice& a, const double* Y, long long ldy, int p, double* AY, long long ldo,
+          cudaStream_t st);
+
 /// Builds the row-block partition on the host from row_ptr.
 /// Returns the first row of each block (size nblocks+1).
 void build_row_blocks(const int* row_ptr_host, int n, int max_rows, int max_nnz,

@@ -79,7 +79,6 @@ CheckOutcome check_pairs(const ArnoldiState& st, const RitzSet& set, int nev,
                            cudaMemcpyHostToDevice, s));
   const long long ldy = round_ld(st.n);
   Scratch Y(static_cast<size_t>(ldy) * p);
-  Scratch AY(static_cast<size_t>(ldy) * 2);  // A y for one real check or one pair
   kern::ts_combine(st.V.get(), st.ld, st.n, d, gdev.get(), p, Y.get(), ldy, s);
   Scratch sums(static_cast<size_t>(p) + 3 * items.size() + 8);
   kern::col_sumsq(Y.get(), ldy, st.n, p, sums.get(), ctx.ws(), ctx.sm_count(), s);
@@ -87,30 +86,47 @@ CheckOutcome check_pairs(const ArnoldiState& st, const RitzSet& set, int nev,
   PPA_CUDA(cudaMemcpyAsync(hs.data(), sums.get(), p * sizeof(double), cudaMemcpyDeviceToHost, s));
   ctx.sync();
   double* outs = sums.get() + p;
-  for (size_t t = 0; t < items.size(); ++t) {
-    const Item& it = items[t];
+  // unit Ritz vectors (ritz_vector's counted normalisation, src/arnoldi.cpp:261-263)
+  for (const Item& it : items) {
     double* yr = Y.get() + static_cast<long long>(it.col) * ldy;
-    double* ar = AY.get();  // reuse is ordered on the stream
     if (!it.pair) {
       kern::div_value(yr, std::sqrt(hs[it.col]), st.n, s);
       rec.vops += d;
       rec.dots += 1;
       rec.vops += 2;
-      a.apply(yr, ar, rec);
+    } else {
+      const double nrm = std::sqrt(hs[it.col] + hs[it.col + 1]);
+      kern::div_value(yr, nrm, st.n, s);
+      kern::div_value(yr + ldy, nrm, st.n, s);
+      rec.vops += 2LL * d;
+      rec.dots += 2;
+      rec.vops += 4;
+    }
+  }
+  // A Y: one multi-RHS SpMM (the matrix is read once per 8 vectors) when A is
+  // a CSR operator, otherwise one counted apply per column.
+  const auto* csr = dynamic_cast<const CsrOperator*>(&a);
+  Scratch AY(static_cast<size_t>(ldy) * (csr ? p : 2));
+  if (csr) {
+    kern::spmm(csr->device(), Y.get(), ldy, p, AY.get(), ldy, s);
+    rec.mvps += p;
+  }
+  for (size_t t = 0; t < items.size(); ++t) {
+    const Item& it = items[t];
+    double* yr = Y.get() + static_cast<long long>(it.col) * ldy;
+    double* ar = csr ? AY.get() + static_cast<long long>(it.col) * ldy : AY.get();
+    if (!it.pair) {
+      if (!csr) a.apply(yr, ar, rec);
       kern::ritz_check_real(yr, ar, st.n, outs + 3 * t, ctx.ws(), ctx.sm_count(), s);
       rec.dots += 2;
       rec.vops += 3;
     } else {
       double* yi = yr + ldy;
       double* ai = ar + ldy;
-      const double nrm = std::sqrt(hs[it.col] + hs[it.col + 1]);
-      kern::div_value(yr, nrm, st.n, s);
-      kern::div_value(yi, nrm, st.n, s);
-      rec.vops += 2LL * d;
-      rec.dots += 2;
-      rec.vops += 4;
-      a.apply(yr, ar, rec);
-      a.apply(yi, ai, rec);
+      if (!csr) {
+        a.apply(yr, ar, rec);
+        a.apply(yi, ai, rec);
+      }
       kern::ritz_check_complex(yr, yi, ar, ai, st.n, outs + 3 * t, ctx.ws(), ctx.sm_count(), s);
       rec.dots += 6;
       rec.vops += 10;

@@ -383,3 +383,23 @@ def test_solve_double_small_vs_oracle(cuda):
     a, b = np.sort(r["eigenvalues"].real), np.sort(o["eigenvalues"].real)
     assert np.max(np.abs(a - b) / np.abs(b)) < 1e-4
     assert abs(r["cost"]["mvps"] - o["cost"]["mvps"]) <= 0.05 * o["cost"]["mvps"]
+
+
+@pytest.mark.parametrize("name,gen", MATRICES)
+@pytest.mark.parametrize("p", [1, 5, 8, 13])
+def test_spmm_columns_bit_exact(cuda, name, gen, p):
+    # multi-RHS SpMM of the convergence check: every column equals the oracle SpMV
+    P, Q = gen(ppa.CsrMatrix), gen(O.Csr)
+    A = ppa.make_csr_operator(P)
+    n = P.n
+    ld = (n + 31) // 32 * 32
+    Y = np.zeros((p, ld))
+    for j in range(p):
+        Y[j, :n] = O.normal_vector(n, 30 + j, 7)
+    Yd = dev(cuda, Y.ravel())
+    AYd = cuda.zeros(p * ld, dtype=cuda.float64, device="cuda")
+    ppa.spmm(A, Yd, ld, p, AYd, ld)
+    AY = host(AYd).reshape(p, ld)
+    Ao = O.csr_operator(Q)
+    for j in range(p):
+        assert np.array_equal(AY[j, :n], Ao.apply(Y[j, :n]))
