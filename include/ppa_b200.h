@@ -179,6 +179,9 @@ typedef struct ppa_solve_config {
   int max_cycles;
   unsigned long long seed;
   int allow_nev_above_k;
+  int damping;               /* 0 off, 1 auto_heuristic, 2 forced (DampingMode) */
+  double damping_alpha;      /* forced: start A^power b + alpha b */
+  int damping_power;
 } ppa_solve_config;
 
 /* EigResult (inc/solver.hpp:71-89); arrays supplied by the caller */
@@ -200,6 +203,7 @@ typedef struct ppa_solve_result {
   /* scalars (out) */
   int n_eig, n_poly, n_inner, n_cycles;
   int converged, cycles, composite_degree, poly_base_degree;
+  int discarded_probes;      /* damping probes whose basis was dropped */
   double rtol, max_err, norm_estimate;
   ppa_cost cost;
   double t_total, t_setup, t_extend, t_check, t_restart;
@@ -207,6 +211,24 @@ typedef struct ppa_solve_result {
 
 /* solve (inc/solver.hpp:94) or solve_double (inc/solver.hpp:111) */
 int ppa_solve(const ppa_op* a, const ppa_solve_config* cfg, ppa_solve_result* res);
+/* check_ideal_order (inc/solver.hpp:99): 1 if the condition holds */
+int ppa_check_ideal_order(const double* re, const double* im, int count, int nev, int* holds);
+/* damping_heuristic (inc/solver.hpp:105-106): the polynomial it settles on */
+int ppa_damping_heuristic(const ppa_op* a, const ppa_solve_config* cfg, double* re, double* im,
+                          int cap, int* nroots, ppa_cost* cost);
+
+/* ---- construction variants and ingest ------------------------ */
+/* make_block2 (inc/operators.hpp:87) and make_shifted (inc/operators.hpp:90) */
+int ppa_block2_operator(const ppa_op* a, ppa_op** out);
+int ppa_shifted_operator(const ppa_op* a, double mu, ppa_op** out);
+/* build_two_vector_poly (src/gmres_poly.cpp:228-264); b1/b2 device, length n */
+int ppa_build_two_vector_poly(const ppa_op* a, const double* b1_dev, const double* b2_dev,
+                              int degree, double* re, double* im, int* nroots, ppa_cost* cost);
+/* damped_start (src/gmres_poly.cpp:266-283): out_dev = (A^p b + alpha b)/||.|| */
+int ppa_damped_start(const ppa_op* a, const double* b_dev, double alpha, int power,
+                     double* out_dev, ppa_cost* cost);
+/* read_matrix_market (src/operators.cpp:246-305) */
+int ppa_read_matrix_market(const char* path, ppa_host_csr** out);
 
 #ifdef __cplusplus
 }

@@ -25,6 +25,7 @@ class _SolveOut(C.Structure):
                 ("cycle_max", _dp),
                 ("n_eig", C.c_int), ("n_poly", C.c_int), ("n_inner", C.c_int), ("n_cycles", C.c_int),
                 ("converged", C.c_int), ("cycles", C.c_int), ("composite", C.c_int),
+                ("discarded", C.c_int),
                 ("rtol", C.c_double), ("max_err", C.c_double), ("norm_est", C.c_double),
                 ("mvps", C.c_longlong), ("dots", C.c_longlong), ("vops", C.c_longlong),
                 ("wall", C.c_double)]
@@ -70,7 +71,13 @@ def lib():
             "orc_ritz_from_H": [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp],
             "orc_solve": [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int,
                           C.c_int, C.c_int, C.c_int, C.c_int, C.c_ulonglong, C.c_int,
-                          C.POINTER(_SolveOut)],
+                          C.c_int, C.c_double, C.c_int, C.POINTER(_SolveOut)],
+            "orc_block2_operator": [vp, C.POINTER(vp)],
+            "orc_shifted_operator": [vp, C.c_double, C.POINTER(vp)],
+            "orc_build_two_vector_poly": [vp, vp, vp, C.c_int, vp, vp, _ip, vp],
+            "orc_damped_start": [vp, vp, C.c_double, C.c_int, vp, vp],
+            "orc_check_ideal_order": [vp, vp, C.c_int, C.c_int, _ip],
+            "orc_read_matrix_market": [C.c_char_p, C.POINTER(vp)],
         }
         for k, a in sig.items():
             getattr(L, k).argtypes = a
@@ -315,8 +322,51 @@ def ritz_from_H(H, d, ordering=0):
     return re + 1j * im, rs
 
 
+def block2_operator(a: Op) -> Op:
+    h = vp()
+    _ck(lib().orc_block2_operator(a.h, C.byref(h)))
+    return Op(h, (a,))
+
+
+def shifted_operator(a: Op, mu) -> Op:
+    h = vp()
+    _ck(lib().orc_shifted_operator(a.h, C.c_double(mu), C.byref(h)))
+    return Op(h, (a,))
+
+
+def build_two_vector_poly(a: Op, b1, b2, degree, cost=None):
+    b1 = np.ascontiguousarray(b1, dtype=np.float64)
+    b2 = np.ascontiguousarray(b2, dtype=np.float64)
+    re, im, nr = np.zeros(max(degree, 1)), np.zeros(max(degree, 1)), C.c_int()
+    c = np.zeros(3) if cost is None else cost
+    _ck(lib().orc_build_two_vector_poly(a.h, _p(b1), _p(b2), degree, _p(re), _p(im), C.byref(nr), _p(c)))
+    return re[:nr.value] + 1j * im[:nr.value]
+
+
+def damped_start(a: Op, b, alpha, power, cost=None):
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    out = np.empty_like(b)
+    c = np.zeros(3) if cost is None else cost
+    _ck(lib().orc_damped_start(a.h, _p(b), C.c_double(alpha), power, _p(out), _p(c)))
+    return out
+
+
+def check_ideal_order(mu, nev):
+    re, im = _ri(mu)
+    h = C.c_int()
+    _ck(lib().orc_check_ideal_order(_p(re), _p(im), len(re), nev, C.byref(h)))
+    return bool(h.value)
+
+
+def read_matrix_market(path) -> Csr:
+    h = vp()
+    _ck(lib().orc_read_matrix_market(str(path).encode(), C.byref(h)))
+    return Csr(h)
+
+
 def solve(a: Op, m, k, nev, degree=0, rtol_multiplier=1e-8, rtol_absolute=0.0, stability=False,
-          double=None, max_cycles=100, seed=1, allow_nev_above_k=False):
+          double=None, max_cycles=100, seed=1, allow_nev_above_k=False, damping=0,
+          damping_alpha=0.0, damping_power=1):
     cap_r, cap_c = 4096, max(max_cycles, 1)
     er, ei, rs = np.zeros(nev), np.zeros(nev), np.zeros(nev)
     cv = np.zeros(nev, dtype=np.int32)
@@ -331,7 +381,7 @@ def solve(a: Op, m, k, nev, degree=0, rtol_multiplier=1e-8, rtol_absolute=0.0, s
     d1, d2 = double if double else (0, 0)
     _ck(lib().orc_solve(a.h, m, k, nev, degree, rtol_multiplier, rtol_absolute, int(bool(stability)),
                         1 if double else 0, d1, d2, max_cycles, seed, int(allow_nev_above_k),
-                        C.byref(o)))
+                        int(damping), C.c_double(damping_alpha), int(damping_power), C.byref(o)))
     ne = min(o.n_eig, nev)
     return {
         "eigenvalues": er[:ne] + 1j * ei[:ne], "residuals": rs[:ne].copy(),
@@ -339,7 +389,7 @@ def solve(a: Op, m, k, nev, degree=0, rtol_multiplier=1e-8, rtol_absolute=0.0, s
         "composite_degree": o.composite, "poly": pr[:o.n_poly] + 1j * pi[:o.n_poly],
         "inner_poly": ir[:o.n_inner] + 1j * ii[:o.n_inner], "rtol": o.rtol, "max_err": o.max_err,
         "norm_estimate": o.norm_est, "cost": {"mvps": o.mvps, "dots": o.dots, "vops": o.vops},
-        "cycle_max_residual": cm[:o.n_cycles].copy(), "wall": o.wall,
+        "cycle_max_residual": cm[:o.n_cycles].copy(), "wall": o.wall, "discarded": o.discarded,
     }
 
 

@@ -409,6 +409,97 @@ class CsrOp final : public Op {
   Vec diag_;
 };
 
+// src/operators.cpp:132-150
+class Block2Op final : public Op {
+ public:
+  explicit Block2Op(OpPtr a) : a_(std::move(a)) {}
+  int dim() const override { return 2 * a_->dim(); }
+  int mvps_per_apply() const override { return 2 * a_->mvps_per_apply(); }
+  double nnzr() const override { return a_->nnzr(); }
+  void apply(const double* x, double* y, Cost& c) const override {
+    const long n = a_->dim();
+    a_->apply(x, y, c);
+    a_->apply(x + n, y + n, c);
+  }
+
+ private:
+  OpPtr a_;
+};
+
+// src/operators.cpp:152-170
+class ShiftedOp final : public Op {
+ public:
+  ShiftedOp(OpPtr a, double mu) : a_(std::move(a)), mu_(mu) {}
+  int dim() const override { return a_->dim(); }
+  int mvps_per_apply() const override { return a_->mvps_per_apply(); }
+  double nnzr() const override { return a_->nnzr(); }
+  void apply(const double* x, double* y, Cost& c) const override {
+    a_->apply(x, y, c);
+    if (mu_ != 0.0) axpy(-mu_, x, y, dim(), c);
+  }
+
+ private:
+  OpPtr a_;
+  double mu_;
+};
+
+// src/operators.cpp:246-305
+Csr read_matrix_market(const std::string& path) {
+  FILE* f = std::fopen(path.c_str(), "r");
+  if (!f) throw std::runtime_error("read_matrix_market: cannot open " + path);
+  std::string text;
+  char buf[1 << 16];
+  size_t got;
+  while ((got = std::fread(buf, 1, sizeof(buf), f)) > 0) text.append(buf, got);
+  std::fclose(f);
+  size_t pos = 0;
+  auto next_line = [&](std::string& line) {
+    if (pos >= text.size()) return false;
+    size_t e = text.find('\n', pos);
+    if (e == std::string::npos) e = text.size();
+    line = text.substr(pos, e - pos);
+    pos = e + 1;
+    return true;
+  };
+  std::string line;
+  if (!next_line(line)) throw std::runtime_error("read_matrix_market: empty file");
+  char b1[64] = {0}, b2[64] = {0}, b3[64] = {0}, b4[64] = {0}, b5[64] = {0};
+  std::sscanf(line.c_str(), "%63s %63s %63s %63s %63s", b1, b2, b3, b4, b5);
+  auto low = [](std::string s) {
+    for (char& ch : s) ch = static_cast<char>(std::tolower(static_cast<unsigned char>(ch)));
+    return s;
+  };
+  const std::string obj = low(b2), fmt = low(b3), field = low(b4), sym = low(b5);
+  if (std::string(b1) != "%%MatrixMarket" || obj != "matrix" || fmt != "coordinate")
+    throw std::runtime_error("read_matrix_market: malformed header");
+  if (field != "real")
+    throw std::runtime_error("read_matrix_market: unsupported field '" + field + "' (only real)");
+  if (sym != "general" && sym != "symmetric")
+    throw std::runtime_error("read_matrix_market: unsupported symmetry '" + sym + "'");
+  while (next_line(line))
+    if (!line.empty() && line[0] != '%') break;
+  long long rows = 0, cols = 0, entries = 0;
+  if (std::sscanf(line.c_str(), "%lld %lld %lld", &rows, &cols, &entries) != 3 || rows <= 0 ||
+      cols <= 0)
+    throw std::runtime_error("read_matrix_market: bad size line");
+  if (rows != cols) throw std::runtime_error("read_matrix_market: matrix must be square");
+  std::vector<std::tuple<int, int, double>> t;
+  const char* p = text.c_str() + std::min(pos, text.size());
+  for (long long e = 0; e < entries; ++e) {
+    long long i, j;
+    double v;
+    int used = 0;
+    if (std::sscanf(p, " %lld %lld %lf%n", &i, &j, &v, &used) != 3)
+      throw std::runtime_error("read_matrix_market: truncated entry list");
+    p += used;
+    if (i < 1 || i > rows || j < 1 || j > cols)
+      throw std::runtime_error("read_matrix_market: index out of range");
+    t.emplace_back(int(i - 1), int(j - 1), v);
+    if (sym == "symmetric" && i != j) t.emplace_back(int(j - 1), int(i - 1), v);
+  }
+  return from_triplets(static_cast<int>(rows), std::move(t));
+}
+
 // ----------------------------------------------------------------- dense --
 struct Mat {
   int r = 0, c = 0;
@@ -864,6 +955,43 @@ Poly build_gmres_poly(const Op& a, const Vec& b, int degree, Cost& c) {
   return p;
 }
 
+// src/gmres_poly.cpp:228-264
+Poly build_two_vector_poly(const OpPtr& a, const Vec& b1, const Vec& b2, int degree, Cost& c) {
+  const long n = a->dim();
+  if (static_cast<long>(b1.size()) != n || static_cast<long>(b2.size()) != n)
+    throw std::invalid_argument("build_two_vector_poly: dimension mismatch");
+  const double n1 = norm(b1.data(), n, c), n2 = norm(b2.data(), n, c);
+  if (n1 == 0.0 || n2 == 0.0) throw std::invalid_argument("build_two_vector_poly: zero starting vector");
+  Vec bhat(2 * n);
+  for (long i = 0; i < n; ++i) {
+    bhat[i] = b1[i] / (n1 * std::sqrt(2.0));
+    bhat[n + i] = b2[i] / (n2 * std::sqrt(2.0));
+  }
+  c.vops += 2;
+  const Block2Op block(a);
+  return build_gmres_poly(block, bhat, degree, c);
+}
+
+// src/gmres_poly.cpp:266-283
+Vec damped_start(const Op& a, const Vec& b, double alpha, int power, Cost& c) {
+  if (power != 1 && power != 2) throw std::invalid_argument("damped_start: power must be 1 or 2");
+  if (alpha < 0.0) throw std::invalid_argument("damped_start: alpha < 0");
+  const long n = a.dim();
+  Vec w(n);
+  a.apply(b.data(), w.data(), c);
+  if (power == 2) {
+    Vec w2(n);
+    a.apply(w.data(), w2.data(), c);
+    w.swap(w2);
+  } else if (alpha != 0.0) {
+    axpy(alpha, b.data(), w.data(), n, c);
+  }
+  const double nw = norm(w.data(), n, c);
+  if (nw == 0.0) throw std::runtime_error("damped_start: damped vector vanished");
+  scale(w.data(), 1.0 / nw, n, c);
+  return w;
+}
+
 // src/gmres_poly.cpp:117-147
 void apply_poly(const Poly& p, const Op& a, const double* v, double* out, Cost& c) {
   const long n = a.dim();
@@ -994,13 +1122,28 @@ struct Config {
   int stability = 0, d1 = 0, d2 = 0, use_double = 0, max_cycles = 100;
   uint64_t seed = 1;
   int allow_nev_above_k = 0;
+  int damping = 0;  // 0 off, 1 auto heuristic, 2 forced
+  double damping_alpha = 0.0;
+  int damping_power = 1;
 };
+
+// inc/solver.hpp:96-99: |mu_1| <= ... <= |mu_nev| and
+// strictly below every remaining magnitude.
+bool check_ideal_order(const std::vector<cd>& mu, int nev) {
+  if (nev < 1 || nev > static_cast<int>(mu.size()))
+    throw std::invalid_argument("check_ideal_order: need 1 <= nev <= size");
+  for (int j = 1; j < nev; ++j)
+    if (std::abs(mu[j]) < std::abs(mu[j - 1])) return false;
+  for (size_t j = nev; j < mu.size(); ++j)
+    if (!(std::abs(mu[nev - 1]) < std::abs(mu[j]))) return false;
+  return true;
+}
 
 struct Result {
   std::vector<cd> mu;
   Vec res;
   std::vector<int> conv;
-  int converged = 0, cycles = 0, composite = 0;
+  int converged = 0, cycles = 0, composite = 0, discarded = 0;
   double rtol = 0.0, max_err = 0.0, norm_est = 0.0;
   Cost cost;
   Poly poly, inner;
@@ -1107,6 +1250,11 @@ Result solve(const OpPtr& A, const Config& g) {
   R.rtol = g.rtol_abs > 0 ? g.rtol_abs : g.rtol_mult * R.norm_est;
   OpPtr op = A;
   int ord = SMALLEST;
+  State probe_state;
+  Ritz probe_set;
+  std::vector<cd> probe_mu;
+  Vec probe_res;
+  bool has_probe = false;
   if (g.use_double) {
     if (g.d1 < 1 || g.d2 < 1) throw std::invalid_argument("solve_double: d1, d2 must be >= 1");
     Poly p1 = build_gmres_poly(*A, rng::gauss_vec(n, g.seed, rng::POLY), g.d1, c);
@@ -1119,21 +1267,80 @@ Result solve(const OpPtr& A, const Config& g) {
     R.poly = p2;
     ord = TARGET_ONE;
   } else if (g.degree > 0) {
-    Poly p = build_gmres_poly(*A, rng::gauss_vec(n, g.seed, rng::POLY), g.degree, c);
-    if (g.stability && p.roots.size() >= 2) p = add_stability_roots(p, 1 << 20);
+    const Vec b = rng::gauss_vec(n, g.seed, rng::POLY);
+    auto stab = [&](Poly p) { return (g.stability && p.roots.size() >= 2) ? add_stability_roots(p, 1 << 20) : p; };
+    Poly p;
+    if (g.damping == 1) {
+      // PAPER.md 6.3 / SPEC.md:169-177: probe one Arnoldi(m,k) cycle; on an
+      // ideal-order failure rebuild from Ab, then halve d until a probe passes
+      // or d = 1.  A passing probe becomes cycle 1.
+      Vec ab;
+      int d = g.degree;
+      bool damped = false;
+      for (;;) {
+        p = stab(build_gmres_poly(*A, damped ? ab : b, d, c));
+        OpPtr pop = std::make_shared<PolyOp>(A, p, false);
+        State ps = arnoldi_init(rng::gauss_vec(n, g.seed, rng::ARNOLDI), g.m, c);
+        arnoldi_extend(ps, *pop, g.m, c);
+        Ritz pset = ritz_pairs(ps, TARGET_ONE);
+        Result tmp;
+        tmp.rtol = R.rtol;
+        bool all_k;
+        double mx_k;
+        check_and_record(ps, pset, g.k, *A, tmp, all_k, mx_k, c);
+        const bool pass = static_cast<int>(tmp.mu.size()) >= g.nev && check_ideal_order(tmp.mu, g.nev);
+        if (pass) {
+          probe_state = std::move(ps);
+          probe_set = std::move(pset);
+          probe_mu = tmp.mu;
+          probe_res = tmp.res;
+          has_probe = true;
+          break;
+        }
+        ++R.discarded;
+        if (d <= 1) break;
+        if (!damped) {
+          ab = damped_start(*A, b, 0.0, 1, c);
+          damped = true;
+        } else {
+          d /= 2;
+        }
+      }
+    } else if (g.damping == 2) {
+      p = stab(build_gmres_poly(*A, damped_start(*A, b, g.damping_alpha, g.damping_power, c), g.degree, c));
+    } else {
+      p = stab(build_gmres_poly(*A, b, g.degree, c));
+    }
     R.composite = p.eff();
     op = std::make_shared<PolyOp>(A, p, false);
     R.poly = p;
     ord = TARGET_ONE;
   }
-  State st = arnoldi_init(rng::gauss_vec(n, g.seed, rng::ARNOLDI), g.m, c);
+  State st = has_probe ? std::move(probe_state)
+                       : arnoldi_init(rng::gauss_vec(n, g.seed, rng::ARNOLDI), g.m, c);
   R.max_err = std::numeric_limits<double>::infinity();
   for (int cyc = 1; cyc <= g.max_cycles; ++cyc) {
-    arnoldi_extend(st, *op, g.m, c);
-    const Ritz s = ritz_pairs(st, ord);
+    Ritz s;
     bool all;
     double mx;
-    check_and_record(st, s, g.nev, *A, R, all, mx, c);
+    if (cyc == 1 && has_probe) {
+      s = std::move(probe_set);
+      const int keep = std::min<int>(g.nev, static_cast<int>(probe_mu.size()));
+      R.mu.assign(probe_mu.begin(), probe_mu.begin() + keep);
+      R.res.assign(probe_res.begin(), probe_res.begin() + keep);
+      all = keep == g.nev;
+      mx = 0.0;
+      for (double r : R.res) {
+        mx = std::max(mx, r);
+        all = all && r <= R.rtol;
+      }
+      R.conv.assign(keep, 0);
+      for (int i = 0; i < keep; ++i) R.conv[i] = R.res[i] <= R.rtol;
+    } else {
+      arnoldi_extend(st, *op, g.m, c);
+      s = ritz_pairs(st, ord);
+      check_and_record(st, s, g.nev, *A, R, all, mx, c);
+    }
     R.cycles = cyc;
     R.cycle_max.push_back(mx);
     R.max_err = std::min(R.max_err, mx);
@@ -1415,7 +1622,7 @@ struct orc_solve_out {
   double* inner_im;
   double* cycle_max;
   int n_eig, n_poly, n_inner, n_cycles;
-  int converged, cycles, composite;
+  int converged, cycles, composite, discarded;
   double rtol, max_err, norm_est;
   long long mvps, dots, vops;
   double wall;
@@ -1423,9 +1630,13 @@ struct orc_solve_out {
 
 int orc_solve(const orc_op* a, int m, int k, int nev, int degree, double rtol_mult, double rtol_abs,
               int stability, int use_double, int d1, int d2, int max_cycles, unsigned long long seed,
-              int allow_nev_above_k, orc_solve_out* out) {
+              int allow_nev_above_k, int damping, double damping_alpha, int damping_power,
+              orc_solve_out* out) {
   return wrap([&] {
     orc::Config g;
+    g.damping = damping;
+    g.damping_alpha = damping_alpha;
+    g.damping_power = damping_power > 0 ? damping_power : 1;
     g.m = m;
     g.k = k;
     g.nev = nev;
@@ -1462,6 +1673,7 @@ int orc_solve(const orc_op* a, int m, int k, int nev, int degree, double rtol_mu
     out->converged = R.converged;
     out->cycles = R.cycles;
     out->composite = R.composite;
+    out->discarded = R.discarded;
     out->rtol = R.rtol;
     out->max_err = R.max_err;
     out->norm_est = R.norm_est;
@@ -1470,6 +1682,46 @@ int orc_solve(const orc_op* a, int m, int k, int nev, int degree, double rtol_mu
     out->vops = R.cost.vops;
     out->wall = R.cost.wall_seconds;
   });
+}
+
+int orc_block2_operator(const orc_op* a, orc_op** out) {
+  return wrap([&] { *out = new orc_op{std::make_shared<orc::Block2Op>(a->p)}; });
+}
+int orc_shifted_operator(const orc_op* a, double mu, orc_op** out) {
+  return wrap([&] { *out = new orc_op{std::make_shared<orc::ShiftedOp>(a->p, mu)}; });
+}
+int orc_build_two_vector_poly(const orc_op* a, const double* b1, const double* b2, int degree, double* re,
+                              double* im, int* nr, double* cost) {
+  return wrap([&] {
+    orc::Cost c;
+    const long n = a->p->dim();
+    const orc::Poly p = orc::build_two_vector_poly(a->p, orc::Vec(b1, b1 + n), orc::Vec(b2, b2 + n), degree, c);
+    for (int i = 0; i < p.eff(); ++i) {
+      re[i] = p.roots[i].real();
+      im[i] = p.roots[i].imag();
+    }
+    *nr = p.eff();
+    addc(cost, c);
+  });
+}
+int orc_damped_start(const orc_op* a, const double* b, double alpha, int power, double* out, double* cost) {
+  return wrap([&] {
+    orc::Cost c;
+    const long n = a->p->dim();
+    const orc::Vec w = orc::damped_start(*a->p, orc::Vec(b, b + n), alpha, power, c);
+    std::copy(w.begin(), w.end(), out);
+    addc(cost, c);
+  });
+}
+int orc_check_ideal_order(const double* re, const double* im, int count, int nev, int* holds) {
+  return wrap([&] {
+    std::vector<orc::cd> mu;
+    for (int i = 0; i < count; ++i) mu.emplace_back(re[i], im[i]);
+    *holds = orc::check_ideal_order(mu, nev) ? 1 : 0;
+  });
+}
+int orc_read_matrix_market(const char* path, orc_csr** out) {
+  return wrap([&] { *out = new orc_csr{orc::read_matrix_market(path)}; });
 }
 
 // cpu_baseline / reference arm: time `reps` applications of the first

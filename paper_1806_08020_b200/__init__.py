@@ -40,6 +40,13 @@ from ._capi import (  # noqa: F401
     ts_combine,
     spmv,
     spmm,
+    check_ideal_order,
+    damping_heuristic,
+    make_block2,
+    make_shifted,
+    build_two_vector_poly,
+    damped_start,
+    read_matrix_market,
     STREAM_NORM,
     STREAM_POLY,
     STREAM_ARNOLDI,

@@ -49,7 +49,8 @@ class _SolveConfigC(C.Structure):
                 ("rtol_multiplier", C.c_double), ("rtol_absolute", C.c_double),
                 ("variant", C.c_int), ("stability", C.c_int), ("double_d1", C.c_int),
                 ("double_d2", C.c_int), ("use_double", C.c_int), ("max_cycles", C.c_int),
-                ("seed", C.c_ulonglong), ("allow_nev_above_k", C.c_int)]
+                ("seed", C.c_ulonglong), ("allow_nev_above_k", C.c_int),
+                ("damping", C.c_int), ("damping_alpha", C.c_double), ("damping_power", C.c_int)]
 
 
 _dp = C.POINTER(C.c_double)
@@ -64,6 +65,7 @@ class _SolveResultC(C.Structure):
                 ("n_eig", C.c_int), ("n_poly", C.c_int), ("n_inner", C.c_int),
                 ("n_cycles", C.c_int), ("converged", C.c_int), ("cycles", C.c_int),
                 ("composite_degree", C.c_int), ("poly_base_degree", C.c_int),
+                ("discarded_probes", C.c_int),
                 ("rtol", C.c_double), ("max_err", C.c_double), ("norm_estimate", C.c_double),
                 ("cost", CostRecord),
                 ("t_total", C.c_double), ("t_setup", C.c_double), ("t_extend", C.c_double),
@@ -126,6 +128,14 @@ def lib():
             "ppa_cgs2_step": [vp, C.c_longlong, C.c_int, C.c_int, vp, vp, vp],
             "ppa_ts_combine": [vp, C.c_longlong, C.c_int, C.c_int, vp, C.c_int, vp, C.c_longlong],
             "ppa_solve": [vp, C.POINTER(_SolveConfigC), C.POINTER(_SolveResultC)],
+            "ppa_check_ideal_order": [vp, vp, C.c_int, C.c_int, _ip],
+            "ppa_damping_heuristic": [vp, C.POINTER(_SolveConfigC), vp, vp, C.c_int, _ip,
+                                      C.POINTER(CostRecord)],
+            "ppa_block2_operator": [vp, C.POINTER(vp)],
+            "ppa_shifted_operator": [vp, C.c_double, C.POINTER(vp)],
+            "ppa_build_two_vector_poly": [vp, vp, vp, C.c_int, vp, vp, _ip, C.POINTER(CostRecord)],
+            "ppa_damped_start": [vp, vp, C.c_double, C.c_int, vp, C.POINTER(CostRecord)],
+            "ppa_read_matrix_market": [C.c_char_p, C.POINTER(vp)],
         }
         for name, args in sigs.items():
             f = getattr(L, name)
@@ -556,14 +566,19 @@ class SolveConfig:
     max_cycles: int = 100
     seed: int = 1
     allow_nev_above_k: bool = False
+    damping: str = "off"          # off | auto_heuristic | forced
+    damping_alpha: float = 0.0
+    damping_power: int = 1
     reference: Sequence[complex] = field(default_factory=list)
 
     def _c(self, use_double: bool) -> _SolveConfigC:
+        damp = {"off": 0, "auto_heuristic": 1, "forced": 2}[self.damping]
         return _SolveConfigC(self.m, self.k, self.nev, self.degree, self.rtol_multiplier,
                              self.rtol_absolute or 0.0, 1 if self.variant == "harmonic" else 0,
                              1 if self.stability == "pof_auto" else 0, self.double_d1,
                              self.double_d2, 1 if use_double else 0, self.max_cycles, self.seed,
-                             1 if self.allow_nev_above_k else 0)
+                             1 if self.allow_nev_above_k else 0, damp, self.damping_alpha,
+                             self.damping_power)
 
 
 def _solve(a: LinearOperator, cfg: SolveConfig, use_double: bool) -> dict:
@@ -598,6 +613,7 @@ def _solve(a: LinearOperator, cfg: SolveConfig, use_double: bool) -> dict:
         "cost": {"mvps": r.cost.mvps, "dots": r.cost.dots, "vops": r.cost.vops,
                  "nnzr": r.cost.nnzr},
         "cycle_max_residual": cyc[:r.n_cycles].copy(),
+        "discarded_probes": r.discarded_probes,
         "timing": {"total": r.t_total, "setup": r.t_setup, "extend": r.t_extend,
                    "check": r.t_check, "restart": r.t_restart},
     }
@@ -607,6 +623,67 @@ def _solve(a: LinearOperator, cfg: SolveConfig, use_double: bool) -> dict:
             1 for z, ok in zip(eig, out["converged_flags"])
             if ok and np.any(np.abs(z - ref) <= 1e-6 * np.abs(ref))))
     return out
+
+
+def check_ideal_order(mu, nev: int) -> bool:
+    """check_ideal_order (inc/solver.hpp:99)."""
+    re, im = _roots(mu)
+    h = C.c_int()
+    _check(lib().ppa_check_ideal_order(_np_ptr(re), _np_ptr(im), len(re), nev, C.byref(h)))
+    return bool(h.value)
+
+
+def damping_heuristic(a: LinearOperator, cfg: SolveConfig, rec: Optional[CostRecord] = None):
+    """damping_heuristic (inc/solver.hpp:105-106): the polynomial it settles on."""
+    cap = max(8 * cfg.degree, 64)
+    re, im = np.zeros(cap), np.zeros(cap)
+    nr = C.c_int()
+    rec = rec if rec is not None else CostRecord()
+    c = cfg._c(False)
+    _check(lib().ppa_damping_heuristic(a._h, C.byref(c), _np_ptr(re), _np_ptr(im), cap,
+                                       C.byref(nr), C.byref(rec)))
+    return re[:nr.value] + 1j * im[:nr.value]
+
+
+def make_block2(a: LinearOperator) -> LinearOperator:
+    """make_block2 (inc/operators.hpp:87): diag(A, A), 2 mvps per apply."""
+    h = C.c_void_p()
+    _check(lib().ppa_block2_operator(a._h, C.byref(h)))
+    return LinearOperator(h, keep=(a,))
+
+
+def make_shifted(a: LinearOperator, mu: float) -> LinearOperator:
+    """make_shifted (inc/operators.hpp:90): v -> Av - mu v."""
+    h = C.c_void_p()
+    _check(lib().ppa_shifted_operator(a._h, C.c_double(mu), C.byref(h)))
+    return LinearOperator(h, keep=(a,))
+
+
+def build_two_vector_poly(a: LinearOperator, b1, b2, degree: int,
+                          rec: Optional[CostRecord] = None) -> np.ndarray:
+    """build_two_vector_poly (src/gmres_poly.cpp:228-264); b1, b2 device vectors."""
+    re, im = np.zeros(max(degree, 1)), np.zeros(max(degree, 1))
+    nr = C.c_int()
+    rec = rec if rec is not None else CostRecord()
+    _check(lib().ppa_build_two_vector_poly(a._h, _ptr(b1), _ptr(b2), degree, _np_ptr(re),
+                                           _np_ptr(im), C.byref(nr), C.byref(rec)))
+    return re[:nr.value] + 1j * im[:nr.value]
+
+
+def damped_start(a: LinearOperator, b, alpha: float, power: int, out,
+                 rec: Optional[CostRecord] = None):
+    """damped_start (src/gmres_poly.cpp:266-283) into the device vector `out`."""
+    rec = rec if rec is not None else CostRecord()
+    _check(lib().ppa_damped_start(a._h, _ptr(b), C.c_double(alpha), power, _ptr(out),
+                                  C.byref(rec)))
+    return rec
+
+
+def read_matrix_market(path: str) -> "CsrMatrix":
+    """read_matrix_market (src/operators.cpp:246-305)."""
+    h = C.c_void_p()
+    _check(lib().ppa_read_matrix_market(str(path).encode(), C.byref(h)))
+    return CsrMatrix(h)
 
 
 def solve(a: LinearOperator, cfg: SolveConfig) -> dict:

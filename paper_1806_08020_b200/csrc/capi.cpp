@@ -91,12 +91,50 @@ void need(const void* p, const char* what) {
   if (!p) throw std::invalid_argument(std::string(what) + ": null pointer");
 }
 
+ppa::SolveConfig to_config(const ppa_solve_config& c) {
+  ppa::SolveConfig cfg;
+  cfg.m = c.m;
+  cfg.k = c.k;
+  cfg.nev = c.nev;
+  cfg.degree = c.degree;
+  cfg.rtol_multiplier = c.rtol_multiplier;
+  if (c.rtol_absolute > 0) cfg.rtol_absolute = c.rtol_absolute;
+  cfg.variant = c.variant ? ppa::RestartVariant::harmonic : ppa::RestartVariant::ritz;
+  cfg.stability = c.stability ? ppa::StabilityMode::pof_auto : ppa::StabilityMode::off;
+  cfg.double_d1 = c.double_d1;
+  cfg.double_d2 = c.double_d2;
+  cfg.max_cycles = c.max_cycles;
+  cfg.seed = c.seed;
+  cfg.allow_nev_above_k = c.allow_nev_above_k != 0;
+  cfg.damping = c.damping == 1   ? ppa::DampingMode::auto_heuristic
+                : c.damping == 2 ? ppa::DampingMode::forced
+                                 : ppa::DampingMode::off;
+  cfg.damping_alpha = c.damping_alpha;
+  cfg.damping_power = c.damping_power > 0 ? c.damping_power : 1;
+  return cfg;
+}
+
+ppa_op* wrap_op(ppa::OperatorPtr p) {
+  auto* o = new ppa_op;
+  o->p = std::move(p);
+  return o;
+}
+
+void roots_out(const ppa::PolyPrecond& p, double* re, double* im, int cap, int* nroots) {
+  if (p.effective_degree() > cap) throw std::invalid_argument("root output capacity too small");
+  for (int i = 0; i < p.effective_degree(); ++i) {
+    re[i] = p.roots[i].real();
+    im[i] = p.roots[i].imag();
+  }
+  if (nroots) *nroots = p.effective_degree();
+}
+
 }  // namespace
 
 extern "C" {
 
 const char* ppa_last_error(void) { return t_err.c_str(); }
-int ppa_abi_version(void) { return 1; }
+int ppa_abi_version(void) { return 2; }
 
 int ppa_device_info(int* sm_count, double* l2_bytes) {
   return guard([&] {
@@ -586,21 +624,10 @@ int ppa_solve(const ppa_op* a, const ppa_solve_config* c, ppa_solve_result* res)
     need(a, "ppa_solve");
     need(c, "ppa_solve");
     need(res, "ppa_solve");
-    ppa::SolveConfig cfg;
-    cfg.m = c->m;
-    cfg.k = c->k;
-    cfg.nev = c->nev;
-    cfg.degree = c->degree;
-    cfg.rtol_multiplier = c->rtol_multiplier;
-    if (c->rtol_absolute > 0) cfg.rtol_absolute = c->rtol_absolute;
-    cfg.variant = c->variant ? ppa::RestartVariant::harmonic : ppa::RestartVariant::ritz;
-    cfg.stability = c->stability ? ppa::StabilityMode::pof_auto : ppa::StabilityMode::off;
-    cfg.double_d1 = c->double_d1;
-    cfg.double_d2 = c->double_d2;
-    cfg.max_cycles = c->max_cycles;
-    cfg.seed = c->seed;
-    cfg.allow_nev_above_k = c->allow_nev_above_k != 0;
+    const ppa::SolveConfig cfg = to_config(*c);
     const ppa::EigResult r = c->use_double ? ppa::solve_double(a->p, cfg) : ppa::solve(a->p, cfg);
+    res->discarded_probes = 0;
+    for (const ppa::CycleStats& h : r.history) res->discarded_probes += h.discarded_probe ? 1 : 0;
     res->n_eig = static_cast<int>(r.eigenvalues.size());
     for (int i = 0; i < res->n_eig && i < res->cap_nev; ++i) {
       if (res->eig_re) res->eig_re[i] = r.eigenvalues[i].real();
@@ -635,6 +662,70 @@ int ppa_solve(const ppa_op* a, const ppa_solve_config* c, ppa_solve_result* res)
     res->t_extend = r.timing.extend;
     res->t_check = r.timing.check;
     res->t_restart = r.timing.restart;
+  });
+}
+
+int ppa_check_ideal_order(const double* re, const double* im, int count, int nev, int* holds) {
+  return guard([&] {
+    need(holds, "ppa_check_ideal_order");
+    *holds = ppa::check_ideal_order(roots_of(re, im, count), nev) ? 1 : 0;
+  });
+}
+
+int ppa_damping_heuristic(const ppa_op* a, const ppa_solve_config* c, double* re, double* im,
+                          int cap, int* nroots, ppa_cost* cost) {
+  return guard([&] {
+    need(a, "ppa_damping_heuristic");
+    need(c, "ppa_damping_heuristic");
+    ppa::CostRecord r;
+    const ppa::PolyPrecond p = ppa::damping_heuristic(a->p, to_config(*c), r);
+    roots_out(p, re, im, cap, nroots);
+    add_cost(cost, r);
+  });
+}
+
+int ppa_block2_operator(const ppa_op* a, ppa_op** out) {
+  return guard([&] {
+    need(a, "ppa_block2_operator");
+    need(out, "ppa_block2_operator");
+    *out = wrap_op(ppa::make_block2(a->p));
+  });
+}
+
+int ppa_shifted_operator(const ppa_op* a, double mu, ppa_op** out) {
+  return guard([&] {
+    need(a, "ppa_shifted_operator");
+    need(out, "ppa_shifted_operator");
+    *out = wrap_op(ppa::make_shifted(a->p, mu));
+  });
+}
+
+int ppa_build_two_vector_poly(const ppa_op* a, const double* b1, const double* b2, int degree,
+                              double* re, double* im, int* nroots, ppa_cost* cost) {
+  return guard([&] {
+    need(a, "ppa_build_two_vector_poly");
+    ppa::CostRecord r;
+    const ppa::PolyPrecond p = ppa::build_two_vector_poly(a->p, b1, b2, degree, r);
+    roots_out(p, re, im, std::max(degree, 1), nroots);
+    add_cost(cost, r);
+  });
+}
+
+int ppa_damped_start(const ppa_op* a, const double* b, double alpha, int power, double* out,
+                     ppa_cost* cost) {
+  return guard([&] {
+    need(a, "ppa_damped_start");
+    ppa::CostRecord r;
+    ppa::damped_start(*a->p, b, alpha, power, out, r);
+    add_cost(cost, r);
+  });
+}
+
+int ppa_read_matrix_market(const char* path, ppa_host_csr** out) {
+  return guard([&] {
+    need(path, "ppa_read_matrix_market");
+    need(out, "ppa_read_matrix_market");
+    *out = wrap(ppa::read_matrix_market(path));
   });
 }
 

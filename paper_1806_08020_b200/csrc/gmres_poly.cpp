@@ -114,6 +114,55 @@ PolyPrecond build_gmres_poly(const LinearOperator& a, const double* b, int degre
   return p;
 }
 
+PolyPrecond build_two_vector_poly(const OperatorPtr& a, const double* b1, const double* b2,
+                                  int degree, CostRecord& rec) {
+  if (!a || !b1 || !b2) throw std::invalid_argument("build_two_vector_poly: dimension mismatch");
+  Context& ctx = current_context();
+  const long long n = a->dim();
+  const double n1 = ctx.nrm2_sync(b1, n);
+  const double n2 = ctx.nrm2_sync(b2, n);
+  rec.dots += 2;
+  rec.vops += 2;
+  if (n1 == 0.0 || n2 == 0.0) {
+    throw std::invalid_argument("build_two_vector_poly: zero starting vector");
+  }
+  Scratch bhat(static_cast<size_t>(2 * n));
+  kern::copy(b1, bhat.get(), n, ctx.stream());
+  kern::copy(b2, bhat.get() + n, n, ctx.stream());
+  kern::div_value(bhat.get(), n1 * std::sqrt(2.0), n, ctx.stream());
+  kern::div_value(bhat.get() + n, n2 * std::sqrt(2.0), n, ctx.stream());
+  rec.vops += 2;  // the two rescalings
+  const OperatorPtr block = make_block2(a);
+  PolyPrecond p = build_gmres_poly(*block, bhat.get(), degree, rec);
+  p.provenance = PolyProvenance::two_vector;
+  return p;
+}
+
+void damped_start(const LinearOperator& a, const double* b, double alpha, int power, double* out,
+                  CostRecord& rec) {
+  if (power != 1 && power != 2) throw std::invalid_argument("damped_start: power must be 1 or 2");
+  if (alpha < 0.0) throw std::invalid_argument("damped_start: alpha < 0");
+  Context& ctx = current_context();
+  const long long n = a.dim();
+  if (power == 2) {
+    Scratch w(static_cast<size_t>(n));
+    a.apply(b, w.get(), rec);
+    a.apply(w.get(), out, rec);
+  } else {
+    a.apply(b, out, rec);
+    if (alpha != 0.0) {
+      kern::axpy(alpha, b, out, n, ctx.stream());
+      ++rec.vops;
+    }
+  }
+  const double nw = ctx.nrm2_sync(out, n);
+  ++rec.dots;
+  ++rec.vops;
+  if (nw == 0.0) throw std::runtime_error("damped_start: damped vector vanished");
+  kern::scale(out, 1.0 / nw, n, ctx.stream());
+  ++rec.vops;
+}
+
 std::vector<PolyFactor> factor_plan(const PolyPrecond& p) {
   std::vector<PolyFactor> plan;
   const size_t nr = p.roots.size();

@@ -3,9 +3,12 @@
 #include "ppa/operators.hpp"
 
 #include <algorithm>
+#include <cctype>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
+#include <sstream>
 #include <stdexcept>
 
 #include "ppa/rng.hpp"
@@ -169,6 +172,108 @@ OperatorPtr make_diagonal(std::vector<double> d) {
   for (int i = 0; i <= m.n; ++i) m.row_ptr[i] = i;
   for (int i = 0; i < m.n; ++i) m.col_idx[i] = i;
   return std::make_shared<CsrOperator>(m, OperatorKind::diagonal, std::move(d));
+}
+
+namespace {
+
+class Block2Operator final : public LinearOperator {
+ public:
+  explicit Block2Operator(OperatorPtr a) : a_(std::move(a)) {
+    if (!a_) throw std::invalid_argument("make_block2: null operator");
+  }
+  int dim() const override { return 2 * a_->dim(); }
+  OperatorKind kind() const override { return OperatorKind::block2; }
+  int mvps_per_apply() const override { return 2 * a_->mvps_per_apply(); }
+  double nnzr() const override { return a_->nnzr(); }
+  void apply(const double* x, double* y, CostRecord& rec) const override {
+    const long long n = a_->dim();
+    a_->apply(x, y, rec);
+    a_->apply(x + n, y + n, rec);
+  }
+
+ private:
+  OperatorPtr a_;
+};
+
+class ShiftedOperator final : public LinearOperator {
+ public:
+  ShiftedOperator(OperatorPtr a, double mu) : a_(std::move(a)), mu_(mu) {
+    if (!a_) throw std::invalid_argument("make_shifted: null operator");
+  }
+  int dim() const override { return a_->dim(); }
+  OperatorKind kind() const override { return OperatorKind::shifted; }
+  int mvps_per_apply() const override { return a_->mvps_per_apply(); }
+  double nnzr() const override { return a_->nnzr(); }
+  void apply(const double* x, double* y, CostRecord& rec) const override {
+    a_->apply(x, y, rec);
+    if (mu_ != 0.0) {
+      kern::axpy(-mu_, x, y, dim(), current_context().stream());
+      ++rec.vops;
+    }
+  }
+
+ private:
+  OperatorPtr a_;
+  double mu_;
+};
+
+std::string lower(std::string s) {
+  std::transform(s.begin(), s.end(), s.begin(), [](unsigned char c) { return std::tolower(c); });
+  return s;
+}
+
+}  // namespace
+
+OperatorPtr make_block2(OperatorPtr a) { return std::make_shared<Block2Operator>(std::move(a)); }
+
+OperatorPtr make_shifted(OperatorPtr a, double mu) {
+  return std::make_shared<ShiftedOperator>(std::move(a), mu);
+}
+
+CsrMatrix read_matrix_market(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) throw std::runtime_error("read_matrix_market: cannot open " + path);
+  std::string line;
+  if (!std::getline(in, line)) throw std::runtime_error("read_matrix_market: empty file");
+  std::istringstream head(line);
+  std::string banner, object, format, field, symmetry;
+  head >> banner >> object >> format >> field >> symmetry;
+  object = lower(object);
+  format = lower(format);
+  field = lower(field);
+  symmetry = lower(symmetry);
+  if (banner != "%%MatrixMarket" || object != "matrix" || format != "coordinate") {
+    throw std::runtime_error("read_matrix_market: malformed header");
+  }
+  if (field != "real") {
+    throw std::runtime_error("read_matrix_market: unsupported field '" + field + "' (only real)");
+  }
+  const bool sym = symmetry == "symmetric";
+  if (!sym && symmetry != "general") {
+    throw std::runtime_error("read_matrix_market: unsupported symmetry '" + symmetry + "'");
+  }
+  while (std::getline(in, line)) {
+    if (!line.empty() && line[0] != '%') break;
+  }
+  std::istringstream size_line(line);
+  long long rows = 0, cols = 0, entries = 0;
+  if (!(size_line >> rows >> cols >> entries) || rows <= 0 || cols <= 0) {
+    throw std::runtime_error("read_matrix_market: bad size line");
+  }
+  if (rows != cols) throw std::runtime_error("read_matrix_market: matrix must be square");
+  std::vector<std::tuple<int, int, double>> trip;
+  trip.reserve(static_cast<size_t>(entries) * (sym ? 2 : 1));
+  for (long long e = 0; e < entries; ++e) {
+    long long i = 0, j = 0;
+    double v = 0.0;
+    if (!(in >> i >> j >> v)) throw std::runtime_error("read_matrix_market: truncated entry list");
+    if (i < 1 || i > rows || j < 1 || j > cols) {
+      throw std::runtime_error("read_matrix_market: index out of range");
+    }
+    trip.emplace_back(static_cast<int>(i - 1), static_cast<int>(j - 1), v);
+    if (sym && i != j) trip.emplace_back(static_cast<int>(j - 1), static_cast<int>(i - 1), v);
+  }
+  return CsrMatrix::from_triplets(static_cast<int>(rows), std::move(trip));
 }
 
 // ---------------------------------------------------------- generators --

@@ -59,6 +59,17 @@ std::complex<double> eval_poly(const PolyPrecond& p, std::complex<double> z);
 PofReport compute_pof(const PolyPrecond& p);
 PolyPrecond add_stability_roots(const PolyPrecond& p, int max_copies_per_root = 1 << 20);
 
+/// One polynomial from two start vectors: GMRES on diag(A, A) with the
+/// stacked start [b1; b2], halves rescaled to norm 1/sqrt(2)
+/// (src/gmres_poly.cpp:228-264).  b1, b2: device vectors of length n.
+PolyPrecond build_two_vector_poly(const OperatorPtr& a, const double* b1, const double* b2,
+                                  int degree, CostRecord& rec);
+
+/// Damped GMRES start A^power b + alpha b (alpha with power 1), normalised,
+/// into `out` (device, length n) (src/gmres_poly.cpp:266-283).
+void damped_start(const LinearOperator& a, const double* b, double alpha, int power, double* out,
+                  CostRecord& rec);
+
 /// pi(A) (or tau(A) = I - pi(A)) as an operator (src/gmres_poly.cpp:287-328).
 OperatorPtr make_poly_operator(OperatorPtr a, PolyPrecond p);
 OperatorPtr make_poly_complement_operator(OperatorPtr a, PolyPrecond p);

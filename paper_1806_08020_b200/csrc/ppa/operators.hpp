@@ -97,6 +97,15 @@ class CsrOperator final : public LinearOperator {
 OperatorPtr make_csr_operator(const CsrMatrix& matrix);
 /// Diagonal operator (src/operators.cpp:89-111), stored as a diagonal CSR.
 OperatorPtr make_diagonal(std::vector<double> diag_values);
+/// 2n-dimensional diag(A, A); one apply costs two applications of A
+/// (src/operators.cpp:132-150).
+OperatorPtr make_block2(OperatorPtr a);
+/// v -> Av - mu v (src/operators.cpp:152-170).
+OperatorPtr make_shifted(OperatorPtr a, double mu);
+
+/// Strict Matrix Market coordinate reader, real general/symmetric
+/// (src/operators.cpp:246-305); symmetric storage is expanded.
+CsrMatrix read_matrix_market(const std::string& path);
 
 // ------------------------------------------------------- generators -----
 // Deterministic synthetic matrices (BASELINE.json configs; DESIGN.md

@@ -94,5 +94,7 @@ EigResult solve(const OperatorPtr& a, const SolveConfig& cfg);
 EigResult solve_double(const OperatorPtr& a, const SolveConfig& cfg);
 double operator_norm_estimate(const LinearOperator& a, unsigned long long seed, CostRecord& rec);
 bool check_ideal_order(const std::vector<std::complex<double>>& mu, int nev);
+/// PAPER.md section 6.3 heuristic (inc/solver.hpp:101-106).
+PolyPrecond damping_heuristic(const OperatorPtr& a, const SolveConfig& cfg, CostRecord& rec);
 
 }  // namespace ppa

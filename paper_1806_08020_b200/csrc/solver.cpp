@@ -159,29 +159,73 @@ CheckOutcome check_pairs(const ArnoldiState& st, const RitzSet& set, int nev,
 }
 
 // Cycle loop shared by solve and solve_double.
+// One full first cycle (extend + Ritz pairs + checks of `nchk` pairs): the
+// damping heuristic's probe, reusable as cycle 1 of the solve.
+struct FirstCycle {
+  ArnoldiState st;
+  RitzSet set;
+  CheckOutcome chk;
+  int start_dim = 0;
+};
+
+RitzSet select_pairs(const ArnoldiState& st, const SolveConfig& cfg, RitzOrdering ordering) {
+  return cfg.variant == RestartVariant::harmonic ? harmonic_restart_selection(st, ordering)
+                                                 : ritz_pairs(st, ordering);
+}
+
+FirstCycle first_cycle(const LinearOperator& a, const LinearOperator& op, const SolveConfig& cfg,
+                       RitzOrdering ordering, int nchk, CostRecord& rec) {
+  const int n = a.dim();
+  DBuffer<double> v0 = upload(rng::normal_vector(n, cfg.seed, rng::kArnoldiStart));
+  FirstCycle f;
+  f.st = arnoldi_init(v0.get(), n, cfg.m, rec);
+  f.start_dim = f.st.cur_dim;
+  arnoldi_extend(f.st, op, cfg.m, rec);
+  f.set = select_pairs(f.st, cfg, ordering);
+  f.chk = check_pairs(f.st, f.set, nchk, a, rec);
+  return f;
+}
+
 void run_cycles(const LinearOperator& a, const LinearOperator& op, const SolveConfig& cfg,
-                RitzOrdering ordering, EigResult& res, CostRecord& rec) {
+                RitzOrdering ordering, EigResult& res, CostRecord& rec,
+                FirstCycle* probe = nullptr) {
   Context& ctx = current_context();
   const int n = a.dim();
-  const std::vector<double> v0h = rng::normal_vector(n, cfg.seed, rng::kArnoldiStart);
-  DBuffer<double> v0 = upload(v0h);
-  ArnoldiState st = arnoldi_init(v0.get(), n, cfg.m, rec);
+  ArnoldiState st;
+  if (probe) {
+    st = std::move(probe->st);
+  } else {
+    DBuffer<double> v0 = upload(rng::normal_vector(n, cfg.seed, rng::kArnoldiStart));
+    st = arnoldi_init(v0.get(), n, cfg.m, rec);
+  }
+  (void)ctx;
   res.max_err = std::numeric_limits<double>::infinity();
   for (int cycle = 1; cycle <= cfg.max_cycles; ++cycle) {
     CycleStats cs;
     cs.cycle = cycle;
-    cs.start_dim = st.cur_dim;
+    RitzSet set;
+    CheckOutcome chk;
     auto t0 = Clock::now();
-    arnoldi_extend(st, op, cfg.m, rec);
-    res.timing.extend += seconds_since(t0);
-    cs.end_dim = st.cur_dim;
-
-    t0 = Clock::now();
-    const RitzSet set = cfg.variant == RestartVariant::harmonic
-                            ? harmonic_restart_selection(st, ordering)
-                            : ritz_pairs(st, ordering);
-    CheckOutcome chk = check_pairs(st, set, cfg.nev, a, rec);
-    res.timing.check += seconds_since(t0);
+    if (cycle == 1 && probe) {
+      // the passing damping probe is this solve's first cycle (SPEC.md
+      // solver design decisions): its checks cover the first k >= nev pairs
+      cs.start_dim = probe->start_dim;
+      cs.end_dim = st.cur_dim;
+      set = std::move(probe->set);
+      chk = std::move(probe->chk);
+      const int keep = std::min<int>(cfg.nev, static_cast<int>(chk.mu.size()));
+      chk.mu.resize(keep);
+      chk.res.resize(keep);
+    } else {
+      cs.start_dim = st.cur_dim;
+      arnoldi_extend(st, op, cfg.m, rec);
+      res.timing.extend += seconds_since(t0);
+      cs.end_dim = st.cur_dim;
+      t0 = Clock::now();
+      set = select_pairs(st, cfg, ordering);
+      chk = check_pairs(st, set, cfg.nev, a, rec);
+      res.timing.check += seconds_since(t0);
+    }
     cs.real_checks = chk.real_checks;
     cs.pair_checks = chk.pair_checks;
     double mx = 0.0;
@@ -209,7 +253,75 @@ void run_cycles(const LinearOperator& a, const LinearOperator& op, const SolveCo
   }
 }
 
+PolyPrecond stabilise(PolyPrecond p, const SolveConfig& cfg) {
+  if (cfg.stability == StabilityMode::pof_auto && p.roots.size() >= 2) {
+    return add_stability_roots(p);
+  }
+  return p;
+}
+
+// The damping heuristic of PAPER.md section 6.3: probe one
+// Arnoldi(m,k) cycle on pi(A); if the Rayleigh quotients of the first k pairs
+// fail the ideal order condition, rebuild pi from the damped start Ab, then
+// keep halving the degree (rebuilding from Ab) until a probe passes or d = 1.
+// A passing probe is handed back for reuse as the solve's first cycle;
+// failed probes are logged as discarded cycles.  All probe costs count.
+PolyPrecond damping_search(const OperatorPtr& a, const SolveConfig& cfg, CostRecord& rec,
+                           std::vector<CycleStats>& history, std::optional<FirstCycle>& keep) {
+  const int n = a->dim();
+  DBuffer<double> b = upload(rng::normal_vector(n, cfg.seed, rng::kPolyStart));
+  DBuffer<double> ab;
+  int d = cfg.degree;
+  bool damped = false;
+  for (;;) {
+    const double* start = damped ? ab.get() : b.get();
+    PolyPrecond p = stabilise(build_gmres_poly(*a, start, d, rec), cfg);
+    if (damped) {
+      p.provenance = PolyProvenance::damped;
+      p.damping_power = 1;
+    }
+    const OperatorPtr op = make_poly_operator(a, p);
+    FirstCycle f = first_cycle(*a, *op, cfg, RitzOrdering::target_one, cfg.k, rec);
+    const bool pass = static_cast<int>(f.chk.mu.size()) >= cfg.nev &&
+                      check_ideal_order(f.chk.mu, cfg.nev);
+    if (pass || d <= 1) {
+      if (pass) keep.emplace(std::move(f));
+      if (!pass) {
+        CycleStats cs;
+        cs.discarded_probe = true;
+        cs.start_dim = f.start_dim;
+        cs.end_dim = f.st.cur_dim;
+        history.push_back(cs);
+      }
+      return p;
+    }
+    CycleStats cs;
+    cs.discarded_probe = true;
+    cs.start_dim = f.start_dim;
+    cs.end_dim = f.st.cur_dim;
+    cs.real_checks = f.chk.real_checks;
+    cs.pair_checks = f.chk.pair_checks;
+    history.push_back(cs);
+    if (!damped) {
+      ab.resize(static_cast<size_t>(n));
+      damped_start(*a, b.get(), 0.0, 1, ab.get(), rec);
+      damped = true;
+    } else {
+      d /= 2;
+    }
+  }
+}
+
 }  // namespace
+
+PolyPrecond damping_heuristic(const OperatorPtr& a, const SolveConfig& cfg, CostRecord& rec) {
+  if (!a) throw std::invalid_argument("damping_heuristic: null operator");
+  cfg.validate();
+  if (cfg.degree < 1) throw std::invalid_argument("damping_heuristic: degree < 1");
+  std::vector<CycleStats> history;
+  std::optional<FirstCycle> probe;
+  return damping_search(a, cfg, rec, history, probe);
+}
 
 void SolveConfig::validate() const {
   if (m < 2) throw std::invalid_argument("SolveConfig: m must be >= 2");
@@ -301,11 +413,25 @@ EigResult solve(const OperatorPtr& a, const SolveConfig& cfg) {
 
   OperatorPtr op = a;
   RitzOrdering ordering = RitzOrdering::smallest_magnitude;
+  std::optional<FirstCycle> probe;
   if (cfg.degree > 0) {
-    DBuffer<double> b = upload(rng::normal_vector(a->dim(), cfg.seed, rng::kPolyStart));
-    PolyPrecond p = build_gmres_poly(*a, b.get(), cfg.degree, rec);
-    if (cfg.stability == StabilityMode::pof_auto && p.roots.size() >= 2) {
-      p = add_stability_roots(p);
+    PolyPrecond p;
+    if (cfg.damping == DampingMode::auto_heuristic) {
+      p = damping_search(a, cfg, rec, res.history, probe);
+    } else {
+      DBuffer<double> b = upload(rng::normal_vector(a->dim(), cfg.seed, rng::kPolyStart));
+      if (cfg.damping == DampingMode::forced) {
+        // damped start A^power b + alpha b (section 6)
+        DBuffer<double> bd(static_cast<size_t>(a->dim()));
+        damped_start(*a, b.get(), cfg.damping_alpha, cfg.damping_power, bd.get(), rec);
+        p = build_gmres_poly(*a, bd.get(), cfg.degree, rec);
+        p.provenance = PolyProvenance::damped;
+        p.damping_alpha = cfg.damping_alpha;
+        p.damping_power = cfg.damping_power;
+      } else {
+        p = build_gmres_poly(*a, b.get(), cfg.degree, rec);
+      }
+      p = stabilise(p, cfg);
     }
     res.composite_degree = p.effective_degree();
     op = make_poly_operator(a, p);
@@ -314,7 +440,7 @@ EigResult solve(const OperatorPtr& a, const SolveConfig& cfg) {
   }
   current_context().sync();
   res.timing.setup = seconds_since(t0);
-  run_cycles(*a, *op, cfg, ordering, res, rec);
+  run_cycles(*a, *op, cfg, ordering, res, rec, probe ? &*probe : nullptr);
   current_context().sync();
   res.timing.total = seconds_since(t_all);
   rec.wall_seconds = res.timing.total;
