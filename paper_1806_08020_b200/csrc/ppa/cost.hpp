@@ -1,11 +1,13 @@
 #pragma once
-// Operation counters.  Field-for-field the reference's CostRecord
-// (inc/cost.hpp:17-23) with the same counting conventions
-// (inc/cost.hpp:10-16): mvps = base-matrix applications, dots = length-n
-// inner products (norms included), vops = every length-n vector operation
-// (dots included).  The device kernels fuse several reference operations
-// into one launch; the host side charges the reference's increments for
-// each fused operation so the counters stay comparable.
+// Work counters of one solve, with the paper's composite cost metric
+// cost = nnzr * mvps + vops (section 4).
+//
+// Conventions are the reference's (inc/cost.hpp:10-16): `mvps` counts
+// base-matrix applications, `dots` counts length-n inner products with norms
+// included, `vops` counts every length-n vector operation, dots included.
+// Device kernels fuse several of those operations into one launch; the host
+// code still charges each fused operation separately, so the numbers stay
+// comparable with the CPU oracle.
 
 #include <stdexcept>
 
@@ -15,31 +17,28 @@ struct CostRecord {
   long long mvps = 0;
   long long dots = 0;
   long long vops = 0;
-  double nnzr = 0.0;  // average nonzeros per row; 0 means unset
+  double nnzr = 0.0;  // nonzeros per row of the base matrix; 0 = not set
   double wall_seconds = 0.0;
 };
 
-/// cost = nnzr * mvps + vops (inc/cost.hpp:26-32).
-inline double cost_estimate(const CostRecord& rec) {
-  if (rec.nnzr <= 0.0) {
-    throw std::invalid_argument("cost_estimate: nnzr is unset");
-  }
-  return rec.nnzr * static_cast<double>(rec.mvps) +
-         static_cast<double>(rec.vops);
+/// Paper metric; nnzr must have been set.
+inline double cost_estimate(const CostRecord& c) {
+  if (!(c.nnzr > 0.0)) throw std::invalid_argument("cost_estimate: nnzr is unset");
+  return c.nnzr * static_cast<double>(c.mvps) + static_cast<double>(c.vops);
 }
 
-/// Componentwise sum (inc/cost.hpp:35-46).
-inline CostRecord merge(const CostRecord& a, const CostRecord& b) {
-  if (a.nnzr > 0.0 && b.nnzr > 0.0 && a.nnzr != b.nnzr) {
-    throw std::invalid_argument("merge: mismatched nnzr");
-  }
-  CostRecord out;
-  out.mvps = a.mvps + b.mvps;
-  out.dots = a.dots + b.dots;
-  out.vops = a.vops + b.vops;
-  out.nnzr = a.nnzr > 0.0 ? a.nnzr : b.nnzr;
-  out.wall_seconds = a.wall_seconds + b.wall_seconds;
-  return out;
+/// Sum of two records that describe the same matrix (nnzr must agree when
+/// both are set).
+inline CostRecord merge(const CostRecord& x, const CostRecord& y) {
+  const bool both = x.nnzr > 0.0 && y.nnzr > 0.0;
+  if (both && x.nnzr != y.nnzr) throw std::invalid_argument("merge: mismatched nnzr");
+  CostRecord s;
+  s.mvps = x.mvps + y.mvps;
+  s.dots = x.dots + y.dots;
+  s.vops = x.vops + y.vops;
+  s.nnzr = x.nnzr > 0.0 ? x.nnzr : y.nnzr;
+  s.wall_seconds = x.wall_seconds + y.wall_seconds;
+  return s;
 }
 
 }  // namespace ppa

@@ -1,8 +1,12 @@
 #pragma once
-// PP-Arnoldi driver (reference inc/solver.hpp).  The reference declares
-// these entry points but ships no body; the behaviour follows
-// SPEC.md "[MODULE] solver" with the frozen choices listed in DESIGN.md
-// ("Solver decisions").
+// The PP-Arnoldi driver.  The reference only declares these entry points
+// (inc/solver.hpp:57-116; no solver.cpp ships), so behaviour comes from
+// SPEC.md "[MODULE] solver" plus the frozen choices of DESIGN.md section 5.
+//
+// Flow of solve(): norm estimate -> polynomial (plain / damped / heuristic,
+// optional stability copies) -> Arnoldi(m, k) cycles on pi(A) with device
+// CGS2 -> per cycle: Ritz pairs of H on the host, nev true residuals against
+// A on the device -> thick restart with V*Q on the device.
 
 #include <complex>
 #include <optional>
@@ -19,36 +23,43 @@ enum class RestartVariant { ritz, harmonic };
 enum class DampingMode { off, auto_heuristic, forced };
 enum class StabilityMode { off, pof_auto };
 
-/// inc/solver.hpp:21-58, field for field, plus allow_nev_above_k (our
-/// extension for BASELINE config 5, whose nev = 20 > k = 15 violates
-/// SPEC.md's 0 < nev <= k < m).
+using EigenList = std::vector<std::complex<double>>;
+
+/// Solver settings.  Every member of the reference's SolveConfig is kept
+/// with its default; `allow_nev_above_k` is ours (BASELINE config 5 asks for
+/// nev = 20 with k = 15, which SPEC.md's rule 0 < nev <= k < m forbids).
 struct SolveConfig {
+  // Arnoldi(m, k) and the wanted count
   int m = 50;
   int k = 20;
   int nev = 15;
-  int degree = 0;
-  double rtol_multiplier = 1e-8;
-  std::optional<double> rtol_absolute;
-  RestartVariant variant = RestartVariant::ritz;
+  // preconditioner
+  int degree = 0;  // 0: plain Arnoldi on A
+  StabilityMode stability = StabilityMode::off;
   DampingMode damping = DampingMode::off;
   double damping_alpha = 0.0;
   int damping_power = 1;
-  StabilityMode stability = StabilityMode::off;
-  int double_d1 = 0;
+  int double_d1 = 0;  // solve_double stages
   int double_d2 = 0;
+  // convergence: rtol = rtol_multiplier * ||A||_est unless rtol_absolute
+  double rtol_multiplier = 1e-8;
+  std::optional<double> rtol_absolute;
   int max_cycles = 100;
+  RestartVariant variant = RestartVariant::ritz;
   unsigned long long seed = 1;
+  // reference members kept for interface parity (not used by the configs)
   bool check_mid_cycle = false;
   int mid_cycle_stride = 5;
   bool stagnation_stop = false;
   int stagnation_window = 5;
   double stagnation_rtol = 0.01;
-  std::vector<std::complex<double>> reference;
+  EigenList reference;
   bool allow_nev_above_k = false;
 
   void validate() const;
 };
 
+/// Per-cycle log entry; damping probes that were thrown away are marked.
 struct CycleStats {
   int cycle = 0;
   bool discarded_probe = false;
@@ -60,17 +71,19 @@ struct CycleStats {
   double max_residual = 0.0;
 };
 
-/// Timing breakdown of one solve (device events + host clock), seconds.
+/// Where a solve spent its time (host clock around synchronised phases).
 struct SolveTiming {
   double total = 0.0;
-  double setup = 0.0;      // norm estimate + polynomial construction
-  double extend = 0.0;     // pi(A)v + CGS2 inside the cycles
-  double check = 0.0;      // Ritz vectors + true residuals
-  double restart = 0.0;    // thick restart
+  double setup = 0.0;    // norm estimate + polynomial construction
+  double extend = 0.0;   // pi(A)v + CGS2 inside the cycles
+  double check = 0.0;    // Ritz vectors + true residuals
+  double restart = 0.0;  // thick restart
 };
 
+/// Outcome: Rayleigh quotients of A with true residuals, the polynomial(s)
+/// used, counters and the cycle history (eigenvectors stay on the device).
 struct EigResult {
-  std::vector<std::complex<double>> eigenvalues;
+  EigenList eigenvalues;
   std::vector<double> residuals;
   std::vector<bool> converged_flags;
   bool converged = false;
@@ -80,21 +93,21 @@ struct EigResult {
   std::optional<PolyPrecond> inner_poly;
   int composite_degree = 0;
   double rtol = 0.0;
-  double max_err = 0.0;
+  double max_err = 0.0;  // best max-residual over the nev pairs across cycles
   std::vector<CycleStats> history;
   int correct_count = -1;
   double norm_estimate = 0.0;
   SolveTiming timing;
 
-  int count_correct(const std::vector<std::complex<double>>& reference,
-                    double rel_tol = 1e-6) const;
+  int count_correct(const EigenList& reference, double rel_tol = 1e-6) const;
 };
 
-EigResult solve(const OperatorPtr& a, const SolveConfig& cfg);
-EigResult solve_double(const OperatorPtr& a, const SolveConfig& cfg);
-double operator_norm_estimate(const LinearOperator& a, unsigned long long seed, CostRecord& rec);
-bool check_ideal_order(const std::vector<std::complex<double>>& mu, int nev);
-/// PAPER.md section 6.3 heuristic (inc/solver.hpp:101-106).
+EigResult solve(const OperatorPtr& a, const SolveConfig& cfg);         // inc/solver.hpp:94
+EigResult solve_double(const OperatorPtr& a, const SolveConfig& cfg);  // inc/solver.hpp:111
+double operator_norm_estimate(const LinearOperator& a, unsigned long long seed,
+                              CostRecord& rec);                        // inc/solver.hpp:115
+bool check_ideal_order(const EigenList& mu, int nev);                  // inc/solver.hpp:99
+/// PAPER.md 6.3 damping heuristic (inc/solver.hpp:105).
 PolyPrecond damping_heuristic(const OperatorPtr& a, const SolveConfig& cfg, CostRecord& rec);
 
 }  // namespace ppa
