@@ -39,7 +39,7 @@ def test_library_is_sm100a():
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", so],
                          capture_output=True, text=True).stdout
     assert "sm_100a" in out
-    assert ppa.lib().ppa_abi_version() == 1
+    assert ppa.lib().ppa_abi_version() == 2
 
 
 @pytest.mark.parametrize("name,gen", [
