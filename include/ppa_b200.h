@@ -182,6 +182,12 @@ typedef struct ppa_solve_config {
   int damping;               /* 0 off, 1 auto_heuristic, 2 forced (DampingMode) */
   double damping_alpha;      /* forced: start A^power b + alpha b */
   int damping_power;
+  /* SolveConfig::check_mid_cycle / mid_cycle_stride (inc/solver.hpp:40-41) */
+  int check_mid_cycle, mid_cycle_stride;
+  /* SolveConfig::stagnation_stop / _window / _rtol (inc/solver.hpp:43-45) */
+  int stagnation_stop, stagnation_window;
+  double stagnation_rtol;
+  int want_eigenvectors;     /* keep unit eigenvectors for evec_re/evec_im */
 } ppa_solve_config;
 
 /* EigResult (inc/solver.hpp:71-89); arrays supplied by the caller */
@@ -207,6 +213,11 @@ typedef struct ppa_solve_result {
   double rtol, max_err, norm_estimate;
   ppa_cost cost;
   double t_total, t_setup, t_extend, t_check, t_restart;
+  /* optional eigenvector output (EigResult::eigenvectors, inc/solver.hpp:73):
+     unit y_j with Re at evec_re[j*evec_ld + i], Im at evec_im[...]; NULL skips */
+  double* evec_re;
+  double* evec_im;
+  long long evec_ld;
 } ppa_solve_result;
 
 /* solve (inc/solver.hpp:94) or solve_double (inc/solver.hpp:111) */

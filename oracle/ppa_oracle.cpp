@@ -1125,6 +1125,9 @@ struct Config {
   int damping = 0;  // 0 off, 1 auto heuristic, 2 forced
   double damping_alpha = 0.0;
   int damping_power = 1;
+  int mid_stride = 0;  // > 0: check_mid_cycle with this stride
+  int stag_window = 0;  // > 0: stagnation_stop over this many cycles
+  double stag_rtol = 0.01;
 };
 
 // inc/solver.hpp:96-99: |mu_1| <= ... <= |mu_nev| and
@@ -1319,6 +1322,7 @@ Result solve(const OpPtr& A, const Config& g) {
   State st = has_probe ? std::move(probe_state)
                        : arnoldi_init(rng::gauss_vec(n, g.seed, rng::ARNOLDI), g.m, c);
   R.max_err = std::numeric_limits<double>::infinity();
+  std::vector<double> best;
   for (int cyc = 1; cyc <= g.max_cycles; ++cyc) {
     Ritz s;
     bool all;
@@ -1336,6 +1340,23 @@ Result solve(const OpPtr& A, const Config& g) {
       }
       R.conv.assign(keep, 0);
       for (int i = 0; i < keep; ++i) R.conv[i] = R.res[i] <= R.rtol;
+    } else if (g.mid_stride > 0) {
+      // SPEC.md:421 mid-cycle checks: test the partial factorisation every
+      // mid_stride steps once it holds nev columns; the full check at m
+      all = false;
+      for (;;) {
+        const int to = std::min(g.m, st.cur_dim + g.mid_stride);
+        arnoldi_extend(st, *op, to, c);
+        if (st.breakdown || st.cur_dim >= g.m) break;
+        if (st.cur_dim < g.nev) continue;
+        s = ritz_pairs(st, ord);
+        check_and_record(st, s, g.nev, *A, R, all, mx, c);
+        if (all) break;
+      }
+      if (!all) {
+        s = ritz_pairs(st, ord);
+        check_and_record(st, s, g.nev, *A, R, all, mx, c);
+      }
     } else {
       arnoldi_extend(st, *op, g.m, c);
       s = ritz_pairs(st, ord);
@@ -1344,7 +1365,12 @@ Result solve(const OpPtr& A, const Config& g) {
     R.cycles = cyc;
     R.cycle_max.push_back(mx);
     R.max_err = std::min(R.max_err, mx);
-    if (all || cyc == g.max_cycles || st.breakdown) {
+    best.push_back(R.max_err);
+    // SPEC.md:621 stagnation: best max-residual improved by < stag_rtol over
+    // the last stag_window cycles
+    const int w = g.stag_window;
+    const bool stalled = w > 0 && cyc > w && best[cyc - 1] > (1.0 - g.stag_rtol) * best[cyc - 1 - w];
+    if ((w > 0 ? stalled : all) || cyc == g.max_cycles || st.breakdown || st.cur_dim < g.m) {
       R.converged = all;
       break;
     }
@@ -1631,9 +1657,12 @@ struct orc_solve_out {
 int orc_solve(const orc_op* a, int m, int k, int nev, int degree, double rtol_mult, double rtol_abs,
               int stability, int use_double, int d1, int d2, int max_cycles, unsigned long long seed,
               int allow_nev_above_k, int damping, double damping_alpha, int damping_power,
-              orc_solve_out* out) {
+              int mid_stride, int stag_window, double stag_rtol, orc_solve_out* out) {
   return wrap([&] {
     orc::Config g;
+    g.mid_stride = mid_stride;
+    g.stag_window = stag_window;
+    if (stag_rtol > 0) g.stag_rtol = stag_rtol;
     g.damping = damping;
     g.damping_alpha = damping_alpha;
     g.damping_power = damping_power > 0 ? damping_power : 1;

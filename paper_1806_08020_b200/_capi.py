@@ -50,7 +50,10 @@ class _SolveConfigC(C.Structure):
                 ("variant", C.c_int), ("stability", C.c_int), ("double_d1", C.c_int),
                 ("double_d2", C.c_int), ("use_double", C.c_int), ("max_cycles", C.c_int),
                 ("seed", C.c_ulonglong), ("allow_nev_above_k", C.c_int),
-                ("damping", C.c_int), ("damping_alpha", C.c_double), ("damping_power", C.c_int)]
+                ("damping", C.c_int), ("damping_alpha", C.c_double), ("damping_power", C.c_int),
+                ("check_mid_cycle", C.c_int), ("mid_cycle_stride", C.c_int),
+                ("stagnation_stop", C.c_int), ("stagnation_window", C.c_int),
+                ("stagnation_rtol", C.c_double), ("want_eigenvectors", C.c_int)]
 
 
 _dp = C.POINTER(C.c_double)
@@ -69,7 +72,8 @@ class _SolveResultC(C.Structure):
                 ("rtol", C.c_double), ("max_err", C.c_double), ("norm_estimate", C.c_double),
                 ("cost", CostRecord),
                 ("t_total", C.c_double), ("t_setup", C.c_double), ("t_extend", C.c_double),
-                ("t_check", C.c_double), ("t_restart", C.c_double)]
+                ("t_check", C.c_double), ("t_restart", C.c_double),
+                ("evec_re", _dp), ("evec_im", _dp), ("evec_ld", C.c_longlong)]
 
 
 _lib = None
@@ -569,6 +573,12 @@ class SolveConfig:
     damping: str = "off"          # off | auto_heuristic | forced
     damping_alpha: float = 0.0
     damping_power: int = 1
+    check_mid_cycle: bool = False
+    mid_cycle_stride: int = 5
+    stagnation_stop: bool = False
+    stagnation_window: int = 5
+    stagnation_rtol: float = 0.01
+    want_eigenvectors: bool = False
     reference: Sequence[complex] = field(default_factory=list)
 
     def _c(self, use_double: bool) -> _SolveConfigC:
@@ -578,7 +588,10 @@ class SolveConfig:
                              1 if self.stability == "pof_auto" else 0, self.double_d1,
                              self.double_d2, 1 if use_double else 0, self.max_cycles, self.seed,
                              1 if self.allow_nev_above_k else 0, damp, self.damping_alpha,
-                             self.damping_power)
+                             self.damping_power, int(self.check_mid_cycle),
+                             self.mid_cycle_stride, int(self.stagnation_stop),
+                             self.stagnation_window, self.stagnation_rtol,
+                             int(self.want_eigenvectors))
 
 
 def _solve(a: LinearOperator, cfg: SolveConfig, use_double: bool) -> dict:
@@ -593,6 +606,12 @@ def _solve(a: LinearOperator, cfg: SolveConfig, use_double: bool) -> dict:
         setattr(r, k, v.ctypes.data_as(_dp))
     r.converged_flags = conv.ctypes.data_as(_ip)
     r.cycle_max_residual = cyc.ctypes.data_as(_dp)
+    evec = None
+    if cfg.want_eigenvectors:
+        evec = np.zeros((2, cap_nev, a.dim()))
+        r.evec_re = evec[0].ctypes.data_as(_dp)
+        r.evec_im = evec[1].ctypes.data_as(_dp)
+        r.evec_ld = a.dim()
     c = cfg._c(use_double)
     _check(lib().ppa_solve(a._h, C.byref(c), C.byref(r)))
     ne = min(r.n_eig, cap_nev)
@@ -617,6 +636,8 @@ def _solve(a: LinearOperator, cfg: SolveConfig, use_double: bool) -> dict:
         "timing": {"total": r.t_total, "setup": r.t_setup, "extend": r.t_extend,
                    "check": r.t_check, "restart": r.t_restart},
     }
+    if evec is not None:
+        out["eigenvectors"] = (evec[0, :ne] + 1j * evec[1, :ne]).T.copy()
     if cfg.reference:
         ref = np.asarray(cfg.reference, dtype=np.complex128)
         out["correct_count"] = int(sum(

@@ -111,6 +111,12 @@ ppa::SolveConfig to_config(const ppa_solve_config& c) {
                                  : ppa::DampingMode::off;
   cfg.damping_alpha = c.damping_alpha;
   cfg.damping_power = c.damping_power > 0 ? c.damping_power : 1;
+  cfg.check_mid_cycle = c.check_mid_cycle != 0;
+  if (c.mid_cycle_stride > 0) cfg.mid_cycle_stride = c.mid_cycle_stride;
+  cfg.stagnation_stop = c.stagnation_stop != 0;
+  if (c.stagnation_window > 0) cfg.stagnation_window = c.stagnation_window;
+  if (c.stagnation_rtol > 0) cfg.stagnation_rtol = c.stagnation_rtol;
+  cfg.want_eigenvectors = c.want_eigenvectors != 0;
   return cfg;
 }
 
@@ -649,6 +655,20 @@ int ppa_solve(const ppa_op* a, const ppa_solve_config* c, ppa_solve_result* res)
     res->n_cycles = static_cast<int>(r.history.size());
     for (int i = 0; i < res->n_cycles && i < res->cap_cycles; ++i) {
       if (res->cycle_max_residual) res->cycle_max_residual[i] = r.history[i].max_residual;
+    }
+    if (r.eigenvectors.get() && (res->evec_re || res->evec_im)) {
+      const int ne = std::min<int>(res->n_eig, res->cap_nev);
+      const long long n = a->p->dim();
+      if (res->evec_ld < n) throw std::invalid_argument("ppa_solve: evec_ld < n");
+      for (int j = 0; j < ne && 2LL * j + 1 < static_cast<long long>(r.eigenvectors.size() / r.eigvec_ld); ++j) {
+        const double* col = r.eigenvectors.get() + 2LL * j * r.eigvec_ld;
+        if (res->evec_re)
+          PPA_CUDA(cudaMemcpy(res->evec_re + j * res->evec_ld, col, n * sizeof(double),
+                              cudaMemcpyDeviceToHost));
+        if (res->evec_im)
+          PPA_CUDA(cudaMemcpy(res->evec_im + j * res->evec_ld, col + r.eigvec_ld,
+                              n * sizeof(double), cudaMemcpyDeviceToHost));
+      }
     }
     res->converged = r.converged ? 1 : 0;
     res->cycles = r.cycles;

@@ -47,13 +47,14 @@ struct SolveConfig {
   int max_cycles = 100;
   RestartVariant variant = RestartVariant::ritz;
   unsigned long long seed = 1;
-  // reference members kept for interface parity (not used by the configs)
+  // optional early exit inside a cycle, every mid_cycle_stride steps
   bool check_mid_cycle = false;
   int mid_cycle_stride = 5;
   bool stagnation_stop = false;
   int stagnation_window = 5;
-  double stagnation_rtol = 0.01;
+  double stagnation_rtol = 0.01;  // run until max-residual stalls
   EigenList reference;
+  bool want_eigenvectors = false;  // materialise EigResult::eigenvectors
   bool allow_nev_above_k = false;
 
   void validate() const;
@@ -81,7 +82,7 @@ struct SolveTiming {
 };
 
 /// Outcome: Rayleigh quotients of A with true residuals, the polynomial(s)
-/// used, counters and the cycle history (eigenvectors stay on the device).
+/// used, counters, the cycle history and (on request) device eigenvectors.
 struct EigResult {
   EigenList eigenvalues;
   std::vector<double> residuals;
@@ -98,6 +99,10 @@ struct EigResult {
   int correct_count = -1;
   double norm_estimate = 0.0;
   SolveTiming timing;
+  /// Unit eigenvector estimates, device-resident: column 2j = Re y_j,
+  /// column 2j+1 = Im y_j, leading dimension eigvec_ld.
+  DBuffer<double> eigenvectors;
+  long long eigvec_ld = 0;
 
   int count_correct(const EigenList& reference, double rel_tol = 1e-6) const;
 };

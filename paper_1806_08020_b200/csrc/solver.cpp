@@ -158,7 +158,44 @@ CheckOutcome check_pairs(const ArnoldiState& st, const RitzSet& set, int nev,
   return out;
 }
 
-// Cycle loop shared by solve and solve_double.
+// Unit eigenvector estimates y_j (j < nev) of the final cycle, kept on the
+// device as (Re, Im) column pairs; conjugate partners share columns with the
+// sign of Im flipped.  Output materialisation only: uncounted.
+void keep_eigenvectors(const ArnoldiState& st, const RitzSet& set, int nev, EigResult& res) {
+  Context& ctx = current_context();
+  const cudaStream_t s = ctx.stream();
+  const int d = set.vectors_h.rows;
+  const int ne = std::min(nev, set.count());
+  if (ne <= 0 || d <= 0) return;
+  const long long ld = round_ld(st.n);
+  std::vector<double> g(static_cast<size_t>(d) * 2 * ne, 0.0);
+  for (int j = 0; j < ne; ++j) {
+    for (int r = 0; r < d; ++r) {
+      g[static_cast<size_t>(2 * j) * d + r] = set.vectors_h(r, j).real();
+      g[static_cast<size_t>(2 * j + 1) * d + r] = set.vectors_h(r, j).imag();
+    }
+  }
+  Scratch gdev(g.size());
+  PPA_CUDA(cudaMemcpyAsync(gdev.get(), g.data(), g.size() * sizeof(double),
+                           cudaMemcpyHostToDevice, s));
+  res.eigenvectors.resize(static_cast<size_t>(ld) * 2 * ne);
+  res.eigvec_ld = ld;
+  kern::ts_combine(st.V.get(), st.ld, st.n, d, gdev.get(), 2 * ne, res.eigenvectors.get(), ld, s);
+  Scratch sums(static_cast<size_t>(2 * ne));
+  kern::col_sumsq(res.eigenvectors.get(), ld, st.n, 2 * ne, sums.get(), ctx.ws(), ctx.sm_count(),
+                  s);
+  std::vector<double> hs(2 * ne);
+  PPA_CUDA(cudaMemcpyAsync(hs.data(), sums.get(), hs.size() * sizeof(double),
+                           cudaMemcpyDeviceToHost, s));
+  ctx.sync();
+  for (int j = 0; j < ne; ++j) {
+    const double nrm = std::sqrt(hs[2 * j] + hs[2 * j + 1]);
+    kern::div_value(res.eigenvectors.get() + 2LL * j * ld, nrm, st.n, s);
+    kern::div_value(res.eigenvectors.get() + (2LL * j + 1) * ld, nrm, st.n, s);
+  }
+  ctx.sync();
+}
+
 // One full first cycle (extend + Ritz pairs + checks of `nchk` pairs): the
 // damping heuristic's probe, reusable as cycle 1 of the solve.
 struct FirstCycle {
@@ -186,6 +223,7 @@ FirstCycle first_cycle(const LinearOperator& a, const LinearOperator& op, const 
   return f;
 }
 
+// Cycle loop shared by solve and solve_double.
 void run_cycles(const LinearOperator& a, const LinearOperator& op, const SolveConfig& cfg,
                 RitzOrdering ordering, EigResult& res, CostRecord& rec,
                 FirstCycle* probe = nullptr) {
@@ -199,6 +237,7 @@ void run_cycles(const LinearOperator& a, const LinearOperator& op, const SolveCo
     st = arnoldi_init(v0.get(), n, cfg.m, rec);
   }
   (void)ctx;
+  std::vector<double> best;
   res.max_err = std::numeric_limits<double>::infinity();
   for (int cycle = 1; cycle <= cfg.max_cycles; ++cycle) {
     CycleStats cs;
@@ -218,13 +257,35 @@ void run_cycles(const LinearOperator& a, const LinearOperator& op, const SolveCo
       chk.res.resize(keep);
     } else {
       cs.start_dim = st.cur_dim;
-      arnoldi_extend(st, op, cfg.m, rec);
+      bool checked = false;
+      if (cfg.check_mid_cycle && cfg.mid_cycle_stride > 0) {
+        // optional early exit inside a cycle (section 8 remark;
+        // SPEC.md solver design decisions): every `stride` steps, test the
+        // Ritz pairs of the partial factorisation against A
+        while (st.cur_dim < cfg.m && !st.breakdown) {
+          const int to = std::min(cfg.m, st.cur_dim + cfg.mid_cycle_stride);
+          arnoldi_extend(st, op, to, rec);
+          if (st.cur_dim >= cfg.m || st.breakdown || st.cur_dim < cfg.nev) continue;
+          set = select_pairs(st, cfg, ordering);
+          chk = check_pairs(st, set, cfg.nev, a, rec);
+          bool ok = static_cast<int>(chk.res.size()) == cfg.nev;
+          for (double r : chk.res) ok = ok && r <= res.rtol;
+          if (ok) {
+            checked = true;
+            break;
+          }
+        }
+      } else {
+        arnoldi_extend(st, op, cfg.m, rec);
+      }
       res.timing.extend += seconds_since(t0);
       cs.end_dim = st.cur_dim;
-      t0 = Clock::now();
-      set = select_pairs(st, cfg, ordering);
-      chk = check_pairs(st, set, cfg.nev, a, rec);
-      res.timing.check += seconds_since(t0);
+      if (!checked) {
+        t0 = Clock::now();
+        set = select_pairs(st, cfg, ordering);
+        chk = check_pairs(st, set, cfg.nev, a, rec);
+        res.timing.check += seconds_since(t0);
+      }
     }
     cs.real_checks = chk.real_checks;
     cs.pair_checks = chk.pair_checks;
@@ -237,13 +298,21 @@ void run_cycles(const LinearOperator& a, const LinearOperator& op, const SolveCo
     cs.max_residual = mx;
     res.cycles = cycle;
     if (mx < res.max_err) res.max_err = mx;
+    best.push_back(res.max_err);
     res.eigenvalues = chk.mu;
     res.residuals = chk.res;
     res.converged_flags.assign(chk.res.size(), false);
     for (size_t i = 0; i < chk.res.size(); ++i) res.converged_flags[i] = chk.res[i] <= res.rtol;
-    if (all || cycle == cfg.max_cycles || st.breakdown) {
+    // stagnation_stop: run until the best max-residual has not improved by
+    // stagnation_rtol over stagnation_window cycles (inc/solver.hpp:48-52)
+    const int w = cfg.stagnation_window;
+    const bool stagnated = cfg.stagnation_stop && w > 0 && cycle > w &&
+                           best.back() > (1.0 - cfg.stagnation_rtol) * best[cycle - 1 - w];
+    const bool done = cfg.stagnation_stop ? stagnated : all;
+    if (done || cycle == cfg.max_cycles || st.breakdown || st.cur_dim < cfg.m) {
       res.converged = all;
       res.history.push_back(cs);
+      if (cfg.want_eigenvectors) keep_eigenvectors(st, set, cfg.nev, res);
       break;
     }
     t0 = Clock::now();

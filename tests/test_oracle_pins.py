@@ -331,3 +331,17 @@ def test_from_triplets_sums_duplicates():
     m = O.Csr.from_triplets(3, [2, 0, 2, 0], [1, 0, 1, 2], [1.0, 2.0, 3.0, 4.0])
     rp, ci, v = m.arrays()
     assert list(rp) == [0, 2, 2, 3] and list(ci) == [0, 2, 1] and list(v) == [2.0, 4.0, 4.0]
+
+
+def test_oracle_mid_cycle_and_stagnation():
+    # SPEC.md:421 / SPEC.md:621 options of the solver restatement
+    A = O.diagonal_operator(np.arange(1.0, 1001.0))
+    full = O.solve(A, 50, 20, 15, degree=60, seed=1)
+    mid = O.solve(A, 50, 20, 15, degree=60, seed=1, mid_cycle_stride=5)
+    assert full["converged"] and mid["converged"] and mid["cycles"] == full["cycles"] == 2
+    # the last cycle stops before m: fewer pi(A) applications in total
+    assert mid["cost"]["mvps"] < 0.8 * full["cost"]["mvps"]
+    stag = O.solve(A, 30, 15, 10, degree=0, seed=1, max_cycles=200, stagnation_window=3)
+    best = np.minimum.accumulate(stag["cycle_max_residual"])
+    assert stag["cycles"] < 200 and best[-1] > 0.99 * best[-4]
+    assert np.all(best[3:-1] <= 0.99 * best[:-4])
