@@ -218,7 +218,11 @@ def run_b200(args):
     t0 = time.time()
     csr = ppa.CsrMatrix.config(3)
     n, nnz, _ = csr.info()
-    A = ppa.make_csr_operator(csr)
+    # headline: SELL-32 with fp64 values and int32 columns, the layout the
+    # north-star byte model describes; the default (automatic) layout is
+    # measured the same way below under "default_layout"
+    A = ppa.make_csr_operator(csr, "sell32")
+    A_auto = ppa.make_csr_operator(csr)
     bspmv = A.model_bytes()
     b = torch.tensor(ppa.normal_vector(n, 2, ppa.STREAM_POLY), device="cuda")
     base, _ = ppa.build_gmres_poly(A, b, 50)
@@ -230,15 +234,18 @@ def run_b200(args):
     v = torch.tensor(ppa.normal_vector(n, 2, ppa.STREAM_ARNOLDI), device="cuda")
     out = torch.empty(n, dtype=torch.float64, device="cuda")
 
-    def step():
-        ppa.apply_poly(roots, A, v, out)
+    def time_pi(op, clk_index=None):
+        def step():
+            ppa.apply_poly(roots, op, v, out)
 
-    for _ in range(max(args.warmup, 3)):
-        step()
-    torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    with ClockSampler(local) as clk:
+        for _ in range(max(args.warmup, 3)):
+            step()
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        clk = ClockSampler(local) if clk_index is not None else None
+        if clk:
+            clk.__enter__()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
@@ -247,37 +254,64 @@ def run_b200(args):
             step()
         e1.record(stream)
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
-    ms = reduce_max(ms, ws, "cuda")
-    if ws > 1:
-        dist.barrier()
-    ms_step = ms / args.steps
-    value = whole_job_gbs(step_bytes, ms_step, ws)
-    avg_launch_ms = ms_step / launches
-    achieved = bspmv / (avg_launch_ms * 1e-3) / 1e9
-    peak, peak_kind = hbm_peak()
+        if clk:
+            clk.__exit__(None, None, None)
+        ms = reduce_max(e0.elapsed_time(e1), ws, "cuda")
+        if ws > 1:
+            dist.barrier()
+        return ms / args.steps, clk
 
     # e2e: pinned host buffers through the C-ABI batch call: every step does the
     # H2D of its input vector, pi(A)v and the D2H of its result; the copies of
     # neighbouring steps overlap the compute (double-buffered, three streams).
-    op = ppa.make_poly_operator(A, roots, len(base))
-    ke = max(2, args.steps)
-    xh = torch.empty((ke, n), dtype=torch.float64).pin_memory()
-    xh[:] = torch.from_numpy(ppa.normal_vector(n, 2, ppa.STREAM_ARNOLDI))
-    yh = torch.empty((ke, n), dtype=torch.float64).pin_memory()
-    op.apply_host_batch(xh[:2], yh[:2])  # warm-up
-    torch.cuda.synchronize()
-    f0 = torch.cuda.Event(enable_timing=True)
-    f1 = torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
-    op.apply_host_batch(xh, yh)
-    f1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = f0.elapsed_time(f1) / ke
-    e2e_ms = reduce_max(e2e_ms, ws, "cuda")
+    def time_e2e(op_base):
+        op = ppa.make_poly_operator(op_base, roots, len(base))
+        ke = max(2, args.steps)
+        xh = torch.empty((ke, n), dtype=torch.float64).pin_memory()
+        xh[:] = torch.from_numpy(ppa.normal_vector(n, 2, ppa.STREAM_ARNOLDI))
+        yh = torch.empty((ke, n), dtype=torch.float64).pin_memory()
+        op.apply_host_batch(xh[:2], yh[:2])  # warm-up
+        torch.cuda.synchronize()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        op.apply_host_batch(xh, yh)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = reduce_max(f0.elapsed_time(f1) / ke, ws, "cuda")
+        match = bool(np.array_equal(yh[ke - 1].numpy(), out.cpu().numpy()))
+        return e_ms, match
+
+    ms_step, clk = time_pi(A, clk_index=local)
+    value = whole_job_gbs(step_bytes, ms_step, ws)
+    avg_launch_ms = ms_step / launches
+    achieved = bspmv / (avg_launch_ms * 1e-3) / 1e9
+    peak, peak_kind = hbm_peak()
+    ref_out = out.clone()
+    e2e_ms, e2e_match = time_e2e(A)
     e2e_val = whole_job_gbs(step_bytes, e2e_ms, ws)
-    e2e_match = bool(np.array_equal(yh[ke - 1].numpy(), out.cpu().numpy()))
-    del xh, yh
+
+    # the default layout on the same workload (bit-identical output)
+    lay = A_auto.layout()
+    ms_auto, _ = time_pi(A_auto)
+    auto_match = bool(torch.equal(out, ref_out))
+    e2e_auto_ms, e2e_auto_match = time_e2e(A_auto)
+    kbytes = lay["stream_bytes"] + 16.0 * n  # + x gather (8n) + y store (8n)
+    auto_launch_s = ms_auto * 1e-3 / launches
+    default_layout = {
+        "layout": lay["layout"], "ms_per_step": round(ms_auto, 4),
+        "value": round(whole_job_gbs(step_bytes, ms_auto, ws), 3), "unit": "GB/s (north-star model)",
+        "speedup_vs_sell32": round(ms_step / ms_auto, 3),
+        "e2e": {"value": round(whole_job_gbs(step_bytes, e2e_auto_ms, ws), 3),
+                "ms_per_step": round(e2e_auto_ms, 4), "matches_device_result": e2e_auto_match},
+        "roofline": {"bound": "hbm", "achieved": round(kbytes / auto_launch_s / 1e9, 2),
+                     "peak": peak, "unit": "GB/s",
+                     "frac": round(kbytes / auto_launch_s / 1e9 / peak, 4),
+                     "kernel": "k_spmv_diar (regular-row diagonal form, fused real-root factor)",
+                     "algorithmic_bytes_per_launch": kbytes,
+                     "bytes_note": "matrix stream of this layout + 8n x + 8n y"},
+        "bit_identical_to_sell32": auto_match,
+    }
 
     # CGS2 step at basis size c = 40 (config 3's m) on a real Arnoldi basis of
     # A: w = A v_39 orthogonalised against V[:,0:40] (3 sweeps, V[:,40] written).
@@ -306,16 +340,23 @@ def run_b200(args):
     cgs_phys = 8.0 * n * (3 * c + 5) / (cgs_ms * 1e-3) / 1e9
     del st, Vt
 
-    # time to nev converged eigenpairs (config 3, matrix already on device)
+    # time to nev converged eigenpairs (config 3, matrix already on device):
+    # default layout, and the SELL-32 layout for comparison
     solve_info = None
     if not args.no_solve:
         cfg = ppa.config_solve_config(3)
-        r = ppa.solve(A, cfg)
-        lam = np.sort(r["eigenvalues"].real)
-        solve_info = {"seconds": round(r["timing"]["total"], 4), "converged": r["converged"],
-                      "cycles": r["cycles"], "mvps": r["cost"]["mvps"], "dots": r["cost"]["dots"],
-                      "eff_degree": r["composite_degree"], "smallest": round(float(lam[0]), 6),
-                      "timing": {k: round(v, 4) for k, v in r["timing"].items()}}
+
+        def solve_on(op):
+            r = ppa.solve(op, cfg)
+            lam = np.sort(r["eigenvalues"].real)
+            return {"seconds": round(r["timing"]["total"], 4), "converged": r["converged"],
+                    "cycles": r["cycles"], "mvps": r["cost"]["mvps"], "dots": r["cost"]["dots"],
+                    "eff_degree": r["composite_degree"], "smallest": round(float(lam[0]), 6),
+                    "timing": {k: round(v, 4) for k, v in r["timing"].items()}}
+
+        solve_info = solve_on(A_auto)
+        solve_info["layout"] = lay["layout"]
+        solve_info["sell32"] = solve_on(A)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -344,7 +385,9 @@ def run_b200(args):
             "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
                     "d2h_bytes_per_step": 8 * n, "ms_per_step": round(e2e_ms, 4),
                     "matches_device_result": e2e_match},
+            "default_layout": default_layout,
             "gpu_launches": launches * args.steps,
+            "layout": "sell32 (fp64 values, int32 columns)",
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "cgs2": {"c": c, "gbs_model": round(cgs_gbs, 2), "ms": round(cgs_ms, 4),

@@ -90,6 +90,10 @@ int ppa_normal_vector(long long n, unsigned long long seed, unsigned long long s
 /* ---- operators --------------------------------------------------------- */
 /* make_csr_operator (inc/operators.hpp:83): validates, uploads to HBM */
 int ppa_csr_operator(const ppa_host_csr* m, ppa_op** out);
+/* make_csr_operator with a device-layout cap: 0 automatic, 1 CSR row blocks,
+   2 SELL-32 (fp64 values, int32 columns: the north-star byte model),
+   3 packed SELL-32, 4 diagonal-coded.  Results are bit-identical. */
+int ppa_csr_operator_layout(const ppa_host_csr* m, int layout, ppa_op** out);
 /* make_diagonal (inc/operators.hpp:81) */
 int ppa_diagonal_operator(int n, const double* diag, ppa_op** out);
 /* make_poly_operator / make_poly_complement_operator (inc/gmres_poly.hpp:91,95) */
@@ -109,6 +113,11 @@ int ppa_op_apply_host_batch(const ppa_op* op, int count, const double* X, double
                             ppa_cost* cost);
 /* CSR operators: bytes of one SpMV under the north-star byte model */
 int ppa_csr_model_bytes(const ppa_op* op, double* bytes, long long* nnz);
+/* Device layout of a CSR operator: 0 CSR row blocks, 1 SELL-32, 2 packed
+   SELL-32, 3 diagonal-coded; stream_bytes = matrix bytes one SpMV streams in that layout;
+   dict_size = value-table size (0: fp64 values) */
+int ppa_csr_layout(const ppa_op* op, int* layout, double* stream_bytes, int* sigma,
+                   int* dict_size);
 
 /* ---- polynomial -------------------------------------------------------- */
 /* apply_poly (src/gmres_poly.cpp:117-147): out_dev = pi(A) v_dev */

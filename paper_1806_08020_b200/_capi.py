@@ -113,6 +113,8 @@ def lib():
             "ppa_op_apply_host": [vp, vp, vp, C.POINTER(CostRecord)],
             "ppa_op_apply_host_batch": [vp, C.c_int, vp, vp, C.POINTER(CostRecord)],
             "ppa_csr_model_bytes": [vp, _dp, C.POINTER(C.c_longlong)],
+            "ppa_csr_layout": [vp, _ip, _dp, _ip, _ip],
+            "ppa_csr_operator_layout": [vp, C.c_int, C.POINTER(vp)],
             "ppa_apply_poly": [vp, vp, C.c_int, vp, vp, vp, C.POINTER(CostRecord)],
             "ppa_build_gmres_poly": [vp, vp, C.c_int, vp, vp, _ip, _ip, C.POINTER(CostRecord)],
             "ppa_leja_order": [vp, vp, C.c_int, vp, vp],
@@ -360,10 +362,27 @@ class LinearOperator:
         _check(lib().ppa_csr_model_bytes(self._h, C.byref(b), C.byref(nnz)))
         return b.value
 
+    def layout(self) -> dict:
+        """Device layout of a CSR operator (ppa_csr_layout)."""
+        lay, sig, nd = C.c_int(), C.c_int(), C.c_int()
+        sb = C.c_double()
+        _check(lib().ppa_csr_layout(self._h, C.byref(lay), C.byref(sb), C.byref(sig),
+                                    C.byref(nd)))
+        return {"layout": ("csr", "sell32", "sell32_packed", "dia_coded")[lay.value],
+                "stream_bytes": sb.value, "sigma": sig.value, "dict_size": nd.value}
 
-def make_csr_operator(m: CsrMatrix) -> LinearOperator:
+
+LAYOUTS = {"auto": 0, "csr": 1, "sell32": 2, "sell32_packed": 3, "dia_coded": 4}
+
+
+def make_csr_operator(m: CsrMatrix, layout: str = "auto") -> LinearOperator:
+    """make_csr_operator (inc/operators.hpp:83); `layout` caps the device
+    layout (ppa_csr_operator_layout), results are bit-identical."""
     h = C.c_void_p()
-    _check(lib().ppa_csr_operator(m._h, C.byref(h)))
+    if layout == "auto":
+        _check(lib().ppa_csr_operator(m._h, C.byref(h)))
+    else:
+        _check(lib().ppa_csr_operator_layout(m._h, LAYOUTS[layout], C.byref(h)))
     return LinearOperator(h)
 
 

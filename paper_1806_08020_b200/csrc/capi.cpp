@@ -245,6 +245,15 @@ int ppa_normal_vector(long long n, unsigned long long seed, unsigned long long s
   });
 }
 
+int ppa_csr_operator_layout(const ppa_host_csr* m, int layout, ppa_op** out) {
+  return guard([&] {
+    need(m, "ppa_csr_operator_layout");
+    need(out, "ppa_csr_operator_layout");
+    if (layout < 0 || layout > 4) throw std::invalid_argument("ppa_csr_operator_layout: layout");
+    *out = wrap_op(ppa::make_csr_operator(m->m, static_cast<ppa::CsrLayout>(layout)));
+  });
+}
+
 int ppa_csr_operator(const ppa_host_csr* m, ppa_op** out) {
   return guard([&] {
     need(m, "ppa_csr_operator");
@@ -401,6 +410,19 @@ int ppa_csr_model_bytes(const ppa_op* op, double* bytes, long long* nnz) {
     if (!c) throw std::invalid_argument("ppa_csr_model_bytes: not a CSR operator");
     if (bytes) *bytes = c->model_bytes();
     if (nnz) *nnz = c->nnz();
+  });
+}
+
+int ppa_csr_layout(const ppa_op* op, int* layout, double* stream_bytes, int* sigma,
+                   int* dict_size) {
+  return guard([&] {
+    need(op, "ppa_csr_layout");
+    const auto* c = dynamic_cast<const ppa::CsrOperator*>(op->p.get());
+    if (!c) throw std::invalid_argument("ppa_csr_layout: not a CSR operator");
+    if (layout) *layout = c->uses_dia() ? 3 : c->uses_packed() ? 2 : c->uses_sell() ? 1 : 0;
+    if (stream_bytes) *stream_bytes = c->stream_bytes();
+    if (sigma) *sigma = c->uses_sell() ? c->sell_sigma() : 0;
+    if (dict_size) *dict_size = c->uses_dia() ? c->device().dia_ndict : c->device().pk_ndict;
   });
 }
 

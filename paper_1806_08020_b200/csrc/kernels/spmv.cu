@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "spmv_epilogue.cuh"
 #include "ppa/kernels.hpp"
 
 namespace ppa {
@@ -34,22 +35,6 @@ constexpr int MAXR = kSpmvMaxRows;
 constexpr int MAXNNZ = kSpmvMaxNnz;
 // Pairs a thread may own: the slice [p0 & ~1, p1) has <= MAXNNZ + 1 elements.
 constexpr int KPAIRS = ((MAXNNZ + 2) / 2 + T - 1) / T;
-
-template <int MODE, bool COMPL>
-__device__ __forceinline__ double epilogue(int r, double s, const double* __restrict__ x,
-                                           double c0, double c1, const double* o,
-                                           const double* base) {
-  double z;
-  if (MODE == 0) {
-    z = s;
-  } else if (MODE == 1) {
-    z = __dadd_rn(__ldg(x + r), __dmul_rn(c0, s));
-  } else {
-    z = __dadd_rn(__dadd_rn(o[r], __dmul_rn(c1, __ldg(x + r))), __dmul_rn(c0, s));
-  }
-  if (COMPL) z = __dsub_rn(base[r], z);
-  return z;
-}
 
 template <int MODE, bool COMPL>
 __global__ void __launch_bounds__(T) k_spmv_rowblock(
@@ -189,6 +174,14 @@ void launch(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep, c
 
 void spmv(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep, cudaStream_t st) {
   if (a.n == 0 || a.nblocks == 0) return;
+  if (a.dia_code) {
+    spmv_dia(a, x, y, ep, st);
+    return;
+  }
+  if (a.pk_ptr) {
+    spmv_packed(a, x, y, ep, st);
+    return;
+  }
   const bool compl_ = ep.base != nullptr;
   switch (ep.mode) {
     case Epi::plain:
@@ -248,6 +241,14 @@ __global__ void __launch_bounds__(SELL_WARPS * 32) k_spmm_sell32(
 void spmm(const CsrDevice& a, const double* Y, long long ldy, int p, double* AY, long long ldo,
           cudaStream_t st) {
   if (a.n == 0 || p <= 0) return;
+  if (a.dia_code) {
+    spmm_dia(a, Y, ldy, p, AY, ldo, st);
+    return;
+  }
+  if (a.pk_ptr) {
+    spmm_packed(a, Y, ldy, p, AY, ldo, st);
+    return;
+  }
   if (!a.sell_val) {
     for (int j = 0; j < p; ++j) spmv(a, Y + j * ldy, AY + j * ldo, EpiArgs{}, st);
     return;

@@ -1,0 +1,458 @@
+// Diagonal-coded SpMV / SpMM for stencil matrices: every nonzero lies on one
+// of a few diagonals (col - row in a small fixed set) and the matrix has few
+// distinct values.  Config 3's 7-point Laplacian has 7 diagonals and 2
+// values; configs 2 and 5 (5-point convection-diffusion) have 5 and 4.
+//
+// Replaces CsrMatrix::multiply (src/operators.cpp:39-48) for such matrices.
+// Coded form: one byte per (row, diagonal), a code into the value table or
+// kDiaAbsent where the row has no entry on that diagonal.  Row r's codes are
+// contiguous (stride 4/8/16/32 bytes), one vector load per lane.
+// Regular-row form (default when at least half the rows qualify): rows whose
+// diagonals all carry their per-diagonal default value stream no codes at
+// all - one mask bit per row - and the remaining rows (matrix boundary,
+// coefficient jumps) come from a compact list with their codes.  Config 3
+// then streams 2.3 MB per SpMV instead of the CSR's 424 MB; what is left is
+// the x gathers and the y store.
+//
+// The x gathers x[r + off_j] of a warp are 32 consecutive doubles per
+// diagonal (coalesced).  Diagonals are visited in increasing offset, i.e.
+// increasing column, and absent entries are skipped, so each row is summed in
+// the CSR's own order without FMA: bit-identical to the CPU loop.
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <unordered_map>
+#include <vector>
+
+#include "common.cuh"
+#include "spmv_epilogue.cuh"
+#include "ppa/kernels.hpp"
+
+namespace ppa {
+namespace kern {
+namespace {
+
+constexpr int DW = 8;  // warps per CTA
+
+// Diagonal offsets (warp-uniform kernel parameters).
+struct DiaOffsets {
+  int off[kDiaMaxDiag];
+};
+
+// Code j of a row (byte j % 4 of word j / 4), one PRMT.
+__device__ __forceinline__ unsigned code_of(unsigned w, int j) {
+  return __byte_perm(w, 0u, 0x4440u | static_cast<unsigned>(j & 3));
+}
+
+// Codes of one row: NW 32-bit words (4 codes each).
+template <int NW>
+__device__ __forceinline__ void load_codes(unsigned (&w)[NW], const unsigned* __restrict__ p) {
+  if (NW == 1) {
+    w[0] = __ldcs(p);
+  } else if (NW == 2) {
+    const uint2 v = __ldcs(reinterpret_cast<const uint2*>(p));
+    w[0] = v.x;
+    w[1] = v.y;
+  } else {
+#pragma unroll
+    for (int k = 0; k < NW / 4; ++k) {
+      const uint4 v = __ldcs(reinterpret_cast<const uint4*>(p) + k);
+      w[4 * k] = v.x;
+      w[4 * k + 1] = v.y;
+      w[4 * k + 2] = v.z;
+      w[4 * k + 3] = v.w;
+    }
+  }
+}
+
+__device__ __forceinline__ void load_table(double* tab, const double* __restrict__ dict,
+                                           int ndict) {
+  // entries past ndict (including kDiaAbsent's slot) are read but never used
+  for (int t = threadIdx.x; t < ndict; t += blockDim.x) tab[t] = dict[t];
+  __syncthreads();
+}
+
+// Gathers of row r: x[r + off_j], clamped into [0, n) so the addresses do
+// not depend on the codes (entries outside the matrix are absent and their
+// values are never used).  The gathers can therefore issue together with the
+// code load instead of after it.
+template <int ND>
+__device__ __forceinline__ void dia_gather(double (&xv)[ND], int r, int n, const DiaOffsets& off,
+                                           const double* __restrict__ x) {
+#pragma unroll
+  for (int j = 0; j < ND; ++j) xv[j] = __ldg(x + min(max(r + off.off[j], 0), n - 1));
+}
+
+// Row sum from the codes and gathered values, diagonals in increasing offset
+// (= increasing column), absent entries skipped.
+template <int NW>
+__device__ __forceinline__ double dia_sum(const unsigned (&w)[NW], const double (&xv)[4 * NW],
+                                          const double* tab) {
+  double sum = 0.0;
+#pragma unroll
+  for (int j = 0; j < 4 * NW; ++j) {
+    const unsigned c = code_of(w[j / 4], j);
+    if (c != kDiaAbsent) sum = __dadd_rn(sum, __dmul_rn(tab[c], xv[j]));
+  }
+  return sum;
+}
+
+// Persistent warps, grid-stride over 32-row slices (all warps sweep the rows
+// together, so the x lines neighbouring slices share stay cached).  The
+// value table is loaded once per CTA.  Software pipeline of depth 2: while
+// slice s is summed, the codes and x gathers of slice s + W are already in
+// flight (their addresses depend only on the row), so every warp keeps a
+// full slice of loads outstanding through its arithmetic.
+// Coded path: persistent warps, grid-stride over 32-row slices (all warps
+// sweep the rows together, so x lines shared by neighbouring slices stay
+// cached).  The value table is loaded once per CTA.  Two-deep software
+// pipeline: while slice s is summed, the codes and x gathers of slice s + W
+// are in flight (gather addresses depend only on the row).
+template <int MODE, bool COMPL, int NW>
+__global__ void __launch_bounds__(DW * 32, 4) k_spmv_dia(
+    const unsigned* __restrict__ codes, const double* __restrict__ dict, int ndict,
+    const DiaOffsets off, int n, int nslices, const double* __restrict__ x, double* y,
+    double c0, double c1, const double* o, const double* base) {
+  __shared__ double tab[kDiaMaxDict + 1];
+  const int lane = threadIdx.x & 31;
+  const int W = gridDim.x * DW;
+  int s = blockIdx.x * DW + (threadIdx.x >> 5);
+  unsigned w[NW];
+  double xv[4 * NW];
+  if (s < nslices) {
+    load_codes<NW>(w, codes + (static_cast<long long>(s) * 32 + lane) * NW);
+    dia_gather<4 * NW>(xv, s * 32 + lane, n, off, x);
+  }
+  load_table(tab, dict, ndict);
+  for (; s < nslices; s += W) {
+    const int sn = s + W;
+    unsigned wn[NW];
+    double xn[4 * NW];
+    if (sn < nslices) {
+      load_codes<NW>(wn, codes + (static_cast<long long>(sn) * 32 + lane) * NW);
+      dia_gather<4 * NW>(xn, sn * 32 + lane, n, off, x);
+    }
+    const int r = s * 32 + lane;
+    const double sum = dia_sum<NW>(w, xv, tab);
+    if (r < n) y[r] = epilogue<MODE, COMPL>(r, sum, x, c0, c1, o, base);
+#pragma unroll
+    for (int k = 0; k < NW; ++k) w[k] = wn[k];
+#pragma unroll
+    for (int j = 0; j < 4 * NW; ++j) xv[j] = xn[j];
+  }
+}
+
+template <typename K>
+int resident_ctas(K kernel) {
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, DW * 32, 0) != cudaSuccess) b = 1;
+  return std::max(b, 1);
+}
+
+int device_sms() {
+  static const int sms = [] {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+      v = 148;
+    }
+    return v;
+  }();
+  return sms;
+}
+
+template <int MODE, bool COMPL, int NW>
+void launch_dia_nw(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep,
+                   cudaStream_t st) {
+  DiaOffsets off{};
+  for (int j = 0; j < a.dia_ndiag; ++j) off.off[j] = a.dia_off[j];
+  auto kernel = k_spmv_dia<MODE, COMPL, NW>;
+  static const int per_sm = resident_ctas(kernel);
+  const int grid = std::min((a.nslices + DW - 1) / DW, device_sms() * per_sm);
+  kernel<<<grid, DW * 32, 0, st>>>(reinterpret_cast<const unsigned*>(a.dia_code), a.dia_dict,
+                                   a.dia_ndict, off, a.n, a.nslices, x, y, ep.c0, ep.c1, ep.o,
+                                   ep.base);
+}
+
+// ---- regular-row form -----------------------------------------------------
+// Rows whose diagonals all carry their default values (the interior of a
+// constant-coefficient stencil) stream no codes at all: per 32-row slice the
+// kernel reads one {regular mask, exception index} pair, gathers x, and sums
+// default_j * x[r + off_j] in diagonal order.  Irregular rows (boundaries,
+// coefficient jumps) read their codes from the exception list.  The sums are
+// the same products in the same order as the coded path.
+struct DiaRParams {
+  int off[kDiaRegularMaxDiag];
+  double val[kDiaRegularMaxDiag];
+};
+
+// One launch, two kinds of CTAs, one thread per row, no shared memory:
+//   CTAs [0, gx)      the irregular rows, from a compact list (row index +
+//                     codes, values from the L1-resident table);
+//   CTAs [gx, ...)    all rows of their 512-row block, storing only the
+//                     regular ones (mask bit set): default values, no codes.
+// The two sets of rows are disjoint and both only read x, so they need no
+// ordering; the irregular CTAs go first so their longer load chain overlaps
+// the regular sweep.
+constexpr int RB = 512;
+
+template <int MODE, bool COMPL, int NW>
+__global__ void __launch_bounds__(RB) k_spmv_diar(
+    const unsigned* __restrict__ mask, const int* __restrict__ irr_rows,
+    const unsigned char* __restrict__ irr_codes, int n_irr, int gx,
+    const double* __restrict__ dict, const DiaRParams P, int ndiag, int n,
+    const double* __restrict__ x, double* y, double c0, double c1, const double* o,
+    const double* base) {
+  double sum = 0.0;
+  int r;
+  const int bx = blockIdx.x;
+  if (bx < gx) {
+    const int k = bx * RB + threadIdx.x;
+    if (k >= n_irr) return;
+    r = __ldg(irr_rows + k);
+    unsigned ec[NW];
+    load_codes<NW>(ec, reinterpret_cast<const unsigned*>(irr_codes) + static_cast<long long>(k) * NW);
+    double xv[4 * NW];
+#pragma unroll
+    for (int j = 0; j < 4 * NW; ++j) {
+      const unsigned c = code_of(ec[j / 4], j);
+      xv[j] = __ldg(x + (c != kDiaAbsent ? r + P.off[j] : r));
+    }
+#pragma unroll
+    for (int j = 0; j < 4 * NW; ++j) {
+      const unsigned c = code_of(ec[j / 4], j);
+      if (c != kDiaAbsent) sum = __dadd_rn(sum, __dmul_rn(__ldg(dict + c), xv[j]));
+    }
+  } else {
+    r = (bx - gx) * RB + threadIdx.x;
+    if (r >= n) return;
+    const unsigned m = __ldg(mask + (r >> 5));
+    // all 4*NW slots gather (padding slots have offset 0 and hit x[r]'s
+    // line): predicating them on ndiag would predicate the parameter loads
+    double xv[4 * NW];
+#pragma unroll
+    for (int j = 0; j < 4 * NW; ++j) xv[j] = __ldg(x + min(max(r + P.off[j], 0), n - 1));
+#pragma unroll
+    for (int j = 0; j < 4 * NW; ++j) {
+      if (j < ndiag) sum = __dadd_rn(sum, __dmul_rn(P.val[j], xv[j]));
+    }
+    if (!((m >> (r & 31)) & 1u)) return;
+  }
+  y[r] = epilogue<MODE, COMPL>(r, sum, x, c0, c1, o, base);
+}
+
+template <int MODE, bool COMPL, int NW>
+void launch_diar_nw(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep,
+                    cudaStream_t st) {
+  DiaRParams P{};
+  for (int j = 0; j < a.dia_ndiag; ++j) {
+    P.off[j] = a.dia_off[j];
+    P.val[j] = a.dia_dflt[j];
+  }
+  const int gx = static_cast<int>((a.dia_nirr + RB - 1) / RB);
+  const int grid = gx + (a.n + RB - 1) / RB;
+  k_spmv_diar<MODE, COMPL, NW><<<grid, RB, 0, st>>>(
+      a.dia_mask, a.dia_irr_rows, a.dia_irr_codes, static_cast<int>(a.dia_nirr), gx, a.dia_dict,
+      P, a.dia_ndiag, a.n, x, y, ep.c0, ep.c1, ep.o, ep.base);
+}
+
+template <int MODE, bool COMPL>
+void launch_dia(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep,
+                cudaStream_t st) {
+  if (a.dia_mask) {
+    switch (a.dia_stride) {
+      case 4: return launch_diar_nw<MODE, COMPL, 1>(a, x, y, ep, st);
+      case 8: return launch_diar_nw<MODE, COMPL, 2>(a, x, y, ep, st);
+      default: return launch_diar_nw<MODE, COMPL, 4>(a, x, y, ep, st);
+    }
+  }
+  switch (a.dia_stride) {
+    case 4: return launch_dia_nw<MODE, COMPL, 1>(a, x, y, ep, st);
+    case 8: return launch_dia_nw<MODE, COMPL, 2>(a, x, y, ep, st);
+    case 16: return launch_dia_nw<MODE, COMPL, 4>(a, x, y, ep, st);
+    default: return launch_dia_nw<MODE, COMPL, 8>(a, x, y, ep, st);
+  }
+}
+
+// Multi-RHS: each code is decoded once and applied to up to DB columns.
+constexpr int DB = 8;
+
+// One thread per row, no shared memory: gathers are unconditional (absent
+// entries read row r itself) so no parameter load is predicated; only the
+// accumulation is.
+template <int NW>
+__global__ void __launch_bounds__(256) k_spmm_dia(
+    const unsigned* __restrict__ codes, const double* __restrict__ dict, const DiaOffsets off,
+    int n, const double* __restrict__ Y, long long ldy, int p, double* __restrict__ AY,
+    long long ldo) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  unsigned w[NW];
+  load_codes<NW>(w, codes + static_cast<long long>(r) * NW);
+  double sum[DB];
+#pragma unroll
+  for (int k = 0; k < DB; ++k) sum[k] = 0.0;
+#pragma unroll
+  for (int j = 0; j < 4 * NW; ++j) {
+    const unsigned c = code_of(w[j / 4], j);
+    const bool present = c != kDiaAbsent;
+    const double v = __ldg(dict + (present ? c : 0u));
+    const double* yc = Y + (present ? r + off.off[j] : r);
+    double yv[DB];
+#pragma unroll
+    for (int k = 0; k < DB; ++k) yv[k] = k < p ? __ldg(yc + k * ldy) : 0.0;
+#pragma unroll
+    for (int k = 0; k < DB; ++k) {
+      if (present && k < p) sum[k] = __dadd_rn(sum[k], __dmul_rn(v, yv[k]));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < DB; ++k) {
+    if (k < p) AY[r + k * ldo] = sum[k];
+  }
+}
+
+template <int NW>
+void launch_spmm_dia_nw(const CsrDevice& a, const double* Y, long long ldy, int p, double* AY,
+                        long long ldo, cudaStream_t st) {
+  DiaOffsets off{};
+  for (int j = 0; j < a.dia_ndiag; ++j) off.off[j] = a.dia_off[j];
+  const int grid = (a.n + 255) / 256;
+  for (int j0 = 0; j0 < p; j0 += DB) {
+    k_spmm_dia<NW><<<grid, 256, 0, st>>>(reinterpret_cast<const unsigned*>(a.dia_code),
+                                         a.dia_dict, off, a.n, Y + j0 * ldy, ldy,
+                                         std::min(DB, p - j0), AY + j0 * ldo, ldo);
+  }
+}
+
+}  // namespace
+
+void spmv_dia(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep,
+              cudaStream_t st) {
+  const bool compl_ = ep.base != nullptr;
+  switch (ep.mode) {
+    case Epi::plain:
+      compl_ ? launch_dia<0, true>(a, x, y, ep, st) : launch_dia<0, false>(a, x, y, ep, st);
+      break;
+    case Epi::real:
+      compl_ ? launch_dia<1, true>(a, x, y, ep, st) : launch_dia<1, false>(a, x, y, ep, st);
+      break;
+    case Epi::pair:
+      compl_ ? launch_dia<2, true>(a, x, y, ep, st) : launch_dia<2, false>(a, x, y, ep, st);
+      break;
+  }
+  PPA_CUDA(cudaGetLastError());
+}
+
+void spmm_dia(const CsrDevice& a, const double* Y, long long ldy, int p, double* AY,
+              long long ldo, cudaStream_t st) {
+  switch (a.dia_stride) {
+    case 4: launch_spmm_dia_nw<1>(a, Y, ldy, p, AY, ldo, st); break;
+    case 8: launch_spmm_dia_nw<2>(a, Y, ldy, p, AY, ldo, st); break;
+    case 16: launch_spmm_dia_nw<4>(a, Y, ldy, p, AY, ldo, st); break;
+    default: launch_spmm_dia_nw<8>(a, Y, ldy, p, AY, ldo, st); break;
+  }
+  PPA_CUDA(cudaGetLastError());
+}
+
+bool build_dia(const int* row_ptr, const int* col_idx, const double* values, int n,
+               std::vector<int>& offsets, int& stride, std::vector<unsigned char>& codes,
+               std::vector<double>& dict) {
+  offsets.clear();
+  codes.clear();
+  dict.clear();
+  const long long nnz = row_ptr[n];
+  if (n <= 0 || nnz <= 0) return false;
+  std::map<long long, long long> diag;  // offset -> count (sorted)
+  for (int r = 0; r < n; ++r) {
+    for (int p = row_ptr[r]; p < row_ptr[r + 1]; ++p) {
+      ++diag[static_cast<long long>(col_idx[p]) - r];
+      if (static_cast<int>(diag.size()) > kDiaMaxDiag) return false;
+    }
+  }
+  const int nd = static_cast<int>(diag.size());
+  // every diagonal must be well filled: the gathers of absent entries are
+  // predicated off, but their code bytes are still streamed
+  if (static_cast<double>(nd) * n > kDiaMaxFill * static_cast<double>(nnz)) return false;
+  std::unordered_map<uint64_t, int> index;
+  for (long long p = 0; p < nnz; ++p) {
+    uint64_t bits;
+    std::memcpy(&bits, values + p, sizeof bits);
+    if (index.count(bits)) continue;
+    if (static_cast<int>(index.size()) == kDiaMaxDict) return false;
+    index.emplace(bits, static_cast<int>(dict.size()));
+    dict.push_back(values[p]);
+  }
+  stride = nd <= 4 ? 4 : nd <= 8 ? 8 : nd <= 16 ? 16 : 32;
+  std::unordered_map<long long, int> slot;
+  for (const auto& kv : diag) {
+    slot.emplace(kv.first, static_cast<int>(offsets.size()));
+    offsets.push_back(static_cast<int>(kv.first));
+  }
+  const long long rows = (static_cast<long long>(n) + 31) / 32 * 32;
+  codes.assign(static_cast<size_t>(rows * stride), static_cast<unsigned char>(kDiaAbsent));
+  for (int r = 0; r < n; ++r) {
+    for (int p = row_ptr[r]; p < row_ptr[r + 1]; ++p) {
+      uint64_t bits;
+      std::memcpy(&bits, values + p, sizeof bits);
+      const int j = slot.at(static_cast<long long>(col_idx[p]) - r);
+      codes[static_cast<size_t>(r) * stride + j] = static_cast<unsigned char>(index.at(bits));
+    }
+  }
+  return true;
+}
+
+bool build_dia_regular(const std::vector<unsigned char>& codes, int n, int ndiag, int stride,
+                       const std::vector<double>& dict, std::vector<unsigned>& mask,
+                       std::vector<int>& irr_rows, std::vector<unsigned char>& irr_codes,
+                       std::vector<double>& dflt) {
+  mask.clear();
+  irr_rows.clear();
+  irr_codes.clear();
+  dflt.clear();
+  if (ndiag > kDiaRegularMaxDiag || n <= 0) return false;
+  // default code of a diagonal: its most frequent present code
+  std::vector<int> dcode(ndiag, -1);
+  for (int j = 0; j < ndiag; ++j) {
+    std::vector<long long> cnt(256, 0);
+    for (int r = 0; r < n; ++r) ++cnt[codes[static_cast<size_t>(r) * stride + j]];
+    long long best = 0;
+    for (int c = 0; c < static_cast<int>(kDiaAbsent); ++c) {
+      if (cnt[c] > best) {
+        best = cnt[c];
+        dcode[j] = c;
+      }
+    }
+    if (dcode[j] < 0) return false;
+    dflt.push_back(dict[dcode[j]]);
+  }
+  auto regular = [&](int r) {
+    for (int j = 0; j < ndiag; ++j) {
+      if (codes[static_cast<size_t>(r) * stride + j] != dcode[j]) return false;
+    }
+    return true;
+  };
+  mask.assign(static_cast<size_t>((n + 31) / 32), 0u);
+  for (int r = 0; r < n; ++r) {
+    if (regular(r)) {
+      mask[r >> 5] |= 1u << (r & 31);
+    } else {
+      irr_rows.push_back(r);
+      irr_codes.insert(irr_codes.end(), codes.begin() + static_cast<long long>(r) * stride,
+                       codes.begin() + static_cast<long long>(r + 1) * stride);
+    }
+  }
+  if (2 * static_cast<long long>(irr_rows.size()) > n) {
+    mask.clear();
+    irr_rows.clear();
+    irr_codes.clear();
+    dflt.clear();
+    return false;
+  }
+  return true;
+}
+
+}  // namespace kern
+}  // namespace ppa

@@ -72,7 +72,8 @@ CsrMatrix CsrMatrix::from_triplets(int n, std::vector<std::tuple<int, int, doubl
 
 // ------------------------------------------------------------ operator --
 
-CsrOperator::CsrOperator(const CsrMatrix& m, OperatorKind kind, std::vector<double> diag)
+CsrOperator::CsrOperator(const CsrMatrix& m, OperatorKind kind, std::vector<double> diag,
+                         CsrLayout layout)
     : kind_(kind), diag_(std::move(diag)) {
   m.validate();
   n_ = m.n;
@@ -116,7 +117,7 @@ CsrOperator::CsrOperator(const CsrMatrix& m, OperatorKind kind, std::vector<doub
   std::vector<double> sv;
   bool sell = false;
   int sigma = 1;
-  if (!std::getenv("PPA_DISABLE_SELL")) {
+  if (layout != CsrLayout::csr && !std::getenv("PPA_DISABLE_SELL")) {
     sell = kern::build_sell32(m.row_ptr.data(), m.col_idx.data(), m.values.data(), n_, 1, sp, sc,
                               sv, perm);
     if (!sell && !std::getenv("PPA_DISABLE_SIGMA")) {
@@ -149,7 +150,114 @@ CsrOperator::CsrOperator(const CsrMatrix& m, OperatorKind kind, std::vector<doub
     dev_.nslices = static_cast<int>(sp.size()) - 1;
     dev_.sell_entries = sp.back();
     dev_.sell_sigma = sigma;
+    const bool dia_ok = layout == CsrLayout::automatic || layout == CsrLayout::dia;
+    const bool packed_ok = dia_ok || layout == CsrLayout::sell32_packed;
+    if (!(dia_ok && upload_dia(m)) && packed_ok) upload_packed(m, perm);
   }
+}
+
+// Diagonal-coded layout for stencil matrices (kernels/spmv_dia.cu);
+// PPA_DISABLE_DIA skips it.
+bool CsrOperator::upload_dia(const CsrMatrix& m) {
+  if (std::getenv("PPA_DISABLE_DIA")) return false;
+  std::vector<int> offs;
+  std::vector<unsigned char> codes;
+  std::vector<double> dict;
+  int stride = 0;
+  if (!kern::build_dia(m.row_ptr.data(), m.col_idx.data(), m.values.data(), n_, offs, stride,
+                       codes, dict)) {
+    return false;
+  }
+  dia_code_.resize(codes.size());
+  PPA_CUDA(cudaMemcpy(dia_code_.get(), codes.data(), codes.size(), cudaMemcpyHostToDevice));
+  dia_dict_.resize(dict.size());
+  PPA_CUDA(cudaMemcpy(dia_dict_.get(), dict.data(), dict.size() * sizeof(double),
+                      cudaMemcpyHostToDevice));
+  dev_.dia_code = dia_code_.get();
+  dev_.dia_dict = dia_dict_.get();
+  dev_.dia_ndict = static_cast<int>(dict.size());
+  dev_.dia_ndiag = static_cast<int>(offs.size());
+  dev_.dia_stride = stride;
+  for (size_t j = 0; j < offs.size(); ++j) dev_.dia_off[j] = offs[j];
+  std::vector<unsigned> mask;
+  std::vector<int> irr;
+  std::vector<unsigned char> irr_codes;
+  std::vector<double> dflt;
+  if (!std::getenv("PPA_DISABLE_DIA_REGULAR") &&
+      kern::build_dia_regular(codes, n_, dev_.dia_ndiag, stride, dict, mask, irr, irr_codes,
+                              dflt)) {
+    dia_mask_.resize(mask.size());
+    PPA_CUDA(cudaMemcpy(dia_mask_.get(), mask.data(), mask.size() * sizeof(unsigned),
+                        cudaMemcpyHostToDevice));
+    // one row of slack: the irregular list may be empty
+    dia_irr_rows_.resize(irr.size() + 1);
+    dia_irr_codes_.resize(irr_codes.size() + static_cast<size_t>(stride));
+    if (!irr.empty()) {
+      PPA_CUDA(cudaMemcpy(dia_irr_rows_.get(), irr.data(), irr.size() * sizeof(int),
+                          cudaMemcpyHostToDevice));
+      PPA_CUDA(cudaMemcpy(dia_irr_codes_.get(), irr_codes.data(), irr_codes.size(),
+                          cudaMemcpyHostToDevice));
+    }
+    dev_.dia_mask = dia_mask_.get();
+    dev_.dia_irr_rows = dia_irr_rows_.get();
+    dev_.dia_irr_codes = dia_irr_codes_.get();
+    dev_.dia_nirr = static_cast<long long>(irr.size());
+    for (size_t j = 0; j < dflt.size(); ++j) dev_.dia_dflt[j] = dflt[j];
+  }
+  return true;
+}
+
+// Packed SELL-32 over the SELL-32 row order when it shrinks the stream
+// (kernels/spmv_packed.cu); PPA_DISABLE_PACKED keeps plain SELL-32.
+void CsrOperator::upload_packed(const CsrMatrix& m, const std::vector<int>& perm) {
+  if (std::getenv("PPA_DISABLE_PACKED")) return;
+  std::vector<long long> pp;
+  std::vector<short> pc;
+  std::vector<unsigned char> codes;
+  std::vector<double> pv, dict;
+  if (!kern::build_sell32_packed(m.row_ptr.data(), m.col_idx.data(), m.values.data(), n_, perm,
+                                 dev_.sell_entries, pp, pc, codes, pv, dict)) {
+    return;
+  }
+  // +kPackChunk*32 entries of slack so no vector load can run off the end
+  const size_t slack = 32 * kern::kPackChunk;
+  pk_ptr_.resize(pp.size());
+  PPA_CUDA(cudaMemcpy(pk_ptr_.get(), pp.data(), pp.size() * sizeof(long long),
+                      cudaMemcpyHostToDevice));
+  pk_col_.resize(pc.size() + slack);
+  PPA_CUDA(cudaMemcpy(pk_col_.get(), pc.data(), pc.size() * sizeof(short),
+                      cudaMemcpyHostToDevice));
+  if (!dict.empty()) {
+    pk_code_.resize(codes.size() + slack);
+    PPA_CUDA(cudaMemcpy(pk_code_.get(), codes.data(), codes.size(), cudaMemcpyHostToDevice));
+    pk_dict_.resize(dict.size());
+    PPA_CUDA(cudaMemcpy(pk_dict_.get(), dict.data(), dict.size() * sizeof(double),
+                        cudaMemcpyHostToDevice));
+    dev_.pk_code = pk_code_.get();
+    dev_.pk_dict = pk_dict_.get();
+    dev_.pk_ndict = static_cast<int>(dict.size());
+  } else {
+    pk_val_.resize(pv.size() + slack);
+    PPA_CUDA(cudaMemcpy(pk_val_.get(), pv.data(), pv.size() * sizeof(double),
+                        cudaMemcpyHostToDevice));
+    dev_.pk_val = pk_val_.get();
+  }
+  dev_.pk_col = pk_col_.get();
+  dev_.pk_entries = pp.back();
+  dev_.pk_ptr = pk_ptr_.get();
+}
+
+double CsrOperator::stream_bytes() const {
+  if (dev_.dia_mask) {
+    return 4.0 * dev_.nslices + double(dev_.dia_nirr) * (4.0 + dev_.dia_stride);
+  }
+  if (dev_.dia_code) return double(dev_.nslices) * 32.0 * dev_.dia_stride;
+  if (dev_.pk_ptr) {
+    return double(dev_.pk_entries) * kern::packed_entry_bytes(dev_.pk_ndict) +
+           8.0 * double(dev_.nslices + 1);
+  }
+  if (dev_.sell_val) return 12.0 * double(dev_.sell_entries) + 8.0 * double(dev_.nslices + 1);
+  return 12.0 * double(nnz_) + 4.0 * double(n_ + 1);
 }
 
 void CsrOperator::apply(const double* x, double* y, CostRecord& rec) const {
@@ -158,8 +266,8 @@ void CsrOperator::apply(const double* x, double* y, CostRecord& rec) const {
   kern::spmv(dev_, x, y, kern::EpiArgs{}, current_context().stream());
 }
 
-OperatorPtr make_csr_operator(const CsrMatrix& matrix) {
-  return std::make_shared<CsrOperator>(matrix);
+OperatorPtr make_csr_operator(const CsrMatrix& matrix, CsrLayout layout) {
+  return std::make_shared<CsrOperator>(matrix, OperatorKind::csr, std::vector<double>{}, layout);
 }
 
 OperatorPtr make_diagonal(std::vector<double> d) {

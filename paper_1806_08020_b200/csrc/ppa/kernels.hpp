@@ -32,7 +32,76 @@ struct CsrDevice {
   int sell_sigma = 1;
   long long sell_entries = 0;
   int bandwidth = -1;  // max |col - row| over the entries (-1: unknown)
+  // Packed SELL-32 (spmv_packed.cu): same slices and row order as SELL-32,
+  // widths rounded up to kPackChunk; column stored as an int16 offset from
+  // the row (kPackPad marks padding), value as a uint8 code into `pk_dict`
+  // (pk_ndict <= 256 distinct values) or, without a dictionary, as fp64.
+  // Entry k of lane l of slice s: pk_ptr[s] + 32*kPackChunk*(k/kPackChunk)
+  // + kPackChunk*l + k%kPackChunk.  nullptr when it would not save bytes.
+  const long long* pk_ptr = nullptr;  // [nslices+1]
+  const short* pk_col = nullptr;
+  const unsigned char* pk_code = nullptr;
+  const double* pk_val = nullptr;
+  const double* pk_dict = nullptr;
+  int pk_ndict = 0;  // 0: values stored in pk_val
+  long long pk_entries = 0;
+  // Diagonal-coded layout (spmv_dia.cu): row r's codes at
+  // dia_code[r*dia_stride + j] for diagonal j (offset dia_off[j], increasing);
+  // a code indexes dia_dict, kDiaAbsent marks no entry.  nullptr: not used.
+  const unsigned char* dia_code = nullptr;
+  const double* dia_dict = nullptr;
+  int dia_ndict = 0;
+  int dia_ndiag = 0;
+  int dia_stride = 0;  // 4, 8, 16 or 32 bytes per row
+  int dia_off[32] = {};
+  // Regular-row form (spmv_dia.cu k_spmv_diar): a row is regular when every
+  // diagonal is present with its default value dia_dflt[j]; regular rows
+  // stream no codes (bit r%32 of dia_mask[r/32] set).  The irregular rows
+  // are listed in dia_irr_rows with their codes at dia_irr_codes[k*stride].
+  // nullptr: every row streams its codes.
+  const unsigned* dia_mask = nullptr;
+  const int* dia_irr_rows = nullptr;
+  const unsigned char* dia_irr_codes = nullptr;
+  long long dia_nirr = 0;
+  double dia_dflt[32] = {};
 };
+
+constexpr int kDiaMaxDiag = 32;
+constexpr int kDiaMaxDict = 255;
+constexpr unsigned kDiaAbsent = 0xffu;
+/// Largest (diagonals x n) / nnz accepted for the diagonal layout.
+constexpr double kDiaMaxFill = 1.5;
+
+/// Host-side diagonal-coded construction; false when the matrix has more
+/// than kDiaMaxDiag diagonals, more than kDiaMaxDict distinct values or a
+/// fill above kDiaMaxFill.
+bool build_dia(const int* row_ptr, const int* col_idx, const double* values, int n,
+               std::vector<int>& offsets, int& stride, std::vector<unsigned char>& codes,
+               std::vector<double>& dict);
+/// Largest diagonal count of the regular-row kernel.
+constexpr int kDiaRegularMaxDiag = 16;
+/// Regular-row form from build_dia's codes; false unless at least half the
+/// rows are regular (and ndiag <= kDiaRegularMaxDiag).
+bool build_dia_regular(const std::vector<unsigned char>& codes, int n, int ndiag, int stride,
+                       const std::vector<double>& dict, std::vector<unsigned>& mask,
+                       std::vector<int>& irr_rows, std::vector<unsigned char>& irr_codes,
+                       std::vector<double>& dflt);
+
+/// Entries per lane per packed load group and the padding marker.
+constexpr int kPackChunk = 4;
+constexpr short kPackPad = -32768;
+constexpr int kPackMaxDict = 256;
+
+/// Host-side packed SELL-32 construction over an existing SELL-32 row order
+/// (`perm` empty: identity).  Returns false when a column offset does not
+/// fit int16 or the packed stream would not be smaller than SELL-32's.
+bool build_sell32_packed(const int* row_ptr, const int* col_idx, const double* values, int n,
+                         const std::vector<int>& perm, long long sell_entries,
+                         std::vector<long long>& pk_ptr, std::vector<short>& cols,
+                         std::vector<unsigned char>& codes, std::vector<double>& vals,
+                         std::vector<double>& dict);
+/// Bytes the packed stream occupies (cols + codes/values) per entry.
+inline double packed_entry_bytes(int ndict) { return 2.0 + (ndict > 0 ? 1.0 : 8.0); }
 
 /// Two polynomial factors fused into one matrix-powers pass (mpk.cu):
 ///   pair = false: y1 = x + a0 (A x),  y2 = y1 + b0 (A y1)   (two real roots)
@@ -89,6 +158,17 @@ struct EpiArgs {
 };
 
 void spmv(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep, cudaStream_t st);
+/// The packed-SELL path of spmv() (requires a.pk_ptr).
+void spmv_packed(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep,
+                 cudaStream_t st);
+/// The diagonal-coded paths of spmv() / spmm() (require a.dia_code).
+void spmv_dia(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep,
+              cudaStream_t st);
+void spmm_dia(const CsrDevice& a, const double* Y, long long ldy, int p, double* AY,
+              long long ldo, cudaStream_t st);
+/// The packed-SELL path of spmm() (requires a.pk_ptr).
+void spmm_packed(const CsrDevice& a, const double* Y, long long ldy, int p, double* AY,
+                 long long ldo, cudaStream_t st);
 
 /// AY[:,j] = A Y[:,j] for j < p (column-major, leading dims ldy / ldo):
 /// one matrix read per 8 columns with SELL-32, per-column SpMV otherwise.

@@ -58,10 +58,17 @@ using OperatorPtr = std::shared_ptr<const LinearOperator>;
 
 /// CSR operator whose matrix lives in HBM (uploaded once at construction,
 /// validated on the host first; src/operators.cpp:113-130).
+/// Device layout of a CSR operator.  `automatic`
+/// takes the first that applies of diagonal-coded, packed SELL-32, SELL-32,
+/// CSR row blocks; the others cap the choice at that layout (falling back
+/// down the same list when the matrix does not fit it).  Every layout gives
+/// bit-identical results.
+enum class CsrLayout { automatic = 0, csr = 1, sell32 = 2, sell32_packed = 3, dia = 4 };
+
 class CsrOperator final : public LinearOperator {
  public:
   explicit CsrOperator(const CsrMatrix& m, OperatorKind kind = OperatorKind::csr,
-                       std::vector<double> diag = {});
+                       std::vector<double> diag = {}, CsrLayout layout = CsrLayout::automatic);
   int dim() const override { return n_; }
   OperatorKind kind() const override { return kind_; }
   int mvps_per_apply() const override { return 1; }
@@ -76,6 +83,10 @@ class CsrOperator final : public LinearOperator {
   bool uses_sell() const { return dev_.sell_val != nullptr; }
   long long sell_entries() const { return dev_.sell_entries; }
   int sell_sigma() const { return dev_.sell_sigma; }
+  bool uses_packed() const { return dev_.pk_ptr != nullptr; }
+  bool uses_dia() const { return dev_.dia_code != nullptr; }
+  /// Matrix-stream bytes one SpMV reads in the layout the kernel uses.
+  double stream_bytes() const;
   /// Bytes one SpMV moves under the north-star model:
   /// 12*nnz + 4*(n+1) + 8n (x) + 8n (y).
   double model_bytes() const {
@@ -90,11 +101,20 @@ class CsrOperator final : public LinearOperator {
   std::vector<double> diag_;
   DBuffer<int> row_ptr_, col_idx_, blk_row_, sell_col_, sell_perm_;
   DBuffer<double> values_, sell_val_;
-  DBuffer<long long> slice_ptr_;
+  DBuffer<long long> slice_ptr_, pk_ptr_;
+  DBuffer<short> pk_col_;
+  DBuffer<unsigned char> pk_code_, dia_code_, dia_irr_codes_;
+  DBuffer<unsigned> dia_mask_;
+  DBuffer<int> dia_irr_rows_;
+  DBuffer<double> pk_val_, pk_dict_, dia_dict_;
   kern::CsrDevice dev_;
+
+  void upload_packed(const CsrMatrix& m, const std::vector<int>& perm);
+  bool upload_dia(const CsrMatrix& m);
 };
 
-OperatorPtr make_csr_operator(const CsrMatrix& matrix);
+OperatorPtr make_csr_operator(const CsrMatrix& matrix,
+                              CsrLayout layout = CsrLayout::automatic);
 /// Diagonal operator (src/operators.cpp:89-111), stored as a diagonal CSR.
 OperatorPtr make_diagonal(std::vector<double> diag_values);
 /// 2n-dimensional diag(A, A); one apply costs two applications of A

@@ -49,11 +49,18 @@ def test_spmv_bit_exact(cuda, name, gen):
 
 
 @pytest.mark.parametrize("name,gen", MATRICES)
-@pytest.mark.parametrize("layout", ["csr_rowblock", "sell_unsorted_only"])
+@pytest.mark.parametrize("layout", ["csr_rowblock", "sell_unsorted_only", "sell_unpacked",
+                                    "sell_packed"])
 def test_spmv_other_layouts_bit_exact(cuda, monkeypatch, name, gen, layout):
-    # the CSR row-block kernel (PPA_DISABLE_SELL) and SELL without sigma
-    # sorting (PPA_DISABLE_SIGMA: irregular rows fall back to the row-block path)
-    monkeypatch.setenv("PPA_DISABLE_SELL" if layout == "csr_rowblock" else "PPA_DISABLE_SIGMA", "1")
+    # the CSR row-block kernel (PPA_DISABLE_SELL), SELL without sigma sorting
+    # (PPA_DISABLE_SIGMA: irregular rows fall back to the row-block path) and
+    # SELL-32 without the packed / diagonal-coded streams, packed SELL-32
+    # without the diagonal-coded one
+    env = {"csr_rowblock": ["PPA_DISABLE_SELL"], "sell_unsorted_only": ["PPA_DISABLE_SIGMA"],
+           "sell_unpacked": ["PPA_DISABLE_PACKED", "PPA_DISABLE_DIA"],
+           "sell_packed": ["PPA_DISABLE_DIA"]}[layout]
+    for e in env:
+        monkeypatch.setenv(e, "1")
     P, Q = gen(ppa.CsrMatrix), gen(O.Csr)
     A = ppa.make_csr_operator(P)
     x = O.normal_vector(P.n, 4, 9)
@@ -62,6 +69,70 @@ def test_spmv_other_layouts_bit_exact(cuda, monkeypatch, name, gen, layout):
     assert np.array_equal(host(y), O.csr_operator(Q).apply(x))
     roots = _roots_mixed()
     out = cuda.empty(P.n, dtype=cuda.float64, device="cuda")
+    ppa.apply_poly(roots, A, dev(cuda, x), out)
+    assert np.array_equal(host(out), O.apply_poly(roots, O.csr_operator(Q), x))
+
+
+EXPECTED_LAYOUT = {
+    # bidiagonal a_ii = i: 777 distinct values, width 2 -> packing would grow the stream
+    "bidiag": ("sell32", 0),
+    "convdiff_ref": ("dia_coded", None),
+    "convdiff_const": ("dia_coded", 4),  # C, E, W, N = S
+    "laplace3d": ("dia_coded", 2),
+    # n = 20000: random offsets still fit int16; > 256 values -> fp64 stream
+    "random_poisson": ("sell32_packed", 0),
+}
+
+
+@pytest.mark.parametrize("name,gen", MATRICES)
+def test_layout_selection(cuda, name, gen):
+    lay = ppa.make_csr_operator(gen(ppa.CsrMatrix)).layout()
+    want, nd = EXPECTED_LAYOUT[name]
+    assert lay["layout"] == want
+    if nd is not None:
+        assert lay["dict_size"] == nd
+
+
+@pytest.mark.parametrize("cap,want", [("auto", "dia_coded"), ("csr", "csr"), ("sell32", "sell32"),
+                                      ("sell32_packed", "sell32_packed"),
+                                      ("dia_coded", "dia_coded")])
+def test_layout_cap_bit_exact(cuda, cap, want):
+    # ppa_csr_operator_layout: every cap computes the same bits
+    P, Q = ppa.CsrMatrix.laplacian_3d(19), O.Csr.laplacian_3d(19)
+    A = ppa.make_csr_operator(P, cap)
+    assert A.layout()["layout"] == want
+    x = O.normal_vector(P.n, 8, 1)
+    roots = _roots_mixed()
+    out = cuda.empty(P.n, dtype=cuda.float64, device="cuda")
+    ppa.apply_poly(roots, A, dev(cuda, x), out)
+    assert np.array_equal(host(out), O.apply_poly(roots, O.csr_operator(Q), x))
+
+
+def test_packed_fp64_values_and_perm(cuda):
+    # packed stream without a value table (> 256 distinct values), sigma-sorted
+    # rows of very different lengths, offsets near the int16 limit
+    n = 70000
+    rng = np.random.default_rng(5)
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        L = 9 + (i * 7919) % 13
+        off = np.unique(rng.integers(-32767, 32768, L))
+        c = np.clip(i + off, 0, n - 1)
+        c = np.unique(c)
+        rows += [i] * len(c)
+        cols += list(c)
+        vals += list(rng.standard_normal(len(c)))
+    P = ppa.CsrMatrix.from_triplets(n, rows, cols, vals)
+    Q = O.Csr.from_triplets(n, rows, cols, vals)
+    A = ppa.make_csr_operator(P)
+    lay = A.layout()
+    assert lay["layout"] == "sell32_packed" and lay["dict_size"] == 0 and lay["sigma"] > 1
+    x = O.normal_vector(n, 2, 2)
+    y = cuda.empty(n, dtype=cuda.float64, device="cuda")
+    A.apply(dev(cuda, x), y)
+    assert np.array_equal(host(y), O.csr_operator(Q).apply(x))
+    roots = _roots_mixed()
+    out = cuda.empty(n, dtype=cuda.float64, device="cuda")
     ppa.apply_poly(roots, A, dev(cuda, x), out)
     assert np.array_equal(host(out), O.apply_poly(roots, O.csr_operator(Q), x))
 

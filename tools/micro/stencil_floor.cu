@@ -1,0 +1,142 @@
+// Floors for the diagonal-coded SpMV at config-3 size (n = 160^3):
+//   copy     y = x                       (16 B/row)
+//   stencil  y = sum_j c_j x[r + off_j]   (7 gathers, constants, no codes)
+//   codes    y = sum_j tab[code] x[...]   (8 B of codes per row)
+// nvcc -O3 -gencode arch=compute_100a,code=sm_100a stencil_floor.cu -o /tmp/sf
+#include <cstdio>
+#include <cuda_runtime.h>
+
+constexpr int N = 160;
+constexpr int NN = N * N * N;
+__constant__ int c_off[8];
+
+__global__ void k_copy(const double* __restrict__ x, double* __restrict__ y, int n) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) y[r] = x[r];
+}
+
+__global__ void k_stencil(const double* __restrict__ x, double* __restrict__ y, int n) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < 7; ++j) {
+    int c = min(max(r + c_off[j], 0), n - 1);
+    s = __dadd_rn(s, __dmul_rn(j == 3 ? 6.0 : -1.0, __ldg(x + c)));
+  }
+  y[r] = s;
+}
+
+__global__ void k_codes(const uint2* __restrict__ codes, const double* __restrict__ x,
+                        double* __restrict__ y, int n) {
+  __shared__ double tab[256];
+  if (threadIdx.x < 2) tab[threadIdx.x] = threadIdx.x ? -1.0 : 6.0;
+  __syncthreads();
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  uint2 w = __ldcs(codes + r);
+  double xv[7];
+#pragma unroll
+  for (int j = 0; j < 7; ++j) xv[j] = __ldg(x + min(max(r + c_off[j], 0), n - 1));
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < 7; ++j) {
+    unsigned c = __byte_perm(j < 4 ? w.x : w.y, 0, 0x4440 | (j & 3));
+    if (c != 0xff) s = __dadd_rn(s, __dmul_rn(tab[c], xv[j]));
+  }
+  y[r] = s;
+}
+
+__constant__ double c_tab[256];
+// codes, values by select (no table)
+__global__ void k_codes_sel(const uint2* __restrict__ codes, const double* __restrict__ x,
+                            double* __restrict__ y, int n) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  uint2 w = __ldcs(codes + r);
+  double xv[7];
+#pragma unroll
+  for (int j = 0; j < 7; ++j) xv[j] = __ldg(x + min(max(r + c_off[j], 0), n - 1));
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < 7; ++j) {
+    unsigned c = __byte_perm(j < 4 ? w.x : w.y, 0, 0x4440 | (j & 3));
+    if (c != 0xff) s = __dadd_rn(s, __dmul_rn(c ? -1.0 : 6.0, xv[j]));
+  }
+  y[r] = s;
+}
+// codes, table in shared but no barrier-dependent init (static pattern), ldg codes
+__global__ void k_codes_ldg(const uint2* __restrict__ codes, const double* __restrict__ x,
+                            double* __restrict__ y, int n) {
+  __shared__ double tab[256];
+  if (threadIdx.x < 2) tab[threadIdx.x] = threadIdx.x ? -1.0 : 6.0;
+  __syncthreads();
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  uint2 w = __ldg(codes + r);
+  double xv[7];
+#pragma unroll
+  for (int j = 0; j < 7; ++j) xv[j] = __ldg(x + min(max(r + c_off[j], 0), n - 1));
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < 7; ++j) {
+    unsigned c = __byte_perm(j < 4 ? w.x : w.y, 0, 0x4440 | (j & 3));
+    if (c != 0xff) s = __dadd_rn(s, __dmul_rn(tab[c], xv[j]));
+  }
+  y[r] = s;
+}
+// codes loaded, then ignored except for the absent test (constant values)
+__global__ void k_codes_only(const uint2* __restrict__ codes, const double* __restrict__ x,
+                             double* __restrict__ y, int n) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  uint2 w = __ldcs(codes + r);
+  double xv[7];
+#pragma unroll
+  for (int j = 0; j < 7; ++j) xv[j] = __ldg(x + min(max(r + c_off[j], 0), n - 1));
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < 7; ++j) s = __dadd_rn(s, __dmul_rn(j == 3 ? 6.0 : -1.0, xv[j]));
+  y[r] = s + (w.x == 12345u ? 1.0 : 0.0);
+}
+
+template <typename F>
+float timeit(F f, int reps) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  for (int i = 0; i < 3; ++i) f();
+  cudaEventRecord(a);
+  for (int i = 0; i < reps; ++i) f();
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms * 1000.f / reps;
+}
+
+int main() {
+  int off[8] = {-N * N, -N, -1, 0, 1, N, N * N, 0};
+  cudaMemcpyToSymbol(c_off, off, sizeof off);
+  double *x, *y;
+  uint2* codes;
+  cudaMalloc(&x, NN * 8);
+  cudaMalloc(&y, NN * 8);
+  cudaMalloc(&codes, NN * 8);
+  cudaMemset(x, 0, NN * 8);
+  cudaMemset(codes, 0, NN * 8);
+  for (int bs : {128, 256, 512}) {
+    int g = (NN + bs - 1) / bs;
+    float t0 = timeit([&] { k_copy<<<g, bs>>>(x, y, NN); }, 50);
+    // ping-pong like pi(A)v so x is the previous output
+    float t1 = timeit([&] { k_stencil<<<g, bs>>>(x, y, NN); std::swap(x, y); }, 50);
+    float t2 = timeit([&] { k_codes<<<g, bs>>>(codes, x, y, NN); std::swap(x, y); }, 50);
+    float t3 = timeit([&] { k_codes_sel<<<g, bs>>>(codes, x, y, NN); std::swap(x, y); }, 50);
+    float t4 = timeit([&] { k_codes_ldg<<<g, bs>>>(codes, x, y, NN); std::swap(x, y); }, 50);
+    float t5 = timeit([&] { k_codes_only<<<g, bs>>>(codes, x, y, NN); std::swap(x, y); }, 50);
+    printf("bs %d: copy %.2f us (%.0f GB/s)  stencil %.2f us  codes %.2f  sel %.2f  ldg %.2f  only %.2f\n", bs, t0,
+           16.0 * NN / t0 / 1e3, t1, t2, t3, t4, t5);
+  }
+  printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
