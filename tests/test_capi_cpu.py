@@ -70,6 +70,8 @@ def test_rng_streams_bit_exact():
                               O.normal_vector(1001, seed, stream))
     v = ppa.normal_vector(200000, 7, 3)
     assert abs(v.mean()) < 0.01 and abs(v.std() - 1) < 0.01
+    # threaded path (chunks split across host threads), odd length
+    assert np.array_equal(ppa.normal_vector(200001, 7, 3), O.normal_vector(200001, 7, 3))
 
 
 def _roots(rng, k_real=20, k_cplx=8):

@@ -128,18 +128,27 @@ def test_config_solve_vs_fixture(cuda, k):
     r = ppa.solve_double(A, cfg) if k == 5 else ppa.solve(A, cfg)
     assert r["converged"] == g["converged"]
     assert abs(r["rtol"] - g["rtol"]) <= 1e-10 * g["rtol"]  # same norm estimate
+    # the polynomial is built before any Arnoldi cycle: it must agree for
+    # every config (CGS2 vs MGS2 roundoff only)
+    inner = _canon_pairs(_c(g["inner_poly"] if k == 5 else g["poly"]))
+    got_inner = _canon_pairs(r["inner_poly"] if k == 5 else r["poly"])
+    assert got_inner.size == inner.size
+    assert np.max(np.abs(got_inner - inner) / np.abs(inner)) < 1e-6
     if not r["converged"]:
+        # config 4 does not converge in 100 cycles on either side (DESIGN.md
+        # "Config 4"); both run the full budget and end at a comparable
+        # residual level
+        assert r["cycles"] == g["cycles"] == cfg.max_cycles
+        hist, ghist = r["cycle_max_residual"], np.array(g["cycle_max_residual"])
+        assert 0.1 < np.min(hist) / np.min(ghist) < 10.0
         return
     assert np.all(r["residuals"] <= r["rtol"])
     assert abs(r["cost"]["mvps"] - g["cost"]["mvps"]) <= 0.05 * g["cost"]["mvps"]
     if k in (2, 5):
         # Constant-Peclet convection-diffusion: the certified Ritz values lie in
         # the pseudospectrum, where CPU and
-        # GPU roundoff select different, equally valid pairs.  The polynomial
-        # built before any Arnoldi cycle must still agree.
-        inner = _canon_pairs(_c(g["inner_poly"] if k == 5 else g["poly"]))
-        got_inner = _canon_pairs(r["inner_poly"] if k == 5 else r["poly"])
-        assert np.max(np.abs(got_inner - inner) / np.abs(inner)) < 1e-6
+        # GPU roundoff select different, equally valid pairs (the polynomial
+        # was compared above).
         return
     got = np.sort_complex(r["eigenvalues"])
     ref = np.sort_complex(_c(g["eigenvalues"]))
