@@ -198,13 +198,13 @@ struct DiaRParams {
 // the regular sweep.
 constexpr int RB = 512;
 
-template <int MODE, bool COMPL, int NW>
+template <int MODE, bool COMPL, int ND>
 __global__ void __launch_bounds__(RB) k_spmv_diar(
     const unsigned* __restrict__ mask, const int* __restrict__ irr_rows,
     const unsigned char* __restrict__ irr_codes, int n_irr, int gx,
-    const double* __restrict__ dict, const DiaRParams P, int ndiag, int n,
-    const double* __restrict__ x, double* y, double c0, double c1, const double* o,
-    const double* base) {
+    const double* __restrict__ dict, const DiaRParams P, int n, const double* __restrict__ x,
+    double* y, double c0, double c1, const double* o, const double* base) {
+  constexpr int NW = ND <= 4 ? 1 : ND <= 8 ? 2 : 4;  // code words per row (stride / 4)
   double sum = 0.0;
   int r;
   const int bx = blockIdx.x;
@@ -214,14 +214,14 @@ __global__ void __launch_bounds__(RB) k_spmv_diar(
     r = __ldg(irr_rows + k);
     unsigned ec[NW];
     load_codes<NW>(ec, reinterpret_cast<const unsigned*>(irr_codes) + static_cast<long long>(k) * NW);
-    double xv[4 * NW];
+    double xv[ND];
 #pragma unroll
-    for (int j = 0; j < 4 * NW; ++j) {
+    for (int j = 0; j < ND; ++j) {
       const unsigned c = code_of(ec[j / 4], j);
       xv[j] = __ldg(x + (c != kDiaAbsent ? r + P.off[j] : r));
     }
 #pragma unroll
-    for (int j = 0; j < 4 * NW; ++j) {
+    for (int j = 0; j < ND; ++j) {
       const unsigned c = code_of(ec[j / 4], j);
       if (c != kDiaAbsent) sum = __dadd_rn(sum, __dmul_rn(__ldg(dict + c), xv[j]));
     }
@@ -229,23 +229,19 @@ __global__ void __launch_bounds__(RB) k_spmv_diar(
     r = (bx - gx) * RB + threadIdx.x;
     if (r >= n) return;
     const unsigned m = __ldg(mask + (r >> 5));
-    // all 4*NW slots gather (padding slots have offset 0 and hit x[r]'s
-    // line): predicating them on ndiag would predicate the parameter loads
-    double xv[4 * NW];
+    double xv[ND];
 #pragma unroll
-    for (int j = 0; j < 4 * NW; ++j) xv[j] = __ldg(x + min(max(r + P.off[j], 0), n - 1));
+    for (int j = 0; j < ND; ++j) xv[j] = __ldg(x + min(max(r + P.off[j], 0), n - 1));
 #pragma unroll
-    for (int j = 0; j < 4 * NW; ++j) {
-      if (j < ndiag) sum = __dadd_rn(sum, __dmul_rn(P.val[j], xv[j]));
-    }
+    for (int j = 0; j < ND; ++j) sum = __dadd_rn(sum, __dmul_rn(P.val[j], xv[j]));
     if (!((m >> (r & 31)) & 1u)) return;
   }
   y[r] = epilogue<MODE, COMPL>(r, sum, x, c0, c1, o, base);
 }
 
-template <int MODE, bool COMPL, int NW>
-void launch_diar_nw(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep,
-                    cudaStream_t st) {
+template <int MODE, bool COMPL, int ND>
+void launch_diar(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep,
+                 cudaStream_t st) {
   DiaRParams P{};
   for (int j = 0; j < a.dia_ndiag; ++j) {
     P.off[j] = a.dia_off[j];
@@ -253,21 +249,26 @@ void launch_diar_nw(const CsrDevice& a, const double* x, double* y, const EpiArg
   }
   const int gx = static_cast<int>((a.dia_nirr + RB - 1) / RB);
   const int grid = gx + (a.n + RB - 1) / RB;
-  k_spmv_diar<MODE, COMPL, NW><<<grid, RB, 0, st>>>(
+  k_spmv_diar<MODE, COMPL, ND><<<grid, RB, 0, st>>>(
       a.dia_mask, a.dia_irr_rows, a.dia_irr_codes, static_cast<int>(a.dia_nirr), gx, a.dia_dict,
-      P, a.dia_ndiag, a.n, x, y, ep.c0, ep.c1, ep.o, ep.base);
+      P, a.n, x, y, ep.c0, ep.c1, ep.o, ep.base);
+}
+
+// The regular-row kernel is instantiated per diagonal count so the row sum
+// is straight-line code over exactly the matrix's diagonals.
+template <int MODE, bool COMPL, int ND = 1>
+void launch_diar_nd(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep,
+                    cudaStream_t st) {
+  if constexpr (ND < kDiaRegularMaxDiag) {
+    if (a.dia_ndiag != ND) return launch_diar_nd<MODE, COMPL, ND + 1>(a, x, y, ep, st);
+  }
+  launch_diar<MODE, COMPL, ND>(a, x, y, ep, st);
 }
 
 template <int MODE, bool COMPL>
 void launch_dia(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep,
                 cudaStream_t st) {
-  if (a.dia_mask) {
-    switch (a.dia_stride) {
-      case 4: return launch_diar_nw<MODE, COMPL, 1>(a, x, y, ep, st);
-      case 8: return launch_diar_nw<MODE, COMPL, 2>(a, x, y, ep, st);
-      default: return launch_diar_nw<MODE, COMPL, 4>(a, x, y, ep, st);
-    }
-  }
+  if (a.dia_mask) return launch_diar_nd<MODE, COMPL>(a, x, y, ep, st);
   switch (a.dia_stride) {
     case 4: return launch_dia_nw<MODE, COMPL, 1>(a, x, y, ep, st);
     case 8: return launch_dia_nw<MODE, COMPL, 2>(a, x, y, ep, st);

@@ -108,6 +108,52 @@ def test_layout_cap_bit_exact(cuda, cap, want):
     assert np.array_equal(host(out), O.apply_poly(roots, O.csr_operator(Q), x))
 
 
+def _banded(n, offsets, vals, irregular=()):
+    """Constant-diagonal band matrix; rows in `irregular` get a perturbed value."""
+    rows, cols, vv = [], [], []
+    for i in range(n):
+        for o, v in zip(offsets, vals):
+            j = i + o
+            if 0 <= j < n:
+                rows.append(i)
+                cols.append(j)
+                vv.append(v * (1.5 if i in irregular else 1.0))
+    return rows, cols, vv
+
+
+@pytest.mark.parametrize("offsets", [
+    (-1, 0, 1),                                        # 3 diagonals: one code word
+    (-41, -40, -39, -1, 0, 1, 39, 40, 41),             # 9-point: four code words
+    tuple(range(-8, 9)),                               # 17 diagonals: coded form only
+])
+def test_dia_diagonal_counts_bit_exact(cuda, offsets):
+    n = 6000
+    vals = [float(k + 2) * (-1) ** k for k in range(len(offsets))]
+    rows, cols, vv = _banded(n, offsets, vals, irregular={5, 1234, 4001})
+    P = ppa.CsrMatrix.from_triplets(n, rows, cols, vv)
+    Q = O.Csr.from_triplets(n, rows, cols, vv)
+    A = ppa.make_csr_operator(P)
+    assert A.layout()["layout"] == "dia_coded"
+    x = O.normal_vector(n, 3, 3)
+    y = cuda.empty(n, dtype=cuda.float64, device="cuda")
+    A.apply(dev(cuda, x), y)
+    assert np.array_equal(host(y), O.csr_operator(Q).apply(x))
+    roots = _roots_mixed()
+    out = cuda.empty(n, dtype=cuda.float64, device="cuda")
+    ppa.apply_poly(roots, A, dev(cuda, x), out)
+    assert np.array_equal(host(out), O.apply_poly(roots, O.csr_operator(Q), x))
+    # multi-RHS
+    ld = (n + 31) // 32 * 32
+    Y = np.zeros((3, ld))
+    for j in range(3):
+        Y[j, :n] = O.normal_vector(n, 40 + j, 1)
+    AYd = cuda.zeros(3 * ld, dtype=cuda.float64, device="cuda")
+    ppa.spmm(A, dev(cuda, Y.ravel()), ld, 3, AYd, ld)
+    AY = host(AYd).reshape(3, ld)
+    for j in range(3):
+        assert np.array_equal(AY[j, :n], O.csr_operator(Q).apply(Y[j, :n]))
+
+
 def test_packed_fp64_values_and_perm(cuda):
     # packed stream without a value table (> 256 distinct values), sigma-sorted
     # rows of very different lengths, offsets near the int16 limit

@@ -100,6 +100,23 @@ __global__ void k_codes_only(const uint2* __restrict__ codes, const double* __re
   y[r] = s + (w.x == 12345u ? 1.0 : 0.0);
 }
 
+// regular-row kernel ingredients, one at a time
+template <int NG, bool MASK, bool EPI>
+__global__ void k_var(const unsigned* __restrict__ mask, const double* __restrict__ x,
+                      double* __restrict__ y, int n, double c0) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  unsigned m = MASK ? __ldg(mask + (r >> 5)) : 0xffffffffu;
+  double xv[NG];
+#pragma unroll
+  for (int j = 0; j < NG; ++j) xv[j] = __ldg(x + min(max(r + c_off[j], 0), n - 1));
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < 7; ++j) s = __dadd_rn(s, __dmul_rn(j == 3 ? 6.0 : -1.0, xv[j]));
+  if (!((m >> (r & 31)) & 1u)) return;
+  y[r] = EPI ? __dadd_rn(__ldg(x + r), __dmul_rn(c0, s)) : s;
+}
+
 template <typename F>
 float timeit(F f, int reps) {
   cudaEvent_t a, b;
@@ -136,6 +153,18 @@ int main() {
     float t5 = timeit([&] { k_codes_only<<<g, bs>>>(codes, x, y, NN); std::swap(x, y); }, 50);
     printf("bs %d: copy %.2f us (%.0f GB/s)  stencil %.2f us  codes %.2f  sel %.2f  ldg %.2f  only %.2f\n", bs, t0,
            16.0 * NN / t0 / 1e3, t1, t2, t3, t4, t5);
+  }
+  unsigned* mask;
+  cudaMalloc(&mask, (NN / 32 + 1) * 4);
+  cudaMemset(mask, 0xff, (NN / 32 + 1) * 4);
+  {
+    int bs = 512, g = (NN + bs - 1) / bs;
+    float a = timeit([&] { k_var<7, false, false><<<g, bs>>>(mask, x, y, NN, 0.5); std::swap(x, y); }, 50);
+    float b = timeit([&] { k_var<8, false, false><<<g, bs>>>(mask, x, y, NN, 0.5); std::swap(x, y); }, 50);
+    float c = timeit([&] { k_var<7, true, false><<<g, bs>>>(mask, x, y, NN, 0.5); std::swap(x, y); }, 50);
+    float d = timeit([&] { k_var<7, false, true><<<g, bs>>>(mask, x, y, NN, 0.5); std::swap(x, y); }, 50);
+    float e = timeit([&] { k_var<8, true, true><<<g, bs>>>(mask, x, y, NN, 0.5); std::swap(x, y); }, 50);
+    printf("var: base7 %.2f  gather8 %.2f  mask %.2f  epi %.2f  all %.2f us\n", a, b, c, d, e);
   }
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;

@@ -1,4 +1,7 @@
-"""Kernel-profiling driver (run under ncu on one GPU): config 3 pi(A)v, CGS2 and V*Q."""
+"""Kernel-profiling driver (run under ncu on one GPU): config 3 pi(A)v, CGS2 and V*Q.
+
+    python tools/prof_kernels.py [all|spmv|cgs] [auto|sell32|sell32_packed|dia_coded|csr]
+"""
 import os
 import sys
 
@@ -9,11 +12,12 @@ import torch
 import paper_1806_08020_b200 as ppa
 
 what = sys.argv[1] if len(sys.argv) > 1 else "all"
+layout = sys.argv[2] if len(sys.argv) > 2 else "auto"
 torch.cuda.set_device(0)
 ppa.set_stream(torch.cuda.current_stream())
 csr = ppa.CsrMatrix.config(3)
 n = csr.n
-A = ppa.make_csr_operator(csr)
+A = ppa.make_csr_operator(csr, layout)
 # 8 real roots spread over the config-3 spectrum (the timing does not depend on them)
 roots = ppa.leja_order(np.linspace(30.0, 311000.0, 8))
 v = torch.tensor(ppa.normal_vector(n, 2, 3), device="cuda")
