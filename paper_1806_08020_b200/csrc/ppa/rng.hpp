@@ -70,23 +70,22 @@ inline double normal_at(uint64_t k, uint64_t i) {
 /// Entries are independent (counter-based), so the host threads split the
 /// range without changing a bit of the result.  Each Box-Muller pair is
 /// evaluated once for both of its members (same r and t as normal_at).
-inline std::vector<double> normal_vector(long long n, uint64_t seed, uint64_t stream) {
-  std::vector<double> v(static_cast<size_t>(n));
+inline void fill_normal(double* v, long long n, uint64_t seed, uint64_t stream) {
   const uint64_t k = key(seed, stream);
   auto fill = [&](long long b, long long e) {  // b even
     for (long long i = b; i < e; i += 2) {
       const uint64_t p = static_cast<uint64_t>(i) >> 1;
       const double r = std::sqrt(-2.0 * std::log(uniform(k, 2 * p)));
       const double t = 6.283185307179586 * uniform(k, 2 * p + 1);
-      v[static_cast<size_t>(i)] = r * std::cos(t);
-      if (i + 1 < e) v[static_cast<size_t>(i) + 1] = r * std::sin(t);
+      v[i] = r * std::cos(t);
+      if (i + 1 < e) v[i + 1] = r * std::sin(t);
     }
   };
   const unsigned hw = std::thread::hardware_concurrency();
   const long long nt = n < (1 << 16) ? 1 : std::max(1u, std::min(hw, 64u));
   if (nt == 1) {
     fill(0, n);
-    return v;
+    return;
   }
   std::vector<std::thread> pool;
   const long long chunk = ((n + nt - 1) / nt + 1) & ~1LL;
@@ -94,6 +93,11 @@ inline std::vector<double> normal_vector(long long n, uint64_t seed, uint64_t st
     pool.emplace_back(fill, t * chunk, std::min(n, (t + 1) * chunk));
   }
   for (auto& th : pool) th.join();
+}
+
+inline std::vector<double> normal_vector(long long n, uint64_t seed, uint64_t stream) {
+  std::vector<double> v(static_cast<size_t>(n));
+  fill_normal(v.data(), n, seed, stream);
   return v;
 }
 

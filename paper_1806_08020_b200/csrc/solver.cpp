@@ -9,7 +9,11 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <future>
 #include <limits>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <stdexcept>
 
 #include "ppa/kernels.hpp"
@@ -33,6 +37,108 @@ DBuffer<double> upload(const std::vector<double>& h) {
 }
 
 long long round_ld(int n) { return (static_cast<long long>(n) + 31) / 32 * 32; }
+
+// The seeded start vectors of one solve,
+// generated on a host thread in the order the solve consumes them, so that
+// drawing the next vector overlaps the device work of the current phase
+// (norm estimate, polynomial build).  take() waits for a stream's vector
+// and returns a fresh device copy (a damping probe restarts from the same
+// Arnoldi start vector).
+// Pinned host buffers for the start vectors, kept across solves (page-locking
+// 32 MB costs milliseconds; a pinned source makes the upload a DMA at full
+// PCIe/C2C speed instead of a staged pageable copy).
+class PinnedPool {
+ public:
+  static PinnedPool& get() {
+    static PinnedPool p;
+    return p;
+  }
+  double* acquire(size_t count) {
+    std::lock_guard<std::mutex> g(mu_);
+    for (size_t i = 0; i < free_.size(); ++i) {
+      if (free_[i].second >= count) {
+        double* p = free_[i].first;
+        free_.erase(free_.begin() + static_cast<long>(i));
+        return p;
+      }
+    }
+    void* p = nullptr;
+    if (cudaMallocHost(&p, count * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      throw std::runtime_error("StartVectors: pinned allocation failed");
+    }
+    size_[static_cast<double*>(p)] = count;
+    return static_cast<double*>(p);
+  }
+  void release(double* p) {
+    std::lock_guard<std::mutex> g(mu_);
+    free_.emplace_back(p, size_[p]);
+    // keep at most four buffers; drop the smallest
+    while (free_.size() > 4) {
+      auto it = std::min_element(free_.begin(), free_.end(),
+                                 [](const auto& a, const auto& b) { return a.second < b.second; });
+      cudaFreeHost(it->first);
+      size_.erase(it->first);
+      free_.erase(it);
+    }
+  }
+
+ private:
+  std::mutex mu_;
+  std::vector<std::pair<double*, size_t>> free_;
+  std::map<double*, size_t> size_;
+};
+
+struct PinnedRelease {
+  void operator()(double* p) const { PinnedPool::get().release(p); }
+};
+
+class StartVectors {
+ public:
+  StartVectors(int n, unsigned long long seed, std::vector<uint64_t> streams)
+      : n_(n), streams_(std::move(streams)) {
+    for (size_t i = 0; i < streams_.size(); ++i) {
+      host_.emplace_back(PinnedPool::get().acquire(static_cast<size_t>(n)));
+      ready_.emplace_back();
+    }
+    std::vector<std::promise<void>> done(streams_.size());
+    for (size_t i = 0; i < streams_.size(); ++i) ready_[i] = done[i].get_future().share();
+    worker_ = std::thread([this, seed, done = std::move(done)]() mutable {
+      for (size_t i = 0; i < streams_.size(); ++i) {
+        try {
+          rng::fill_normal(host_[i].get(), n_, seed, streams_[i]);
+          done[i].set_value();
+        } catch (...) {
+          done[i].set_exception(std::current_exception());
+        }
+      }
+    });
+  }
+  StartVectors(const StartVectors&) = delete;
+  StartVectors& operator=(const StartVectors&) = delete;
+  ~StartVectors() {
+    if (worker_.joinable()) worker_.join();
+  }
+
+  DBuffer<double> take(uint64_t stream) {
+    for (size_t i = 0; i < streams_.size(); ++i) {
+      if (streams_[i] != stream) continue;
+      ready_[i].get();
+      DBuffer<double> d(static_cast<size_t>(n_));
+      PPA_CUDA(cudaMemcpy(d.get(), host_[i].get(), static_cast<size_t>(n_) * sizeof(double),
+                          cudaMemcpyHostToDevice));
+      return d;
+    }
+    throw std::logic_error("StartVectors: stream not scheduled");
+  }
+
+ private:
+  int n_;
+  std::vector<uint64_t> streams_;
+  std::vector<std::unique_ptr<double, PinnedRelease>> host_;
+  std::vector<std::shared_future<void>> ready_;
+  std::thread worker_;
+};
 
 struct CheckOutcome {
   std::vector<cplx> mu;
@@ -211,9 +317,9 @@ RitzSet select_pairs(const ArnoldiState& st, const SolveConfig& cfg, RitzOrderin
 }
 
 FirstCycle first_cycle(const LinearOperator& a, const LinearOperator& op, const SolveConfig& cfg,
-                       RitzOrdering ordering, int nchk, CostRecord& rec) {
+                       RitzOrdering ordering, int nchk, CostRecord& rec, StartVectors& sv) {
   const int n = a.dim();
-  DBuffer<double> v0 = upload(rng::normal_vector(n, cfg.seed, rng::kArnoldiStart));
+  DBuffer<double> v0 = sv.take(rng::kArnoldiStart);
   FirstCycle f;
   f.st = arnoldi_init(v0.get(), n, cfg.m, rec);
   f.start_dim = f.st.cur_dim;
@@ -225,7 +331,7 @@ FirstCycle first_cycle(const LinearOperator& a, const LinearOperator& op, const 
 
 // Cycle loop shared by solve and solve_double.
 void run_cycles(const LinearOperator& a, const LinearOperator& op, const SolveConfig& cfg,
-                RitzOrdering ordering, EigResult& res, CostRecord& rec,
+                RitzOrdering ordering, EigResult& res, CostRecord& rec, StartVectors& sv,
                 FirstCycle* probe = nullptr) {
   Context& ctx = current_context();
   const int n = a.dim();
@@ -233,7 +339,7 @@ void run_cycles(const LinearOperator& a, const LinearOperator& op, const SolveCo
   if (probe) {
     st = std::move(probe->st);
   } else {
-    DBuffer<double> v0 = upload(rng::normal_vector(n, cfg.seed, rng::kArnoldiStart));
+    DBuffer<double> v0 = sv.take(rng::kArnoldiStart);
     st = arnoldi_init(v0.get(), n, cfg.m, rec);
   }
   (void)ctx;
@@ -336,9 +442,10 @@ PolyPrecond stabilise(PolyPrecond p, const SolveConfig& cfg) {
 // A passing probe is handed back for reuse as the solve's first cycle;
 // failed probes are logged as discarded cycles.  All probe costs count.
 PolyPrecond damping_search(const OperatorPtr& a, const SolveConfig& cfg, CostRecord& rec,
-                           std::vector<CycleStats>& history, std::optional<FirstCycle>& keep) {
+                           std::vector<CycleStats>& history, std::optional<FirstCycle>& keep,
+                           StartVectors& sv) {
   const int n = a->dim();
-  DBuffer<double> b = upload(rng::normal_vector(n, cfg.seed, rng::kPolyStart));
+  DBuffer<double> b = sv.take(rng::kPolyStart);
   DBuffer<double> ab;
   int d = cfg.degree;
   bool damped = false;
@@ -350,7 +457,7 @@ PolyPrecond damping_search(const OperatorPtr& a, const SolveConfig& cfg, CostRec
       p.damping_power = 1;
     }
     const OperatorPtr op = make_poly_operator(a, p);
-    FirstCycle f = first_cycle(*a, *op, cfg, RitzOrdering::target_one, cfg.k, rec);
+    FirstCycle f = first_cycle(*a, *op, cfg, RitzOrdering::target_one, cfg.k, rec, sv);
     const bool pass = static_cast<int>(f.chk.mu.size()) >= cfg.nev &&
                       check_ideal_order(f.chk.mu, cfg.nev);
     if (pass || d <= 1) {
@@ -389,7 +496,8 @@ PolyPrecond damping_heuristic(const OperatorPtr& a, const SolveConfig& cfg, Cost
   if (cfg.degree < 1) throw std::invalid_argument("damping_heuristic: degree < 1");
   std::vector<CycleStats> history;
   std::optional<FirstCycle> probe;
-  return damping_search(a, cfg, rec, history, probe);
+  StartVectors sv(a->dim(), cfg.seed, {rng::kPolyStart, rng::kArnoldiStart});
+  return damping_search(a, cfg, rec, history, probe, sv);
 }
 
 void SolveConfig::validate() const {
@@ -432,18 +540,14 @@ bool check_ideal_order(const std::vector<cplx>& mu, int nev) {
   return true;
 }
 
-double operator_norm_estimate(const LinearOperator& a, unsigned long long seed, CostRecord& rec) {
-  if (const std::vector<double>* d = a.diagonal()) {
-    double mx = 0.0;
-    for (double v : *d) mx = std::max(mx, std::abs(v));
-    return mx;
-  }
-  // Five counted power-iteration steps from a seeded N(0,1) vector
-  // (SPEC.md "one cycle of power iteration (5 mvps)").
+namespace {
+
+// Five counted power-iteration steps from the seeded N(0,1) vector x
+// (SPEC.md "one cycle of power iteration (5 mvps)").
+double power_norm_estimate(const LinearOperator& a, DBuffer<double> x, CostRecord& rec) {
   Context& ctx = current_context();
   const cudaStream_t s = ctx.stream();
   const int n = a.dim();
-  DBuffer<double> x = upload(rng::normal_vector(n, seed, rng::kNormEstimate));
   DBuffer<double> y(static_cast<size_t>(n));
   double nx = ctx.nrm2_sync(x.get(), n);
   ++rec.dots;
@@ -468,6 +572,37 @@ double operator_norm_estimate(const LinearOperator& a, unsigned long long seed, 
   return est;
 }
 
+double diagonal_norm(const std::vector<double>& d) {
+  double mx = 0.0;
+  for (double v : d) mx = std::max(mx, std::abs(v));
+  return mx;
+}
+
+double norm_estimate(const LinearOperator& a, CostRecord& rec, StartVectors& sv) {
+  if (const std::vector<double>* d = a.diagonal()) return diagonal_norm(*d);
+  return power_norm_estimate(a, sv.take(rng::kNormEstimate), rec);
+}
+
+// Streams a solve draws, in the order it draws them: the polynomial start
+// vector(s) first, then the norm-estimate vector (the estimate only sets
+// rtol, which the first convergence test needs, so it runs after the
+// polynomial build while the host draws the remaining vectors), then the
+// Arnoldi start vector.
+std::vector<uint64_t> solve_streams(const LinearOperator& a, std::vector<uint64_t> poly) {
+  std::vector<uint64_t> s = std::move(poly);
+  if (!a.diagonal()) s.push_back(rng::kNormEstimate);
+  s.push_back(rng::kArnoldiStart);
+  return s;
+}
+
+}  // namespace
+
+double operator_norm_estimate(const LinearOperator& a, unsigned long long seed, CostRecord& rec) {
+  if (const std::vector<double>* d = a.diagonal()) return diagonal_norm(*d);
+  DBuffer<double> x = upload(rng::normal_vector(a.dim(), seed, rng::kNormEstimate));
+  return power_norm_estimate(a, std::move(x), rec);
+}
+
 EigResult solve(const OperatorPtr& a, const SolveConfig& cfg) {
   if (!a) throw std::invalid_argument("solve: null operator");
   cfg.validate();
@@ -477,18 +612,18 @@ EigResult solve(const OperatorPtr& a, const SolveConfig& cfg) {
   CostRecord rec;
   rec.nnzr = a->nnzr();
   auto t0 = Clock::now();
-  res.norm_estimate = operator_norm_estimate(*a, cfg.seed, rec);
-  res.rtol = cfg.rtol_absolute ? *cfg.rtol_absolute : cfg.rtol_multiplier * res.norm_estimate;
-
+  StartVectors sv(a->dim(), cfg.seed,
+                  solve_streams(*a, cfg.degree > 0 ? std::vector<uint64_t>{rng::kPolyStart}
+                                                   : std::vector<uint64_t>{}));
   OperatorPtr op = a;
   RitzOrdering ordering = RitzOrdering::smallest_magnitude;
   std::optional<FirstCycle> probe;
   if (cfg.degree > 0) {
     PolyPrecond p;
     if (cfg.damping == DampingMode::auto_heuristic) {
-      p = damping_search(a, cfg, rec, res.history, probe);
+      p = damping_search(a, cfg, rec, res.history, probe, sv);
     } else {
-      DBuffer<double> b = upload(rng::normal_vector(a->dim(), cfg.seed, rng::kPolyStart));
+      DBuffer<double> b = sv.take(rng::kPolyStart);
       if (cfg.damping == DampingMode::forced) {
         // damped start A^power b + alpha b (section 6)
         DBuffer<double> bd(static_cast<size_t>(a->dim()));
@@ -507,9 +642,11 @@ EigResult solve(const OperatorPtr& a, const SolveConfig& cfg) {
     res.poly = p;
     ordering = RitzOrdering::target_one;
   }
+  res.norm_estimate = norm_estimate(*a, rec, sv);
+  res.rtol = cfg.rtol_absolute ? *cfg.rtol_absolute : cfg.rtol_multiplier * res.norm_estimate;
   current_context().sync();
   res.timing.setup = seconds_since(t0);
-  run_cycles(*a, *op, cfg, ordering, res, rec, probe ? &*probe : nullptr);
+  run_cycles(*a, *op, cfg, ordering, res, rec, sv, probe ? &*probe : nullptr);
   current_context().sync();
   res.timing.total = seconds_since(t_all);
   rec.wall_seconds = res.timing.total;
@@ -530,14 +667,12 @@ EigResult solve_double(const OperatorPtr& a, const SolveConfig& cfg) {
   CostRecord rec;
   rec.nnzr = a->nnzr();
   auto t0 = Clock::now();
-  res.norm_estimate = operator_norm_estimate(*a, cfg.seed, rec);
-  res.rtol = cfg.rtol_absolute ? *cfg.rtol_absolute : cfg.rtol_multiplier * res.norm_estimate;
-  const int n = a->dim();
-  DBuffer<double> b1 = upload(rng::normal_vector(n, cfg.seed, rng::kPolyStart));
+  StartVectors sv(a->dim(), cfg.seed, solve_streams(*a, {rng::kPolyStart, rng::kPoly2Start}));
+  DBuffer<double> b1 = sv.take(rng::kPolyStart);
   PolyPrecond p1 = build_gmres_poly(*a, b1.get(), cfg.double_d1, rec);
   p1.provenance = PolyProvenance::composite_stage;
   OperatorPtr tau = make_poly_complement_operator(a, p1);
-  DBuffer<double> b2 = upload(rng::normal_vector(n, cfg.seed, rng::kPoly2Start));
+  DBuffer<double> b2 = sv.take(rng::kPoly2Start);
   PolyPrecond p2 = build_gmres_poly(*tau, b2.get(), cfg.double_d2, rec);
   if (cfg.stability == StabilityMode::pof_auto && p2.roots.size() >= 2) {
     p2 = add_stability_roots(p2);
@@ -546,9 +681,11 @@ EigResult solve_double(const OperatorPtr& a, const SolveConfig& cfg) {
   OperatorPtr op = make_poly_operator(tau, p2);
   res.inner_poly = p1;
   res.poly = p2;
+  res.norm_estimate = norm_estimate(*a, rec, sv);
+  res.rtol = cfg.rtol_absolute ? *cfg.rtol_absolute : cfg.rtol_multiplier * res.norm_estimate;
   current_context().sync();
   res.timing.setup = seconds_since(t0);
-  run_cycles(*a, *op, cfg, RitzOrdering::target_one, res, rec);
+  run_cycles(*a, *op, cfg, RitzOrdering::target_one, res, rec, sv);
   current_context().sync();
   res.timing.total = seconds_since(t_all);
   rec.wall_seconds = res.timing.total;
