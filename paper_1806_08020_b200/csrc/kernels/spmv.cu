@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "pdl.cuh"
 #include "spmv_epilogue.cuh"
 #include "ppa/kernels.hpp"
 
@@ -122,9 +123,13 @@ __global__ void __launch_bounds__(SELL_WARPS * 32) k_spmv_sell32(
     const double* __restrict__ sval, const int* __restrict__ perm, int n, int nslices,
     const double* __restrict__ x, double* y, double c0, double c1, const double* o,
     const double* base) {
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int s = blockIdx.x * SELL_WARPS + (threadIdx.x >> 5);
-  if (s >= nslices) return;
+  if (s >= nslices) {
+    pdl_wait();
+    return;
+  }
   const int idx = s * 32 + lane;
   const int r = (PERM && idx < n) ? __ldg(perm + idx) : idx;
   const long long b0 = slice_ptr[s];
@@ -132,6 +137,7 @@ __global__ void __launch_bounds__(SELL_WARPS * 32) k_spmv_sell32(
   const int* cp = scol + b0 + lane;
   const double* vp = sval + b0 + lane;
   double sum = 0.0;
+  pdl_wait();  // x is the previous factor's output
   for (int k0 = 0; k0 < width; k0 += SELL_UNROLL) {
     int c[SELL_UNROLL];
     double v[SELL_UNROLL];
@@ -155,13 +161,13 @@ void launch(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep, c
   if (a.sell_val) {
     const int grid = (a.nslices + SELL_WARPS - 1) / SELL_WARPS;
     if (a.sell_perm) {
-      k_spmv_sell32<MODE, COMPL, true><<<grid, SELL_WARPS * 32, 0, st>>>(
-          a.slice_ptr, a.sell_col, a.sell_val, a.sell_perm, a.n, a.nslices, x, y, ep.c0, ep.c1,
-          ep.o, ep.base);
+      launch_pdl(k_spmv_sell32<MODE, COMPL, true>, dim3(grid), dim3(SELL_WARPS * 32), 0, st,
+                 a.slice_ptr, a.sell_col, a.sell_val, a.sell_perm, a.n, a.nslices, x, y, ep.c0,
+                 ep.c1, ep.o, ep.base);
     } else {
-      k_spmv_sell32<MODE, COMPL, false><<<grid, SELL_WARPS * 32, 0, st>>>(
-          a.slice_ptr, a.sell_col, a.sell_val, nullptr, a.n, a.nslices, x, y, ep.c0, ep.c1, ep.o,
-          ep.base);
+      launch_pdl(k_spmv_sell32<MODE, COMPL, false>, dim3(grid), dim3(SELL_WARPS * 32), 0, st,
+                 a.slice_ptr, a.sell_col, a.sell_val, static_cast<const int*>(nullptr), a.n,
+                 a.nslices, x, y, ep.c0, ep.c1, ep.o, ep.base);
     }
     return;
   }

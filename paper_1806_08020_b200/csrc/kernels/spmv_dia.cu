@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "pdl.cuh"
 #include "spmv_epilogue.cuh"
 #include "ppa/kernels.hpp"
 
@@ -121,11 +122,11 @@ __global__ void __launch_bounds__(DW * 32, 4) k_spmv_dia(
   int s = blockIdx.x * DW + (threadIdx.x >> 5);
   unsigned w[NW];
   double xv[4 * NW];
-  if (s < nslices) {
-    load_codes<NW>(w, codes + (static_cast<long long>(s) * 32 + lane) * NW);
-    dia_gather<4 * NW>(xv, s * 32 + lane, n, off, x);
-  }
+  pdl_trigger();
+  if (s < nslices) load_codes<NW>(w, codes + (static_cast<long long>(s) * 32 + lane) * NW);
   load_table(tab, dict, ndict);
+  pdl_wait();  // x is the previous factor's output
+  if (s < nslices) dia_gather<4 * NW>(xv, s * 32 + lane, n, off, x);
   for (; s < nslices; s += W) {
     const int sn = s + W;
     unsigned wn[NW];
@@ -171,9 +172,9 @@ void launch_dia_nw(const CsrDevice& a, const double* x, double* y, const EpiArgs
   auto kernel = k_spmv_dia<MODE, COMPL, NW>;
   static const int per_sm = resident_ctas(kernel);
   const int grid = std::min((a.nslices + DW - 1) / DW, device_sms() * per_sm);
-  kernel<<<grid, DW * 32, 0, st>>>(reinterpret_cast<const unsigned*>(a.dia_code), a.dia_dict,
-                                   a.dia_ndict, off, a.n, a.nslices, x, y, ep.c0, ep.c1, ep.o,
-                                   ep.base);
+  launch_pdl(kernel, dim3(grid), dim3(DW * 32), 0, st,
+             reinterpret_cast<const unsigned*>(a.dia_code), a.dia_dict, a.dia_ndict, off, a.n,
+             a.nslices, x, y, ep.c0, ep.c1, ep.o, ep.base);
 }
 
 // ---- regular-row form -----------------------------------------------------
@@ -205,15 +206,20 @@ __global__ void __launch_bounds__(RB) k_spmv_diar(
     const double* __restrict__ dict, const DiaRParams P, int n, const double* __restrict__ x,
     double* y, double c0, double c1, const double* o, const double* base) {
   constexpr int NW = ND <= 4 ? 1 : ND <= 8 ? 2 : 4;  // code words per row (stride / 4)
+  pdl_trigger();
   double sum = 0.0;
   int r;
   const int bx = blockIdx.x;
   if (bx < gx) {
     const int k = bx * RB + threadIdx.x;
-    if (k >= n_irr) return;
+    if (k >= n_irr) {
+      pdl_wait();
+      return;
+    }
     r = __ldg(irr_rows + k);
     unsigned ec[NW];
     load_codes<NW>(ec, reinterpret_cast<const unsigned*>(irr_codes) + static_cast<long long>(k) * NW);
+    pdl_wait();  // x is the previous factor's output
     double xv[ND];
 #pragma unroll
     for (int j = 0; j < ND; ++j) {
@@ -227,8 +233,12 @@ __global__ void __launch_bounds__(RB) k_spmv_diar(
     }
   } else {
     r = (bx - gx) * RB + threadIdx.x;
-    if (r >= n) return;
+    if (r >= n) {
+      pdl_wait();
+      return;
+    }
     const unsigned m = __ldg(mask + (r >> 5));
+    pdl_wait();  // x is the previous factor's output
     double xv[ND];
 #pragma unroll
     for (int j = 0; j < ND; ++j) xv[j] = __ldg(x + min(max(r + P.off[j], 0), n - 1));
@@ -249,9 +259,9 @@ void launch_diar(const CsrDevice& a, const double* x, double* y, const EpiArgs& 
   }
   const int gx = static_cast<int>((a.dia_nirr + RB - 1) / RB);
   const int grid = gx + (a.n + RB - 1) / RB;
-  k_spmv_diar<MODE, COMPL, ND><<<grid, RB, 0, st>>>(
-      a.dia_mask, a.dia_irr_rows, a.dia_irr_codes, static_cast<int>(a.dia_nirr), gx, a.dia_dict,
-      P, a.n, x, y, ep.c0, ep.c1, ep.o, ep.base);
+  launch_pdl(k_spmv_diar<MODE, COMPL, ND>, dim3(grid), dim3(RB), 0, st, a.dia_mask,
+             a.dia_irr_rows, a.dia_irr_codes, static_cast<int>(a.dia_nirr), gx, a.dia_dict, P,
+             a.n, x, y, ep.c0, ep.c1, ep.o, ep.base);
 }
 
 // The regular-row kernel is instantiated per diagonal count so the row sum

@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "pdl.cuh"
 #include "spmv_epilogue.cuh"
 #include "ppa/kernels.hpp"
 
@@ -84,10 +85,14 @@ __global__ void __launch_bounds__(PW * 32) k_spmv_sellp(
     int nslices, const double* __restrict__ x, double* y, double c0, double c1,
     const double* o, const double* base) {
   __shared__ double tab[DICT ? kPackMaxDict : 1];
+  pdl_trigger();
   load_table<DICT>(tab, dict, ndict);
   const int lane = threadIdx.x & 31;
   const int s = blockIdx.x * PW + (threadIdx.x >> 5);
-  if (s >= nslices) return;
+  if (s >= nslices) {
+    pdl_wait();
+    return;
+  }
   const int idx = s * 32 + lane;
   const int r = (PERM && idx < n) ? __ldg(perm + idx) : idx;
   const long long b0 = pk_ptr[s];
@@ -95,6 +100,7 @@ __global__ void __launch_bounds__(PW * 32) k_spmv_sellp(
   const long long lb = b0 + KC * lane;
   const double* xr = x + r;
   double sum = 0.0;
+  pdl_wait();  // x is the previous factor's output
   for (int j0 = 0; j0 < nch; j0 += PU) {
     PackedChunk c[PU];
 #pragma unroll
@@ -121,9 +127,9 @@ template <int MODE, bool COMPL, bool PERM, bool DICT>
 void launch_sellp(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep,
                   cudaStream_t st) {
   const int grid = (a.nslices + PW - 1) / PW;
-  k_spmv_sellp<MODE, COMPL, PERM, DICT><<<grid, PW * 32, 0, st>>>(
-      a.pk_ptr, a.pk_col, a.pk_code, a.pk_val, a.pk_dict, a.pk_ndict, a.sell_perm, a.n,
-      a.nslices, x, y, ep.c0, ep.c1, ep.o, ep.base);
+  launch_pdl(k_spmv_sellp<MODE, COMPL, PERM, DICT>, dim3(grid), dim3(PW * 32), 0, st, a.pk_ptr,
+             a.pk_col, a.pk_code, a.pk_val, a.pk_dict, a.pk_ndict, a.sell_perm, a.n, a.nslices,
+             x, y, ep.c0, ep.c1, ep.o, ep.base);
 }
 
 template <int MODE, bool COMPL>
