@@ -202,12 +202,14 @@ namespace {
 // y = base - pi(A) x).  Counters charge the reference's per-factor
 // increments (src/gmres_poly.cpp:129-143).
 void apply_poly_csr(const std::vector<PolyFactor>& plan, const CsrOperator& a, const double* v,
-                    double* dst, const double* complement_base, CostRecord& rec) {
+                    double* dst, const double* complement_base, CostRecord& rec,
+                    const kern::EpiArgs* outer_fold = nullptr) {
   Context& ctx = current_context();
   const cudaStream_t st = ctx.stream();
   const long long n = a.dim();
   const int K = static_cast<int>(plan.size());
   if (K == 0) {
+    if (outer_fold) throw std::logic_error("apply_poly_csr: outer fold needs an inner factor");
     if (complement_base) {
       kern::sub(complement_base, v, dst, n, st);
     } else {
@@ -219,7 +221,7 @@ void apply_poly_csr(const std::vector<PolyFactor>& plan, const CsrOperator& a, c
   // (L2 reuse), but its cross-CTA waits make it slower than two plain
   // launches on B200.
   const char* mpk_env = std::getenv("PPA_ENABLE_MPK");
-  const bool mp = mpk_env && mpk_env[0] == '1' && kern::mp2_supported(a.device());
+  const bool mp = mpk_env && mpk_env[0] == '1' && kern::mp2_supported(a.device()) && !outer_fold;
   struct Pass {
     int first;
     int count;  // factors in the pass (1 or 2 real roots, or 1 pair)
@@ -262,21 +264,27 @@ void apply_poly_csr(const std::vector<PolyFactor>& plan, const CsrOperator& a, c
       }
       kern::spmv_mp2(a.device(), m, cur, t1buf.get(), out, base, ctx.mp_work(), ctx.sm_count(),
                      st);
-    } else if (!f.pair) {
-      kern::EpiArgs ep;
-      ep.base = base;
-      ep.mode = kern::Epi::real;
-      ep.c0 = f.c0;
-      kern::spmv(a.device(), cur, out, ep, st);
     } else {
-      kern::spmv(a.device(), cur, t1buf.get(), kern::EpiArgs{}, st);
       kern::EpiArgs ep;
       ep.base = base;
-      ep.mode = kern::Epi::pair;
-      ep.c0 = f.c0;
-      ep.c1 = f.c1;
-      ep.o = cur;
-      kern::spmv(a.device(), t1buf.get(), out, ep, st);
+      if (base && outer_fold) {
+        ep.outer = outer_fold->outer;
+        ep.oc0 = outer_fold->oc0;
+        ep.oc1 = outer_fold->oc1;
+        ep.oo = outer_fold->oo;
+      }
+      if (!f.pair) {
+        ep.mode = kern::Epi::real;
+        ep.c0 = f.c0;
+        kern::spmv(a.device(), cur, out, ep, st);
+      } else {
+        kern::spmv(a.device(), cur, t1buf.get(), kern::EpiArgs{}, st);
+        ep.mode = kern::Epi::pair;
+        ep.c0 = f.c0;
+        ep.c1 = f.c1;
+        ep.o = cur;
+        kern::spmv(a.device(), t1buf.get(), out, ep, st);
+      }
     }
     const int mv = f.pair ? 2 : ps.count;
     rec.mvps += mv;
@@ -307,6 +315,48 @@ void apply_poly_generic(const std::vector<PolyFactor>& plan, const LinearOperato
       kern::axpy(f.c0, t2.get(), out, n, st);
       rec.vops += 2;
     }
+  }
+}
+
+// phi(tau(A)) v with tau = I - pi_1 over a CSR matrix (solve_double's
+// operator): the same operation sequence as apply_poly_generic over the tau
+// operator, but each outer factor's axpy is folded into the epilogue of the
+// last inner launch (K4), so an outer real factor costs the
+// inner chain only and no copy of v is made.  Outer factors ping-pong
+// between `out` and one scratch vector, assigned backwards so the last one
+// lands in `out`; counters are those of the generic path.
+void apply_nested_csr(const std::vector<PolyFactor>& outer, const std::vector<PolyFactor>& inner,
+                      const CsrOperator& a, const double* v, double* out, CostRecord& rec) {
+  const long long n = a.dim();
+  const int Q = static_cast<int>(outer.size());
+  if (Q == 0) {
+    kern::copy(v, out, n, current_context().stream());
+    return;
+  }
+  bool any_pair = false;
+  for (const PolyFactor& f : outer) any_pair |= f.pair;
+  Scratch other(static_cast<size_t>(n));
+  Scratch t1(any_pair ? static_cast<size_t>(n) : 1);
+  double* bufs[2] = {out, other.get()};
+  const double* cur = v;
+  for (int q = 0; q < Q; ++q) {
+    const PolyFactor& f = outer[q];
+    double* next = bufs[(Q - 1 - q) & 1];
+    kern::EpiArgs fold;
+    fold.oo = cur;
+    fold.oc0 = f.c0;
+    if (!f.pair) {
+      fold.outer = 1;
+      apply_poly_csr(inner, a, cur, next, cur, rec, &fold);
+      rec.vops += 2;  // tau's complement + the outer axpy
+    } else {
+      apply_poly_csr(inner, a, cur, t1.get(), cur, rec);
+      fold.outer = 2;
+      fold.oc1 = f.c1;
+      apply_poly_csr(inner, a, t1.get(), next, t1.get(), rec, &fold);
+      rec.vops += 4;  // two complements + two outer axpys
+    }
+    cur = next;
   }
 }
 
@@ -413,6 +463,14 @@ class PolyOperator final : public LinearOperator {
       return;
     }
     if (!complement_) {
+      const auto* tau = dynamic_cast<const PolyOperator*>(a_.get());
+      const auto* base_csr = tau ? dynamic_cast<const CsrOperator*>(tau->a_.get()) : nullptr;
+      const char* mpk_env = std::getenv("PPA_ENABLE_MPK");
+      if (tau && tau->complement_ && base_csr && !tau->plan_.empty() &&
+          !(mpk_env && mpk_env[0] == '1')) {
+        apply_nested_csr(plan_, tau->plan_, *base_csr, x, y, rec);
+        return;
+      }
       apply_poly_generic(plan_, *a_, x, y, rec);
       return;
     }

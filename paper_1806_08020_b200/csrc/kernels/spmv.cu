@@ -41,8 +41,7 @@ template <int MODE, bool COMPL>
 __global__ void __launch_bounds__(T) k_spmv_rowblock(
     const int* __restrict__ row_ptr, const int* __restrict__ col_idx,
     const double* __restrict__ vals, const int* __restrict__ blk_row,
-    const double* __restrict__ x, double* y, double c0, double c1, const double* o,
-    const double* base) {
+    const double* __restrict__ x, double* y, const EpiDev e) {
   __shared__ __align__(16) double prod[MAXNNZ + 2];
   __shared__ int rp[MAXR + 1];
   __shared__ double s_warp[T / 32];
@@ -85,7 +84,7 @@ __global__ void __launch_bounds__(T) k_spmv_rowblock(
       const int b = rp[t + 1] - q0;
       double s = 0.0;
       for (int p = a; p < b; ++p) s = __dadd_rn(s, prod[p]);
-      y[r0 + t] = epilogue<MODE, COMPL>(r0 + t, s, x, c0, c1, o, base);
+      y[r0 + t] = epilogue<MODE, COMPL>(r0 + t, s, x, e);
     }
   } else {
     // One long row (nr == 1): block-strided partial sums + fixed-order tree.
@@ -100,7 +99,7 @@ __global__ void __launch_bounds__(T) k_spmv_rowblock(
       double tot = 0.0;
 #pragma unroll
       for (int w = 0; w < T / 32; ++w) tot += s_warp[w];
-      y[r0] = epilogue<MODE, COMPL>(r0, tot, x, c0, c1, o, base);
+      y[r0] = epilogue<MODE, COMPL>(r0, tot, x, e);
     }
   }
 }
@@ -121,8 +120,7 @@ template <int MODE, bool COMPL, bool PERM>
 __global__ void __launch_bounds__(SELL_WARPS * 32) k_spmv_sell32(
     const long long* __restrict__ slice_ptr, const int* __restrict__ scol,
     const double* __restrict__ sval, const int* __restrict__ perm, int n, int nslices,
-    const double* __restrict__ x, double* y, double c0, double c1, const double* o,
-    const double* base) {
+    const double* __restrict__ x, double* y, const EpiDev e) {
   pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int s = blockIdx.x * SELL_WARPS + (threadIdx.x >> 5);
@@ -153,7 +151,7 @@ __global__ void __launch_bounds__(SELL_WARPS * 32) k_spmv_sell32(
       if (k0 + u < width && c[u] >= 0) sum = __dadd_rn(sum, __dmul_rn(v[u], __ldg(x + c[u])));
     }
   }
-  if (idx < n) y[r] = epilogue<MODE, COMPL>(r, sum, x, c0, c1, o, base);
+  if (idx < n) y[r] = epilogue<MODE, COMPL>(r, sum, x, e);
 }
 
 template <int MODE, bool COMPL>
@@ -162,18 +160,16 @@ void launch(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep, c
     const int grid = (a.nslices + SELL_WARPS - 1) / SELL_WARPS;
     if (a.sell_perm) {
       launch_pdl(k_spmv_sell32<MODE, COMPL, true>, dim3(grid), dim3(SELL_WARPS * 32), 0, st,
-                 a.slice_ptr, a.sell_col, a.sell_val, a.sell_perm, a.n, a.nslices, x, y, ep.c0,
-                 ep.c1, ep.o, ep.base);
+                 a.slice_ptr, a.sell_col, a.sell_val, a.sell_perm, a.n, a.nslices, x, y, epi_dev(ep));
     } else {
       launch_pdl(k_spmv_sell32<MODE, COMPL, false>, dim3(grid), dim3(SELL_WARPS * 32), 0, st,
                  a.slice_ptr, a.sell_col, a.sell_val, static_cast<const int*>(nullptr), a.n,
-                 a.nslices, x, y, ep.c0, ep.c1, ep.o, ep.base);
+                 a.nslices, x, y, epi_dev(ep));
     }
     return;
   }
   k_spmv_rowblock<MODE, COMPL><<<a.nblocks, T, 0, st>>>(a.row_ptr, a.col_idx, a.values,
-                                                       a.blk_row, x, y, ep.c0, ep.c1, ep.o,
-                                                       ep.base);
+                                                       a.blk_row, x, y, epi_dev(ep));
 }
 
 }  // namespace

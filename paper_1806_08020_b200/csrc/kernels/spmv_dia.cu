@@ -115,7 +115,7 @@ template <int MODE, bool COMPL, int NW>
 __global__ void __launch_bounds__(DW * 32, 4) k_spmv_dia(
     const unsigned* __restrict__ codes, const double* __restrict__ dict, int ndict,
     const DiaOffsets off, int n, int nslices, const double* __restrict__ x, double* y,
-    double c0, double c1, const double* o, const double* base) {
+    const EpiDev e) {
   __shared__ double tab[kDiaMaxDict + 1];
   const int lane = threadIdx.x & 31;
   const int W = gridDim.x * DW;
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(DW * 32, 4) k_spmv_dia(
     }
     const int r = s * 32 + lane;
     const double sum = dia_sum<NW>(w, xv, tab);
-    if (r < n) y[r] = epilogue<MODE, COMPL>(r, sum, x, c0, c1, o, base);
+    if (r < n) y[r] = epilogue<MODE, COMPL>(r, sum, x, e);
 #pragma unroll
     for (int k = 0; k < NW; ++k) w[k] = wn[k];
 #pragma unroll
@@ -174,7 +174,7 @@ void launch_dia_nw(const CsrDevice& a, const double* x, double* y, const EpiArgs
   const int grid = std::min((a.nslices + DW - 1) / DW, device_sms() * per_sm);
   launch_pdl(kernel, dim3(grid), dim3(DW * 32), 0, st,
              reinterpret_cast<const unsigned*>(a.dia_code), a.dia_dict, a.dia_ndict, off, a.n,
-             a.nslices, x, y, ep.c0, ep.c1, ep.o, ep.base);
+             a.nslices, x, y, epi_dev(ep));
 }
 
 // ---- regular-row form -----------------------------------------------------
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(RB) k_spmv_diar(
     const unsigned* __restrict__ mask, const int* __restrict__ irr_rows,
     const unsigned char* __restrict__ irr_codes, int n_irr, int gx,
     const double* __restrict__ dict, const DiaRParams P, int n, const double* __restrict__ x,
-    double* y, double c0, double c1, const double* o, const double* base) {
+    double* y, const EpiDev e) {
   constexpr int NW = ND <= 4 ? 1 : ND <= 8 ? 2 : 4;  // code words per row (stride / 4)
   pdl_trigger();
   double sum = 0.0;
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(RB) k_spmv_diar(
     for (int j = 0; j < ND; ++j) sum = __dadd_rn(sum, __dmul_rn(P.val[j], xv[j]));
     if (!((m >> (r & 31)) & 1u)) return;
   }
-  y[r] = epilogue<MODE, COMPL>(r, sum, x, c0, c1, o, base);
+  y[r] = epilogue<MODE, COMPL>(r, sum, x, e);
 }
 
 template <int MODE, bool COMPL, int ND>
@@ -261,7 +261,7 @@ void launch_diar(const CsrDevice& a, const double* x, double* y, const EpiArgs& 
   const int grid = gx + (a.n + RB - 1) / RB;
   launch_pdl(k_spmv_diar<MODE, COMPL, ND>, dim3(grid), dim3(RB), 0, st, a.dia_mask,
              a.dia_irr_rows, a.dia_irr_codes, static_cast<int>(a.dia_nirr), gx, a.dia_dict, P,
-             a.n, x, y, ep.c0, ep.c1, ep.o, ep.base);
+             a.n, x, y, epi_dev(ep));
 }
 
 // The regular-row kernel is instantiated per diagonal count so the row sum

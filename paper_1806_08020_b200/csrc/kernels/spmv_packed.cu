@@ -82,8 +82,7 @@ __global__ void __launch_bounds__(PW * 32) k_spmv_sellp(
     const long long* __restrict__ pk_ptr, const short* __restrict__ pcol,
     const unsigned char* __restrict__ pcode, const double* __restrict__ pval,
     const double* __restrict__ dict, int ndict, const int* __restrict__ perm, int n,
-    int nslices, const double* __restrict__ x, double* y, double c0, double c1,
-    const double* o, const double* base) {
+    int nslices, const double* __restrict__ x, double* y, const EpiDev e) {
   __shared__ double tab[DICT ? kPackMaxDict : 1];
   pdl_trigger();
   load_table<DICT>(tab, dict, ndict);
@@ -120,7 +119,7 @@ __global__ void __launch_bounds__(PW * 32) k_spmv_sellp(
       }
     }
   }
-  if (idx < n) y[r] = epilogue<MODE, COMPL>(r, sum, x, c0, c1, o, base);
+  if (idx < n) y[r] = epilogue<MODE, COMPL>(r, sum, x, e);
 }
 
 template <int MODE, bool COMPL, bool PERM, bool DICT>
@@ -129,7 +128,7 @@ void launch_sellp(const CsrDevice& a, const double* x, double* y, const EpiArgs&
   const int grid = (a.nslices + PW - 1) / PW;
   launch_pdl(k_spmv_sellp<MODE, COMPL, PERM, DICT>, dim3(grid), dim3(PW * 32), 0, st, a.pk_ptr,
              a.pk_col, a.pk_code, a.pk_val, a.pk_dict, a.pk_ndict, a.sell_perm, a.n, a.nslices,
-             x, y, ep.c0, ep.c1, ep.o, ep.base);
+             x, y, epi_dev(ep));
 }
 
 template <int MODE, bool COMPL>

@@ -155,6 +155,11 @@ struct EpiArgs {
   double c1 = 0.0;
   const double* o = nullptr;     // pair: running product (may alias y)
   const double* base = nullptr;  // complement base (nullptr: no complement)
+  // outer factor of a nested polynomial folded after the complement
+  // (spmv_epilogue.cuh); only with base != nullptr.  oo may alias y.
+  int outer = 0;  // 0 none, 1 real, 2 pair
+  double oc0 = 0.0, oc1 = 0.0;
+  const double* oo = nullptr;
 };
 
 void spmv(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep, cudaStream_t st);

@@ -301,12 +301,16 @@ def test_poly_operator_and_complement(cuda, complement):
     assert (rec.mvps, rec.vops) == (int(cost[0]), int(cost[2]))
 
 
-def test_nested_double_polynomial(cuda):
-    # pi2(tau(A)), tau = I - pi1(A): the generic (non-CSR) apply path over a
-    # fused complement operator (src/gmres_poly.cpp:302-311).
+@pytest.mark.parametrize("inner_kind", ["real", "mixed"])
+def test_nested_double_polynomial(cuda, inner_kind):
+    # pi2(tau(A)), tau = I - pi1(A) over CSR: each outer factor's axpy is
+    # folded into the last inner launch (src/gmres_poly.cpp:129-143 over the
+    # tau operator of src/gmres_poly.cpp:302-311); bit-identical to the
+    # oracle's generic sequence, with its counters.
     P = ppa.CsrMatrix.convection_diffusion_const(30, 0.5)
     Q = O.Csr.convection_diffusion_const(30, 0.5)
-    r1 = _roots_real(5, 100.0, 7000.0)
+    r1 = _roots_real(5, 100.0, 7000.0) if inner_kind == "real" else O.leja_order(
+        [150.0, 3000.0 + 400.0j, 3000.0 - 400.0j, 6500.0])
     r2 = O.leja_order([0.9, 0.5 + 0.1j, 0.5 - 0.1j, 0.2])
     tau = ppa.make_poly_complement_operator(ppa.make_csr_operator(P), r1)
     op = ppa.make_poly_operator(tau, r2)
@@ -317,7 +321,7 @@ def test_nested_double_polynomial(cuda):
     rec = op.apply(dev(cuda, x), y)
     cost = np.zeros(3)
     ref = opo.apply(x, cost)
-    assert rel(host(y), ref) <= 1e-12
+    assert np.array_equal(host(y), ref)
     assert (rec.mvps, rec.vops) == (int(cost[0]), int(cost[2]))
 
 
