@@ -363,6 +363,13 @@ def run_b200(args):
         solve_info = solve_on(A_auto)
         solve_info["layout"] = lay["layout"]
         solve_info["sell32"] = solve_on(A)
+        # opt-in delayed CGS2 (two sweeps over V per step instead of three;
+        # DESIGN.md §3.2): same eigenpairs, roundoff may move convergence by a cycle
+        os.environ["PPA_DCGS2"] = "1"
+        try:
+            solve_info["dcgs2"] = solve_on(A_auto)
+        finally:
+            del os.environ["PPA_DCGS2"]
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

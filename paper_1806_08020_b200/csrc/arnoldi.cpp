@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <numeric>
 #include <stdexcept>
 
@@ -136,10 +137,11 @@ ArnoldiState arnoldi_init(const double* v0, int n, int m, CostRecord& rec) {
   return st;
 }
 
-void arnoldi_extend(ArnoldiState& st, const LinearOperator& op, int to_dim, CostRecord& rec) {
-  if (to_dim > st.max_dim) throw std::invalid_argument("arnoldi_extend: to_dim > max_dim");
-  if (to_dim <= st.cur_dim) throw std::invalid_argument("arnoldi_extend: to_dim <= cur_dim");
-  if (op.dim() != st.n) throw std::invalid_argument("arnoldi_extend: dimension mismatch");
+namespace {
+
+// Classic CGS2: three sweeps per step (kernels/cgs.cu), one host sync to
+// read the Hessenberg column and the breakdown flag.
+void extend_cgs2(ArnoldiState& st, const LinearOperator& op, int to_dim, CostRecord& rec) {
   Context& ctx = current_context();
   const cudaStream_t s = ctx.stream();
   Scratch w(static_cast<size_t>(st.n));
@@ -167,6 +169,156 @@ void arnoldi_extend(ArnoldiState& st, const LinearOperator& op, int to_dim, Cost
       return;
     }
     ++rec.vops;  // the scaling (src/arnoldi.cpp:149-150)
+  }
+}
+
+// Column j-1 of H gets its reorthogonalisation coefficients s and its
+// subdiagonal rho; returns false (and records the breakdown) when rho fails
+// the test of src/arnoldi.cpp:143-148.
+bool finish_column(ArnoldiState& st, int col, const double* s, double rho) {
+  double cn = 0.0;
+  for (int k = 0; k <= col; ++k) {
+    st.h(k, col) += s[k];
+    cn += st.h(k, col) * st.h(k, col);
+  }
+  cn += rho * rho;
+  const double colnorm = std::sqrt(cn);
+  if (!std::isfinite(rho) || !std::isfinite(colnorm)) {
+    throw std::runtime_error("arnoldi_extend: non-finite basis vector");
+  }
+  if (rho <= 1e-14 * colnorm) {
+    st.h(col + 1, col) = 0.0;
+    st.breakdown = true;
+    st.cur_dim = col + 1;
+    return false;
+  }
+  st.h(col + 1, col) = rho;
+  st.cur_dim = col + 1;
+  return true;
+}
+
+// Delayed CGS2 (DCGS2): the second (reorthogonalisation) pass of v_j and
+// its normalisation are deferred to step j+1 and share its two sweeps over
+// V, so a step reads V twice instead of three times.  Step j applies the
+// operator to the pending first-pass vector u = V[:,j]: z = op(u), then
+//   sweep 1 (dcgs2_dot): t = Q^T z, beta = u.z, s = Q^T u, nu = u.u
+//   host: rho = sqrt(nu - |s|^2) completes column j-1 of H (+= s, rho);
+//         A q_j = (z - Q_{j+1} g)/rho with g = H(0:j,0:j-1) s (Arnoldi
+//         relation), so its first-pass coefficients are
+//         h = [(t - g[:j])/rho ; ((beta - s.t)/rho - g[j])/rho]
+//   sweep 2 (dcgs2_update): V[:,j] = (u - Q s)/rho (final q_j) and the next
+//         pending vector z/rho - Q_{j+1}(g/rho + h), written over z.
+// The first step of an extend is a plain first pass, the last pending vector
+// is flushed with one more CGS pass.  Counters are charged exactly as the
+// reference's MGS2 (src/arnoldi.cpp:130-150); a breakdown found one step
+// late un-charges the extra operator application.
+void extend_dcgs2(ArnoldiState& st, const LinearOperator& op, int to_dim, CostRecord& rec) {
+  Context& ctx = current_context();
+  const cudaStream_t str = ctx.stream();
+  const int M = st.max_dim;
+  Scratch dbuf(static_cast<size_t>(4 * M + 8));
+  double* dout = dbuf.get();               // 2c reductions (or c + norm)
+  double* dcoef = dbuf.get() + 2 * M + 4;  // 2j + 2 coefficients
+  double* host = ctx.pinned(static_cast<size_t>(4 * M + 8));
+  double* hout = host;
+  double* hcoef = host + 2 * M + 4;
+  double* V = st.V.get();
+  const int j0 = st.cur_dim;
+
+  // step j0: first pass only; the pending vector lands in V[:, j0+1]
+  op.apply(st.col(j0), st.col(j0 + 1), rec);
+  {
+    const int c = j0 + 1;
+    kern::cgs1_pass(V, st.ld, st.n, c, st.col(j0 + 1), dout, dout + c, ctx.ws(), ctx.sm_count(),
+                    str);
+    PPA_CUDA(cudaMemcpyAsync(hout, dout, c * sizeof(double), cudaMemcpyDeviceToHost, str));
+    ctx.sync();
+    for (int i = 0; i < c; ++i) st.h(i, j0) = hout[i];
+    rec.dots += 2LL * c + 1;
+    rec.vops += 4LL * c + 1;
+  }
+  std::vector<double> g, hcol;
+  for (int j = j0 + 1; j < to_dim; ++j) {
+    const CostRecord before = rec;
+    op.apply(st.col(j), st.col(j + 1), rec);  // z = op(u)
+    const int c = j + 1;
+    kern::dcgs2_dot(V, st.ld, st.n, c, st.col(j + 1), dout, ctx.ws(), ctx.sm_count(), str);
+    PPA_CUDA(cudaMemcpyAsync(hout, dout, 2 * c * sizeof(double), cudaMemcpyDeviceToHost, str));
+    ctx.sync();
+    const double* t = hout;
+    const double beta = hout[j];
+    const double* sv = hout + c;
+    const double nu = hout[c + j];
+    double ss = 0.0, st_dot = 0.0;
+    for (int k = 0; k < j; ++k) {
+      ss += sv[k] * sv[k];
+      st_dot += sv[k] * t[k];
+    }
+    const double d2 = nu - ss;
+    const double rho = d2 > 0.0 ? std::sqrt(d2) : 0.0;
+    if (!finish_column(st, j - 1, sv, rho)) {
+      rec = before;  // the application to the dependent vector does not count
+      return;
+    }
+    ++rec.vops;  // the scaling of v_j (src/arnoldi.cpp:149-150)
+    // g = H(0:j, 0:j-1) s (upper Hessenberg)
+    g.assign(static_cast<size_t>(j) + 1, 0.0);
+    for (int k = 0; k < j; ++k) {
+      for (int i = 0; i <= k + 1; ++i) g[i] += st.h(i, k) * sv[k];
+    }
+    hcol.assign(static_cast<size_t>(j) + 1, 0.0);
+    for (int k = 0; k < j; ++k) hcol[k] = (t[k] - g[k]) / rho;
+    hcol[j] = ((beta - st_dot) / rho - g[j]) / rho;
+    const double cj = g[j] / rho + hcol[j];
+    const double e = cj / rho;
+    for (int k = 0; k < j; ++k) {
+      hcoef[k] = sv[k];
+      hcoef[j + k] = (g[k] / rho + hcol[k]) - e * sv[k];
+    }
+    hcoef[2 * j] = e;
+    hcoef[2 * j + 1] = rho;
+    for (int i = 0; i <= j; ++i) st.h(i, j) = hcol[i];
+    PPA_CUDA(cudaMemcpyAsync(dcoef, hcoef, (2 * j + 2) * sizeof(double), cudaMemcpyHostToDevice,
+                             str));
+    kern::dcgs2_update(V, st.ld, st.n, c, st.col(j + 1), dcoef, ctx.ws(), ctx.sm_count(), str);
+    rec.dots += 2LL * c + 1;
+    rec.vops += 4LL * c + 1;
+  }
+  // flush the pending V[:, to_dim]: second pass, then normalise
+  const int c = to_dim;
+  kern::cgs1_pass(V, st.ld, st.n, c, st.col(to_dim), dout, dout + c, ctx.ws(), ctx.sm_count(),
+                  str);
+  PPA_CUDA(cudaMemcpyAsync(hout, dout, (c + 1) * sizeof(double), cudaMemcpyDeviceToHost, str));
+  ctx.sync();
+  if (!finish_column(st, to_dim - 1, hout, hout[c])) return;
+  kern::div_value(st.col(to_dim), hout[c], st.n, str);
+  ++rec.vops;
+}
+
+// DCGS2 is opt-in (PPA_DCGS2=1): it is as stable as CGS2 but its roundoff
+// differs enough that borderline convergence tests can flip by a cycle
+// (config 3 converges in 4 cycles instead of the oracle's 5), which breaks
+// the matvec-count parity the reference comparison asks for.  With it on,
+// small bases keep CGS2 (the extra host round trip per step only pays once a
+// sweep over V is long); PPA_FORCE_DCGS2=1 ignores the size (tests).
+bool use_dcgs2(const ArnoldiState& st, int steps) {
+  if (std::getenv("PPA_DISABLE_DCGS2")) return false;
+  const bool force = std::getenv("PPA_FORCE_DCGS2") != nullptr;
+  const char* on = std::getenv("PPA_DCGS2");
+  const bool enabled = force || (on && on[0] == '1');
+  return enabled && steps >= 2 && (force || st.n >= (1 << 17));
+}
+
+}  // namespace
+
+void arnoldi_extend(ArnoldiState& st, const LinearOperator& op, int to_dim, CostRecord& rec) {
+  if (to_dim > st.max_dim) throw std::invalid_argument("arnoldi_extend: to_dim > max_dim");
+  if (to_dim <= st.cur_dim) throw std::invalid_argument("arnoldi_extend: to_dim <= cur_dim");
+  if (op.dim() != st.n) throw std::invalid_argument("arnoldi_extend: dimension mismatch");
+  if (use_dcgs2(st, to_dim - st.cur_dim)) {
+    extend_dcgs2(st, op, to_dim, rec);
+  } else {
+    extend_cgs2(st, op, to_dim, rec);
   }
 }
 

@@ -43,7 +43,7 @@ constexpr int NT = 256;  // threads per CTA
 constexpr int NWARP = NT / 32;
 constexpr size_t kSmemPerSm = 200 * 1024;
 
-enum Mode : int { kDot = 0, kSumSq = 1, kUpd2 = 2, kUpd1 = 3, kStore = 4 };
+enum Mode : int { kDot = 0, kSumSq = 1, kUpd2 = 2, kUpd1 = 3, kStore = 4, kDot2 = 5, kUpdD = 6 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -140,10 +140,11 @@ __global__ void __launch_bounds__(NT) k_tspipe(const __grid_constant__ CUtensorM
   constexpr int MAXC = NWARP * CPW;
   constexpr int RQ = TR / 32;  // rows per lane in the column-owner mapping
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ double s_h[MAXC];
-  __shared__ double s_part[2][TR];
-  __shared__ double s_col[MAXC + 1];
-  __shared__ double s_final[MAXC + 1];
+  constexpr bool kTwo = MODE == kDot2 || MODE == kUpdD;  // two vectors / two row sums
+  __shared__ double s_h[kTwo ? 2 * MAXC + 2 : MAXC];
+  __shared__ double s_part[kTwo ? 4 : 2][TR];
+  __shared__ double s_col[kTwo ? 2 * MAXC + 1 : MAXC + 1];
+  __shared__ double s_final[kTwo ? 2 * MAXC + 1 : MAXC + 1];
   __shared__ double s_red[NWARP];
 
   if (MODE == kStore && *a.flag) return;
@@ -160,6 +161,10 @@ __global__ void __launch_bounds__(NT) k_tspipe(const __grid_constant__ CUtensorM
 
   if (MODE == kUpd2 || MODE == kUpd1 || MODE == kStore) {
     for (int j = tid; j < MAXC; j += NT) s_h[j] = j < c ? a.h[j] : 0.0;
+  }
+  if (MODE == kUpdD) {
+    // h = [s (c-1), d (c-1), e, rho]: column c-1 of the tile is the pending u
+    for (int j = tid; j < 2 * (c - 1) + 2; j += NT) s_h[j] = a.h[j];
   }
   if (tid == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
@@ -181,9 +186,11 @@ __global__ void __launch_bounds__(NT) k_tspipe(const __grid_constant__ CUtensorM
     for (int i = 0; i < min(S, count); ++i) issue(i);
   }
 
-  double acc[CPW];
+  double acc[CPW], acc2[kTwo ? CPW : 1];
 #pragma unroll
   for (int jj = 0; jj < CPW; ++jj) acc[jj] = 0.0;
+#pragma unroll
+  for (int jj = 0; jj < (kTwo ? CPW : 1); ++jj) acc2[jj] = 0.0;
   double nrm = 0.0;
   const int half = tid >> 7;  // row-sum split over two halves of the columns
   const int hr = tid & (TR - 1);
@@ -201,7 +208,54 @@ __global__ void __launch_bounds__(NT) k_tspipe(const __grid_constant__ CUtensorM
     const bool full = rows == TR;
     const double* W = T + c * TR;
 
-    if (MODE == kDot || MODE == kSumSq) {
+    if (MODE == kDot2) {
+      // V^T z and V^T u in one sweep; u is the tile's last column
+      double wr[RQ], ur[RQ];
+#pragma unroll
+      for (int q = 0; q < RQ; ++q) {
+        const int r = lane + 32 * q;
+        wr[q] = full ? W[r] : (r < rows ? a.w[row0 + r] : 0.0);
+        ur[q] = T[(c - 1) * TR + r];
+      }
+#pragma unroll
+      for (int jj = 0; jj < CPW; ++jj) {
+        const int j = g + NWARP * jj;
+        if (j < c) {
+          const double* col = T + j * TR + lane;
+#pragma unroll
+          for (int q = 0; q < RQ; ++q) {
+            const double v = col[32 * q];
+            acc[jj] = fma(v, wr[q], acc[jj]);
+            acc2[jj] = fma(v, ur[q], acc2[jj]);
+          }
+        }
+      }
+    } else if (MODE == kUpdD) {
+      // V[:,c-1] = (u - V s)/rho and w = z/rho - V d - e u over the c-1 final
+      // columns; u = tile column c-1, z = w (read and overwritten in place)
+      const int cf = c - 1;
+      const int chf = (cf + 1) >> 1;
+      const int lo = half ? chf : 0, hi = half ? cf : chf;
+      double sp = 0.0, sd = 0.0;
+      const double* col = T + hr;
+      for (int j = lo; j < hi; ++j) {
+        const double v = col[j * TR];
+        sp = fma(v, s_h[j], sp);
+        sd = fma(v, s_h[cf + j], sd);
+      }
+      s_part[half][hr] = sp;
+      s_part[2 + half][hr] = sd;
+      __syncthreads();
+      if (tid < rows) {
+        const double rho = s_h[2 * cf + 1], e = s_h[2 * cf];
+        const double u = T[cf * TR + tid];
+        const double z = full ? W[tid] : a.w[row0 + tid];
+        const double vs = s_part[0][tid] + s_part[1][tid];
+        const double vd = s_part[2][tid] + s_part[3][tid];
+        dstcol[row0 + tid - a.ld] = (u - vs) / rho;  // V[:, c-1]
+        a.w[row0 + tid] = (z / rho - vd) - e * u;
+      }
+    } else if (MODE == kDot || MODE == kSumSq) {
       // rows beyond n are zero in the tile (TMA OOB fill) and w is zeroed here
       double wr[RQ];
 #pragma unroll
@@ -262,8 +316,23 @@ __global__ void __launch_bounds__(NT) k_tspipe(const __grid_constant__ CUtensorM
     }
   }
 
-  if (MODE == kStore) return;
+  if (MODE == kStore || MODE == kUpdD) return;
   int width = 1;
+  if (MODE == kDot2) {
+#pragma unroll
+    for (int jj = 0; jj < CPW; ++jj) {
+      const int j = g + NWARP * jj;
+      if (j < c) {
+        const double t = dev::warp_sum(acc[jj]);
+        const double t2 = dev::warp_sum(acc2[jj]);
+        if (lane == 0) {
+          s_col[j] = t;
+          s_col[c + j] = t2;
+        }
+      }
+    }
+    width = 2 * c;
+  }
   if (MODE == kDot || MODE == kSumSq || MODE == kUpd2) {
 #pragma unroll
     for (int jj = 0; jj < CPW; ++jj) {
@@ -288,8 +357,8 @@ __global__ void __launch_bounds__(NT) k_tspipe(const __grid_constant__ CUtensorM
   __syncthreads();
   if (!finish_grid(s_col, width, a.partials, a.ticket, s_final)) return;
 
-  if (MODE == kDot || MODE == kSumSq) {
-    for (int j = tid; j < c; j += NT) a.out[j] = s_final[j];
+  if (MODE == kDot || MODE == kSumSq || MODE == kDot2) {
+    for (int j = tid; j < width; j += NT) a.out[j] = s_final[j];
     return;
   }
   if (MODE == kUpd1) {
@@ -375,7 +444,7 @@ void launch_pipe(PipeArgs a, ReduceWorkspace& ws, int sm_count, cudaStream_t st)
   a.tiles_per_cta = (ntiles + grid0 - 1) / grid0;
   const int grid = (ntiles + a.tiles_per_cta - 1) / a.tiles_per_cta;
   a.stages = stages;
-  ensure_workspace(ws, grid, NWARP * CPW + 1);
+  ensure_workspace(ws, grid, 2 * NWARP * CPW + 1);
   a.partials = ws.partials.get();
   a.ticket = ws.tickets.get();
   const CUtensorMap map = basis_map(a.V, a.ld, a.n, a.c);
@@ -456,6 +525,29 @@ void cgs2_step(double* V, long long ld, int n, int c, double* w, double* Hcol, i
   b.scal = scal;
   b.flag = flag;
   dispatch<kStore>(b, ws, sm_count, st);
+}
+
+void dcgs2_dot(const double* V, long long ld, int n, int c, const double* z, double* out,
+               ReduceWorkspace& ws, int sm_count, cudaStream_t st) {
+  if (n <= 0) return;
+  check_basis(V, ld, n, c, "dcgs2_dot");
+  check_aligned(z, "dcgs2_dot");
+  PipeArgs a = base_args(V, ld, n, c);
+  a.w = const_cast<double*>(z);
+  a.out = out;
+  dispatch<kDot2>(a, ws, sm_count, st);
+}
+
+void dcgs2_update(double* V, long long ld, int n, int c, double* z, const double* coef,
+                  ReduceWorkspace& ws, int sm_count, cudaStream_t st) {
+  if (n <= 0) return;
+  check_basis(V, ld, n, c, "dcgs2_update");
+  check_aligned(z, "dcgs2_update");
+  if (c < 2) throw std::invalid_argument("dcgs2_update: needs a final column and u");
+  PipeArgs a = base_args(V, ld, n, c);
+  a.w = z;
+  a.h = coef;
+  dispatch<kUpdD>(a, ws, sm_count, st);
 }
 
 void cgs1_pass(const double* V, long long ld, int n, int c, double* v, double* corr,

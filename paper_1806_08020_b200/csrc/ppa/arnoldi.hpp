@@ -16,7 +16,7 @@ namespace ppa {
 /// column-major on the device with ld = n rounded up to 32 doubles; H is
 /// (m+1) x m column-major on the host.
 struct ArnoldiState {
-  DBuffer<double> V;
+  PoolBuffer V;  // (max_dim + 1) columns of ld doubles
   long long ld = 0;
   int n = 0;
   std::vector<double> H;

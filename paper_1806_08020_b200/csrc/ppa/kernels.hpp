@@ -216,6 +216,17 @@ void ts_dot(const double* V, long long ld, int n, int c, const double* w, double
 void cgs2_step(double* V, long long ld, int n, int c, double* w, double* Hcol, int* flag,
                ReduceWorkspace& ws, int sm_count, cudaStream_t st);
 
+/// Delayed CGS2 (arnoldi.cpp "DCGS2"), sweep 1: with the pending vector u in
+/// column c-1 of V, out[0..c) = V[:,0:c]^T z and out[c..2c) = V[:,0:c]^T u in
+/// one read of V.
+void dcgs2_dot(const double* V, long long ld, int n, int c, const double* z, double* out,
+               ReduceWorkspace& ws, int sm_count, cudaStream_t st);
+/// Delayed CGS2, sweep 2: coef = [s (c-1), d (c-1), e, rho];
+/// V[:,c-1] = (u - V[:,0:c-1] s) / rho  and, in place,
+/// z = (z / rho - V[:,0:c-1] d) - e u  (the next pending vector).
+void dcgs2_update(double* V, long long ld, int n, int c, double* z, const double* coef,
+                  ReduceWorkspace& ws, int sm_count, cudaStream_t st);
+
 /// One classical Gram-Schmidt pass: c = V^T v; v -= V c; out_norm = ||v||.
 /// corr (device, c) receives the coefficients.
 void cgs1_pass(const double* V, long long ld, int n, int c, double* v, double* corr,

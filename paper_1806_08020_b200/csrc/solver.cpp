@@ -118,15 +118,19 @@ class StartVectors {
   StartVectors& operator=(const StartVectors&) = delete;
   ~StartVectors() {
     if (worker_.joinable()) worker_.join();
+    cudaStreamSynchronize(current_context().stream());  // uploads from host_ done
   }
 
-  DBuffer<double> take(uint64_t stream) {
+  PoolBuffer take(uint64_t stream) {
     for (size_t i = 0; i < streams_.size(); ++i) {
       if (streams_[i] != stream) continue;
       ready_[i].get();
-      DBuffer<double> d(static_cast<size_t>(n_));
-      PPA_CUDA(cudaMemcpy(d.get(), host_[i].get(), static_cast<size_t>(n_) * sizeof(double),
-                          cudaMemcpyHostToDevice));
+      PoolBuffer d;
+      d.resize(static_cast<size_t>(n_));
+      PPA_CUDA(cudaMemcpyAsync(d.get(), host_[i].get(), static_cast<size_t>(n_) * sizeof(double),
+                               cudaMemcpyHostToDevice, current_context().stream()));
+      // the pinned source stays valid until the StartVectors dies, which
+      // synchronises in its destructor
       return d;
     }
     throw std::logic_error("StartVectors: stream not scheduled");
@@ -319,7 +323,7 @@ RitzSet select_pairs(const ArnoldiState& st, const SolveConfig& cfg, RitzOrderin
 FirstCycle first_cycle(const LinearOperator& a, const LinearOperator& op, const SolveConfig& cfg,
                        RitzOrdering ordering, int nchk, CostRecord& rec, StartVectors& sv) {
   const int n = a.dim();
-  DBuffer<double> v0 = sv.take(rng::kArnoldiStart);
+  PoolBuffer v0 = sv.take(rng::kArnoldiStart);
   FirstCycle f;
   f.st = arnoldi_init(v0.get(), n, cfg.m, rec);
   f.start_dim = f.st.cur_dim;
@@ -339,7 +343,7 @@ void run_cycles(const LinearOperator& a, const LinearOperator& op, const SolveCo
   if (probe) {
     st = std::move(probe->st);
   } else {
-    DBuffer<double> v0 = sv.take(rng::kArnoldiStart);
+    PoolBuffer v0 = sv.take(rng::kArnoldiStart);
     st = arnoldi_init(v0.get(), n, cfg.m, rec);
   }
   (void)ctx;
@@ -445,7 +449,7 @@ PolyPrecond damping_search(const OperatorPtr& a, const SolveConfig& cfg, CostRec
                            std::vector<CycleStats>& history, std::optional<FirstCycle>& keep,
                            StartVectors& sv) {
   const int n = a->dim();
-  DBuffer<double> b = sv.take(rng::kPolyStart);
+  PoolBuffer b = sv.take(rng::kPolyStart);
   DBuffer<double> ab;
   int d = cfg.degree;
   bool damped = false;
@@ -544,7 +548,8 @@ namespace {
 
 // Five counted power-iteration steps from the seeded N(0,1) vector x
 // (SPEC.md "one cycle of power iteration (5 mvps)").
-double power_norm_estimate(const LinearOperator& a, DBuffer<double> x, CostRecord& rec) {
+template <typename Buf>
+double power_norm_estimate(const LinearOperator& a, Buf x, CostRecord& rec) {
   Context& ctx = current_context();
   const cudaStream_t s = ctx.stream();
   const int n = a.dim();
@@ -623,7 +628,7 @@ EigResult solve(const OperatorPtr& a, const SolveConfig& cfg) {
     if (cfg.damping == DampingMode::auto_heuristic) {
       p = damping_search(a, cfg, rec, res.history, probe, sv);
     } else {
-      DBuffer<double> b = sv.take(rng::kPolyStart);
+      PoolBuffer b = sv.take(rng::kPolyStart);
       if (cfg.damping == DampingMode::forced) {
         // damped start A^power b + alpha b (section 6)
         DBuffer<double> bd(static_cast<size_t>(a->dim()));
@@ -668,11 +673,11 @@ EigResult solve_double(const OperatorPtr& a, const SolveConfig& cfg) {
   rec.nnzr = a->nnzr();
   auto t0 = Clock::now();
   StartVectors sv(a->dim(), cfg.seed, solve_streams(*a, {rng::kPolyStart, rng::kPoly2Start}));
-  DBuffer<double> b1 = sv.take(rng::kPolyStart);
+  PoolBuffer b1 = sv.take(rng::kPolyStart);
   PolyPrecond p1 = build_gmres_poly(*a, b1.get(), cfg.double_d1, rec);
   p1.provenance = PolyProvenance::composite_stage;
   OperatorPtr tau = make_poly_complement_operator(a, p1);
-  DBuffer<double> b2 = sv.take(rng::kPoly2Start);
+  PoolBuffer b2 = sv.take(rng::kPoly2Start);
   PolyPrecond p2 = build_gmres_poly(*tau, b2.get(), cfg.double_d2, rec);
   if (cfg.stability == StabilityMode::pof_auto && p2.roots.size() >= 2) {
     p2 = add_stability_roots(p2);

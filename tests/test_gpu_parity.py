@@ -386,7 +386,17 @@ def test_build_gmres_poly_vs_oracle(cuda, gen, deg):
     assert abs(np.linalg.norm(host(out)) - gm) / gm < 1e-6
 
 
-def test_arnoldi_relation_and_orthonormality(cuda):
+@pytest.fixture(params=["cgs2", "dcgs2"])
+def ortho(request, monkeypatch):
+    """Run a test under classic CGS2 and under delayed CGS2 (arnoldi.cpp)."""
+    if request.param == "dcgs2":
+        monkeypatch.setenv("PPA_FORCE_DCGS2", "1")
+    else:
+        monkeypatch.setenv("PPA_DISABLE_DCGS2", "1")
+    return request.param
+
+
+def test_arnoldi_relation_and_orthonormality(cuda, ortho):
     P = ppa.CsrMatrix.convection_diffusion(32)
     n = P.n
     A = ppa.make_csr_operator(P)
@@ -430,17 +440,20 @@ def _read_V(torch, st, n, cols):
     return host(buf).reshape(cols, ld)[:, :n].T.copy()
 
 
-def test_breakdown_diag_e1(cuda):
+def test_breakdown_diag_e1(cuda, ortho):
     # diag[1..6] with e1 breaks down at dimension 1
     A = ppa.make_diagonal(np.arange(1.0, 7.0))
     e1 = np.zeros(6)
     e1[0] = 1.0
-    st = ppa.arnoldi_init(dev(cuda, e1), 6, 3)
-    st.extend(A, 3)
+    rec = ppa.CostRecord()
+    st = ppa.arnoldi_init(dev(cuda, e1), 6, 3, rec)
+    st.extend(A, 3, rec)
     assert st.breakdown and st.cur_dim == 1 and st.H[1, 0] == 0.0
+    # counters as the reference's MGS2: one application, no scaling charge
+    assert rec.mvps == 1 and rec.dots == 1 + 3
 
 
-def test_thick_restart_preserves_pairs(cuda):
+def test_thick_restart_preserves_pairs(cuda, ortho):
     # retained pairs keep value and residual across a restart
     d = np.arange(1.0, 101.0)
     A = ppa.make_diagonal(d)
@@ -460,6 +473,40 @@ def test_thick_restart_preserves_pairs(cuda):
     Vh = _read_V(cuda, st, 100, 21)
     R = np.diag(d) @ Vh[:, :20] - Vh @ st.H
     assert np.linalg.norm(R) <= 1e-9 * max(1.0, np.linalg.norm(st.H))
+
+
+def test_breakdown_late_invariant_subspace(cuda, ortho):
+    # breakdown at step 4 (invariant subspace of dimension 4): DCGS2 finds it
+    # one step late and must un-charge the extra application
+    d = np.arange(1.0, 301.0)
+    v0 = np.zeros(300)
+    v0[[3, 50, 120, 299]] = [1.0, 2.0, -1.0, 0.5]
+    A = ppa.make_diagonal(d)
+    rec = ppa.CostRecord()
+    st = ppa.arnoldi_init(dev(cuda, v0), 300, 10, rec)
+    st.extend(A, 10, rec)
+    assert st.breakdown and st.cur_dim == 4
+    assert rec.mvps == 4
+    assert rec.dots == 1 + sum(2 * (j + 1) + 1 for j in range(4))
+    assert rec.vops == 2 + sum(4 * (j + 1) + 2 for j in range(3)) + 4 * 4 + 1
+    ev = np.sort(np.linalg.eigvals(st.H[:4, :4]).real)
+    assert np.allclose(ev, [4.0, 51.0, 121.0, 300.0], rtol=1e-10)
+
+
+def test_poly_solve_both_orthogonalisations(cuda, ortho):
+    # the polynomial-preconditioned solve on a nonsymmetric matrix agrees with
+    # the oracle under either orthogonalisation
+    P = ppa.CsrMatrix.convection_diffusion(40)
+    A = ppa.make_csr_operator(P)
+    cfg = ppa.SolveConfig(m=40, k=20, nev=8, degree=12, seed=5, max_cycles=60)
+    r = ppa.solve(A, cfg)
+    o = O.solve(O.csr_operator(O.Csr.convection_diffusion(40)), 40, 20, 8, degree=12, seed=5,
+                max_cycles=60)
+    assert r["converged"] and o["converged"]
+    assert np.all(r["residuals"] <= r["rtol"])
+    got, ref = np.sort_complex(r["eigenvalues"]), np.sort_complex(o["eigenvalues"])
+    assert np.max(np.abs(got - ref) / np.abs(ref)) < 1e-8
+    assert abs(r["cost"]["mvps"] - o["cost"]["mvps"]) <= 0.05 * o["cost"]["mvps"]
 
 
 def test_solve_config1_vs_oracle(cuda):

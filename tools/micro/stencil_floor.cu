@@ -117,6 +117,40 @@ __global__ void k_var(const unsigned* __restrict__ mask, const double* __restric
   y[r] = EPI ? __dadd_rn(__ldg(x + r), __dmul_rn(c0, s)) : s;
 }
 
+// 2.5D march along the +-S diagonals (S = N*N): x[r+S] is loaded once and
+// reused as the 0 and -S entries of the next two planes.
+template <int T>
+__global__ void k_march(const unsigned* __restrict__ mask, const double* __restrict__ x,
+                        double* __restrict__ y, int n, double c0, int S, int G, int NQ) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int g = w % G, ch = w / G;
+  const int p = g * 32 + lane;
+  const int q0 = ch * T;
+  if (q0 >= NQ) return;
+  int r = q0 * S + p;
+  double xm = __ldg(x + max(r - S, 0) ), x0 = __ldg(x + min(r, n - 1));
+#pragma unroll 1
+  for (int t = 0; t < T && q0 + t < NQ; ++t, r += S) {
+    const double xp = __ldg(x + min(r + S, n - 1));
+    const unsigned m = __ldg(mask + (min(r, n - 1) >> 5));
+    double xv[7];
+    xv[0] = xm;
+    xv[1] = __ldg(x + min(max(r - N, 0), n - 1));
+    xv[2] = __ldg(x + min(max(r - 1, 0), n - 1));
+    xv[3] = x0;
+    xv[4] = __ldg(x + min(r + 1, n - 1));
+    xv[5] = __ldg(x + min(r + N, n - 1));
+    xv[6] = xp;
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < 7; ++j) s = __dadd_rn(s, __dmul_rn(j == 3 ? 6.0 : -1.0, xv[j]));
+    if (r < n && ((m >> (r & 31)) & 1u)) y[r] = __dadd_rn(x0, __dmul_rn(c0, s));
+    xm = x0;
+    x0 = xp;
+  }
+}
+
 template <typename F>
 float timeit(F f, int reps) {
   cudaEvent_t a, b;
@@ -165,6 +199,16 @@ int main() {
     float d = timeit([&] { k_var<7, false, true><<<g, bs>>>(mask, x, y, NN, 0.5); std::swap(x, y); }, 50);
     float e = timeit([&] { k_var<8, true, true><<<g, bs>>>(mask, x, y, NN, 0.5); std::swap(x, y); }, 50);
     printf("var: base7 %.2f  gather8 %.2f  mask %.2f  epi %.2f  all %.2f us\n", a, b, c, d, e);
+    const int S = N * N, G = S / 32, NQ = N;
+    for (int T : {4, 8, 16}) {
+      const int warps = G * ((NQ + T - 1) / T);
+      const int blocks = (warps * 32 + 255) / 256;
+      float tm = 0;
+      if (T == 4) tm = timeit([&] { k_march<4><<<blocks, 256>>>(mask, x, y, NN, 0.5, S, G, NQ); std::swap(x, y); }, 50);
+      if (T == 8) tm = timeit([&] { k_march<8><<<blocks, 256>>>(mask, x, y, NN, 0.5, S, G, NQ); std::swap(x, y); }, 50);
+      if (T == 16) tm = timeit([&] { k_march<16><<<blocks, 256>>>(mask, x, y, NN, 0.5, S, G, NQ); std::swap(x, y); }, 50);
+      printf("march T=%d: %.2f us\n", T, tm);
+    }
   }
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
