@@ -394,7 +394,13 @@ def run_b200(args):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "kernel": "k_spmv_sell32 (fused real-root factor)",
-                         "algorithmic_bytes_per_launch": bspmv},
+                         "algorithmic_bytes_per_launch": bspmv,
+                         # the byte model counts row_ptr (16.4 MB) that SELL-32 never
+                         # reads; the ncu DRAM bytes per launch over the same time:
+                         "traffic_gbs": (round(traffic / (avg_launch_ms * 1e-3) / 1e9, 2)
+                                         if traffic else None),
+                         "traffic_frac": (round(traffic / (avg_launch_ms * 1e-3) / 1e9 / peak, 4)
+                                          if traffic else None)},
             "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
                     "d2h_bytes_per_step": 8 * n, "ms_per_step": round(e2e_ms, 4),
                     "matches_device_result": e2e_match},

@@ -154,6 +154,58 @@ def test_dia_diagonal_counts_bit_exact(cuda, offsets):
         assert np.array_equal(AY[j, :n], O.csr_operator(Q).apply(Y[j, :n]))
 
 
+def _edge_matrices():
+    rng = np.random.default_rng(11)
+    out = {}
+    # ragged: every third row empty, the rest 1-9 entries near the diagonal
+    n = 3000
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        if i % 3 == 0:
+            continue
+        for o in sorted(set(rng.integers(-40, 41, 1 + i % 9).tolist())):
+            if 0 <= i + o < n:
+                rows.append(i)
+                cols.append(i + o)
+                vals.append(float(rng.choice([-1.0, 2.5, 0.0, -0.0])))  # explicit zeros
+    out["ragged_zeros"] = (n, rows, cols, vals)
+    # one row, one entry
+    out["n1"] = (1, [0], [0], [3.0])
+    # last rows empty, first row dense-ish
+    n = 700
+    rows, cols, vals = [], [], []
+    for j in range(0, n, 7):
+        rows.append(0)
+        cols.append(j)
+        vals.append(1.0 + j)
+    for i in range(1, n - 40):
+        rows += [i, i]
+        cols += [i - 1, i]
+        vals += [-1.0, 2.0]
+    out["tail_empty"] = (n, rows, cols, vals)
+    return out
+
+
+EDGE = _edge_matrices()
+
+
+@pytest.mark.parametrize("cap", ["auto", "csr", "sell32", "sell32_packed", "dia_coded"])
+@pytest.mark.parametrize("name", sorted(EDGE))
+def test_edge_matrices_every_layout(cuda, cap, name):
+    n, rows, cols, vals = EDGE[name]
+    P = ppa.CsrMatrix.from_triplets(n, rows, cols, vals)
+    Q = O.Csr.from_triplets(n, rows, cols, vals)
+    A = ppa.make_csr_operator(P, cap)
+    x = O.normal_vector(n, 5, 5)
+    y = cuda.empty(n, dtype=cuda.float64, device="cuda")
+    A.apply(dev(cuda, x), y)
+    assert np.array_equal(host(y), O.csr_operator(Q).apply(x))
+    roots = _roots_mixed()
+    out = cuda.empty(n, dtype=cuda.float64, device="cuda")
+    ppa.apply_poly(roots, A, dev(cuda, x), out)
+    assert np.array_equal(host(out), O.apply_poly(roots, O.csr_operator(Q), x))
+
+
 def test_packed_fp64_values_and_perm(cuda):
     # packed stream without a value table (> 256 distinct values), sigma-sorted
     # rows of very different lengths, offsets near the int16 limit
