@@ -147,6 +147,11 @@ def test_config_solve_vs_fixture(cuda, k):
         return
     assert np.all(r["residuals"] <= r["rtol"])
     assert abs(r["cost"]["mvps"] - g["cost"]["mvps"]) <= 0.05 * g["cost"]["mvps"]
+    if k in (1, 2):
+        # simple spectra: the GPU and oracle trajectories agree to roundoff
+        # through the early cycles (~1e-13 observed in cycles 1-2)
+        hist, ghist = r["cycle_max_residual"], np.array(g["cycle_max_residual"])
+        assert np.allclose(hist[:3], ghist[:3], rtol=1e-8, atol=0)
     if k in (2, 5):
         # Constant-Peclet convection-diffusion: the certified Ritz values lie in
         # the pseudospectrum, where CPU and
