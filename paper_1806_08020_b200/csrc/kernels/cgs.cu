@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(NT) k_tspipe(const __grid_constant__ CUtensorM
   __shared__ double s_col[kTwo ? 2 * MAXC + 1 : MAXC + 1];
   __shared__ double s_final[kTwo ? 2 * MAXC + 1 : MAXC + 1];
   __shared__ double s_red[NWARP];
+  __shared__ double s_wn[MODE == kUpd2 ? TR : 1];
 
   if (MODE == kStore && *a.flag) return;
   const int tid = threadIdx.x, lane = tid & 31, g = tid >> 5;
@@ -283,20 +284,30 @@ __global__ void __launch_bounds__(NT) k_tspipe(const __grid_constant__ CUtensorM
       s_part[half][hr] = sp;
       __syncthreads();
       if (MODE == kUpd2) {
+        // the updated rows once (first 128 threads), then every warp's
+        // pass-2 dots read them from shared memory
+        if (tid < TR) {
+          double wn = 0.0;
+          if (tid < rows) {
+            const double wo = full ? W[tid] : a.w[row0 + tid];
+            wn = wo - (s_part[0][tid] + s_part[1][tid]);
+            a.w[row0 + tid] = wn;
+          }
+          s_wn[tid] = wn;
+        }
+        __syncthreads();
 #pragma unroll
         for (int q = 0; q < RQ; ++q) {
           const int r = lane + 32 * q;
-          const double wo = full ? W[r] : (r < rows ? a.w[row0 + r] : 0.0);
-          const double wn = r < rows ? wo - (s_part[0][r] + s_part[1][r]) : 0.0;
+          const double wn = s_wn[r];
 #pragma unroll
           for (int jj = 0; jj < CPW; ++jj) {
             const int j = g + NWARP * jj;
             if (j < c) acc[jj] = fma(T[j * TR + r], wn, acc[jj]);
           }
-          if (g == 0 && r < rows) {
-            nrm = fma(wn, wn, nrm);
-            a.w[row0 + r] = wn;
-          }
+          // ||w||^2 in warp 0, rows lane + 32q (the reduction order the
+          // Hessenberg subdiagonal has always used)
+          if (g == 0 && r < rows) nrm = fma(wn, wn, nrm);
         }
       } else if (tid < rows) {
         const double wo = full ? W[tid] : a.w[row0 + tid];
@@ -427,17 +438,34 @@ CUtensorMap basis_map(const double* V, long long ld, int n, int c) {
 template <int MODE, int CPW>
 void launch_pipe(PipeArgs a, ReduceWorkspace& ws, int sm_count, cudaStream_t st) {
   const size_t stage_bytes = static_cast<size_t>(a.c + 1) * TR * sizeof(double);
-  // two CTAs per SM when two double-buffered CTAs fit, else one deeper CTA
-  const int per_sm = 4 * stage_bytes <= kSmemPerSm ? 2 : 1;
-  const size_t budget = kSmemPerSm / per_sm;
-  const int stages =
-      static_cast<int>(std::max<size_t>(2, std::min<size_t>(6, budget / stage_bytes)));
+  int per_sm, stages;
+  if (8 * stage_bytes <= kSmemPerSm / 2) {
+    // small bases (c < ~12): short tiles, so more resident CTAs (4 stages
+    // each) keep enough rows in flight and enough warps issuing
+    stages = 4;
+    per_sm = static_cast<int>(
+        std::max<size_t>(1, std::min<size_t>(6, kSmemPerSm / (stages * stage_bytes + 1024))));
+  } else {
+    // two CTAs per SM when two double-buffered CTAs fit, else one deeper CTA
+    per_sm = 4 * stage_bytes <= kSmemPerSm ? 2 : 1;
+    const size_t budget = kSmemPerSm / per_sm;
+    stages = static_cast<int>(std::max<size_t>(2, std::min<size_t>(6, budget / stage_bytes)));
+  }
   const size_t smem = 128 + stage_bytes * stages;
   static size_t configured = 0;
   if (smem > configured) {
     PPA_CUDA(cudaFuncSetAttribute(k_tspipe<MODE, CPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(std::max<size_t>(smem, 48 * 1024))));
     configured = std::max<size_t>(smem, 48 * 1024);
+  }
+  {
+    // never more CTAs than can be resident: the kernel is persistent
+    int fit = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, k_tspipe<MODE, CPW>, NT, smem) ==
+            cudaSuccess &&
+        fit > 0) {
+      per_sm = std::min(per_sm, fit);
+    }
   }
   const int ntiles = (a.n + TR - 1) / TR;
   const int grid0 = std::max(1, std::min(ntiles, sm_count * per_sm));
