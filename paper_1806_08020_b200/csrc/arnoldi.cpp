@@ -139,36 +139,69 @@ ArnoldiState arnoldi_init(const double* v0, int n, int m, CostRecord& rec) {
 
 namespace {
 
-// Classic CGS2: three sweeps per step (kernels/cgs.cu), one host sync to
-// read the Hessenberg column and the breakdown flag.
+// Classic CGS2: three sweeps per step (kernels/cgs.cu).  The host needs each
+// step's Hessenberg column and breakdown flag, but the device does not need
+// the host to start the next step (its input V[:,j+1] is written by the
+// store sweep), so step j+1 is enqueued before the host waits for step j:
+// the device never idles on the round trip.  If step j breaks down, step
+// j+1 ran on an unwritten column; its results are ignored (columns past
+// cur_dim are never read) and its operator application is un-charged.
 void extend_cgs2(ArnoldiState& st, const LinearOperator& op, int to_dim, CostRecord& rec) {
   Context& ctx = current_context();
   const cudaStream_t s = ctx.stream();
   Scratch w(static_cast<size_t>(st.n));
-  Scratch hdev(static_cast<size_t>(st.max_dim) + 4);
+  const size_t slot = static_cast<size_t>(st.max_dim) + 4;
+  Scratch hdev(slot);
   double* Hcol = hdev.get();
   int* flag = reinterpret_cast<int*>(hdev.get() + st.max_dim + 2);
-  double* host = ctx.pinned(static_cast<size_t>(st.max_dim) + 4);
-  for (int j = st.cur_dim; j < to_dim; ++j) {
+  double* host = ctx.pinned(2 * slot);
+  cudaEvent_t ev[2];
+  PPA_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  PPA_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  struct EventGuard {
+    cudaEvent_t* e;
+    ~EventGuard() {
+      cudaEventDestroy(e[0]);
+      cudaEventDestroy(e[1]);
+    }
+  } guard{ev};
+  const int j0 = st.cur_dim;
+  auto issue = [&](int j) {
     op.apply(st.col(j), w.get(), rec);
-    const int c = j + 1;
-    kern::cgs2_step(st.V.get(), st.ld, st.n, c, w.get(), Hcol, flag, ctx.ws(), ctx.sm_count(), s);
-    PPA_CUDA(cudaMemcpyAsync(host, hdev.get(), (st.max_dim + 4) * sizeof(double),
+    kern::cgs2_step(st.V.get(), st.ld, st.n, j + 1, w.get(), Hcol, flag, ctx.ws(),
+                    ctx.sm_count(), s);
+    const int b = (j - j0) & 1;
+    PPA_CUDA(cudaMemcpyAsync(host + b * slot, hdev.get(), slot * sizeof(double),
                              cudaMemcpyDeviceToHost, s));
-    ctx.sync();
-    for (int i = 0; i <= c; ++i) st.h(i, j) = host[i];
-    const int bd = *reinterpret_cast<const int*>(host + st.max_dim + 2);
-    // MGS2 charges (src/arnoldi.cpp:130-140): 2c dots+axpys, one norm.
-    rec.dots += 2LL * c + 1;
-    rec.vops += 4LL * c + 1;
+    PPA_CUDA(cudaEventRecord(ev[b], s));
+  };
+  issue(j0);
+  for (int j = j0; j < to_dim; ++j) {
+    const CostRecord before_next = rec;
+    if (j + 1 < to_dim) issue(j + 1);
+    const int b = (j - j0) & 1;
+    PPA_CUDA(cudaEventSynchronize(ev[b]));
+    const double* hc = host + b * slot;
+    const int c = j + 1;
+    for (int i = 0; i <= c; ++i) st.h(i, j) = hc[i];
+    const int bd = *reinterpret_cast<const int*>(hc + st.max_dim + 2);
     st.cur_dim = j + 1;
-    if (bd == 2) throw std::runtime_error("arnoldi_extend: non-finite basis vector");
+    if (bd == 2) {
+      ctx.sync();
+      throw std::runtime_error("arnoldi_extend: non-finite basis vector");
+    }
+    // MGS2 charges (src/arnoldi.cpp:130-140): 2c dots+axpys, one norm.
     if (bd == 1) {
+      ctx.sync();
+      rec = before_next;  // the speculative next step does not count
+      rec.dots += 2LL * c + 1;
+      rec.vops += 4LL * c + 1;
       st.h(j + 1, j) = 0.0;
       st.breakdown = true;
       return;
     }
-    ++rec.vops;  // the scaling (src/arnoldi.cpp:149-150)
+    rec.dots += 2LL * c + 1;
+    rec.vops += 4LL * c + 2;  // + the scaling (src/arnoldi.cpp:149-150)
   }
 }
 
