@@ -365,11 +365,9 @@ def run_b200(args):
         solve_info["sell32"] = solve_on(A)
         # opt-in delayed CGS2 (two sweeps over V per step instead of three;
         # DESIGN.md §3.2): same eigenpairs, roundoff may move convergence by a cycle
-        os.environ["PPA_DCGS2"] = "1"
-        try:
-            solve_info["dcgs2"] = solve_on(A_auto)
-        finally:
-            del os.environ["PPA_DCGS2"]
+        cfg.orthogonalization = "dcgs2"
+        warm.orthogonalization = "dcgs2"
+        solve_info["dcgs2"] = solve_on(A_auto)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

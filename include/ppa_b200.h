@@ -144,6 +144,8 @@ int ppa_eval_poly(const double* re, const double* im, int n, double z_re, double
 int ppa_arnoldi_init(const double* v0_dev, int n, int m, ppa_cost* cost, ppa_arnoldi** out);
 /* arnoldi_extend (src/arnoldi.cpp:115-152), CGS2 on device */
 int ppa_arnoldi_extend(ppa_arnoldi* st, const ppa_op* op, int to_dim, ppa_cost* cost);
+/* orthogonalisation of later extends: 0 CGS2 (default), 1 delayed CGS2 */
+int ppa_arnoldi_set_orthogonalization(ppa_arnoldi* st, int mode);
 int ppa_arnoldi_info(const ppa_arnoldi* st, int* cur_dim, int* max_dim, int* breakdown,
                      long long* ld, double** V_dev);
 /* H, (m+1) x m column-major */
@@ -197,6 +199,7 @@ typedef struct ppa_solve_config {
   int stagnation_stop, stagnation_window;
   double stagnation_rtol;
   int want_eigenvectors;     /* keep unit eigenvectors for evec_re/evec_im */
+  int orthogonalization;     /* 0 CGS2 (default), 1 delayed CGS2 */
 } ppa_solve_config;
 
 /* EigResult (inc/solver.hpp:71-89); arrays supplied by the caller */

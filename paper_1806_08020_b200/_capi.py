@@ -53,7 +53,8 @@ class _SolveConfigC(C.Structure):
                 ("damping", C.c_int), ("damping_alpha", C.c_double), ("damping_power", C.c_int),
                 ("check_mid_cycle", C.c_int), ("mid_cycle_stride", C.c_int),
                 ("stagnation_stop", C.c_int), ("stagnation_window", C.c_int),
-                ("stagnation_rtol", C.c_double), ("want_eigenvectors", C.c_int)]
+                ("stagnation_rtol", C.c_double), ("want_eigenvectors", C.c_int),
+                ("orthogonalization", C.c_int)]
 
 
 _dp = C.POINTER(C.c_double)
@@ -115,6 +116,7 @@ def lib():
             "ppa_csr_model_bytes": [vp, _dp, C.POINTER(C.c_longlong)],
             "ppa_csr_layout": [vp, _ip, _dp, _ip, _ip],
             "ppa_csr_operator_layout": [vp, C.c_int, C.POINTER(vp)],
+            "ppa_arnoldi_set_orthogonalization": [vp, C.c_int],
             "ppa_apply_poly": [vp, vp, C.c_int, vp, vp, vp, C.POINTER(CostRecord)],
             "ppa_build_gmres_poly": [vp, vp, C.c_int, vp, vp, _ip, _ip, C.POINTER(CostRecord)],
             "ppa_leja_order": [vp, vp, C.c_int, vp, vp],
@@ -525,6 +527,10 @@ class ArnoldiState:
         _check(lib().ppa_arnoldi_get_H(self._h, _np_ptr(h)))
         return h.reshape((m, m + 1)).T.copy()
 
+    def set_orthogonalization(self, mode: str) -> None:
+        """cgs2 (default) or dcgs2 for later extends (ppa_arnoldi_set_orthogonalization)."""
+        _check(lib().ppa_arnoldi_set_orthogonalization(self._h, {"cgs2": 0, "dcgs2": 1}[mode]))
+
     def extend(self, op: LinearOperator, to_dim: int, rec: Optional[CostRecord] = None):
         rec = rec if rec is not None else CostRecord()
         _check(lib().ppa_arnoldi_extend(self._h, op._h, to_dim, C.byref(rec)))
@@ -598,6 +604,7 @@ class SolveConfig:
     stagnation_window: int = 5
     stagnation_rtol: float = 0.01
     want_eigenvectors: bool = False
+    orthogonalization: str = "cgs2"  # cgs2 | dcgs2 (delayed CGS2)
     reference: Sequence[complex] = field(default_factory=list)
 
     def _c(self, use_double: bool) -> _SolveConfigC:
@@ -610,7 +617,8 @@ class SolveConfig:
                              self.damping_power, int(self.check_mid_cycle),
                              self.mid_cycle_stride, int(self.stagnation_stop),
                              self.stagnation_window, self.stagnation_rtol,
-                             int(self.want_eigenvectors))
+                             int(self.want_eigenvectors),
+                             {"cgs2": 0, "dcgs2": 1}[self.orthogonalization])
 
 
 def _solve(a: LinearOperator, cfg: SolveConfig, use_double: bool) -> dict:

@@ -5,7 +5,6 @@
 
 #include <algorithm>
 #include <cmath>
-#include <cstdlib>
 #include <numeric>
 #include <stdexcept>
 
@@ -328,18 +327,14 @@ void extend_dcgs2(ArnoldiState& st, const LinearOperator& op, int to_dim, CostRe
   ++rec.vops;
 }
 
-// DCGS2 is opt-in (PPA_DCGS2=1): it is as stable as CGS2 but its roundoff
-// differs enough that borderline convergence tests can flip by a cycle
-// (config 3 converges in 4 cycles instead of the oracle's 5), which breaks
-// the matvec-count parity the reference comparison asks for.  With it on,
-// small bases keep CGS2 (the extra host round trip per step only pays once a
-// sweep over V is long); PPA_FORCE_DCGS2=1 ignores the size (tests).
+// DCGS2 is opt-in (ArnoldiState::ortho, SolveConfig::orthogonalization):
+// it is as stable as CGS2 but its roundoff differs enough that borderline
+// convergence tests can flip by a cycle (config 3 converges in 4 cycles
+// instead of the oracle's 5), which breaks the matvec-count parity the
+// reference comparison asks for.  A single-step extend keeps CGS2 (the
+// delayed form would need a flush pass as well).
 bool use_dcgs2(const ArnoldiState& st, int steps) {
-  if (std::getenv("PPA_DISABLE_DCGS2")) return false;
-  const bool force = std::getenv("PPA_FORCE_DCGS2") != nullptr;
-  const char* on = std::getenv("PPA_DCGS2");
-  const bool enabled = force || (on && on[0] == '1');
-  return enabled && steps >= 2 && (force || st.n >= (1 << 17));
+  return st.ortho == Orthogonalization::dcgs2 && steps >= 2;
 }
 
 }  // namespace

@@ -117,6 +117,10 @@ ppa::SolveConfig to_config(const ppa_solve_config& c) {
   if (c.stagnation_window > 0) cfg.stagnation_window = c.stagnation_window;
   if (c.stagnation_rtol > 0) cfg.stagnation_rtol = c.stagnation_rtol;
   cfg.want_eigenvectors = c.want_eigenvectors != 0;
+  if (c.orthogonalization < 0 || c.orthogonalization > 1) {
+    throw std::invalid_argument("SolveConfig: orthogonalization must be 0 or 1");
+  }
+  cfg.orthogonalization = static_cast<ppa::Orthogonalization>(c.orthogonalization);
   return cfg;
 }
 
@@ -538,6 +542,14 @@ int ppa_arnoldi_extend(ppa_arnoldi* st, const ppa_op* op, int to_dim, ppa_cost* 
       throw;
     }
     add_cost(cost, r);
+  });
+}
+
+int ppa_arnoldi_set_orthogonalization(ppa_arnoldi* st, int mode) {
+  return guard([&] {
+    need(st, "ppa_arnoldi_set_orthogonalization");
+    if (mode < 0 || mode > 1) throw std::invalid_argument("orthogonalization must be 0 or 1");
+    st->s.ortho = static_cast<ppa::Orthogonalization>(mode);
   });
 }
 

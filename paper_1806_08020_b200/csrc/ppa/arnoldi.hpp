@@ -15,8 +15,13 @@ namespace ppa {
 /// Op V_j = V_{j+1} H_{j+1,j} (inc/arnoldi.hpp:18-26).  V is n x (m+1),
 /// column-major on the device with ld = n rounded up to 32 doubles; H is
 /// (m+1) x m column-major on the host.
+/// Orthogonalisation of arnoldi_extend: classic CGS2 (three sweeps per
+/// step, the default) or delayed CGS2 (two sweeps per step; arnoldi.cpp).
+enum class Orthogonalization { cgs2 = 0, dcgs2 = 1 };
+
 struct ArnoldiState {
   PoolBuffer V;  // (max_dim + 1) columns of ld doubles
+  Orthogonalization ortho = Orthogonalization::cgs2;
   long long ld = 0;
   int n = 0;
   std::vector<double> H;

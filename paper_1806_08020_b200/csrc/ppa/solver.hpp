@@ -55,6 +55,8 @@ struct SolveConfig {
   double stagnation_rtol = 0.01;  // run until max-residual stalls
   EigenList reference;
   bool want_eigenvectors = false;  // materialise EigResult::eigenvectors
+  // cycle orthogonalisation (ours; the polynomial build always uses CGS2)
+  Orthogonalization orthogonalization = Orthogonalization::cgs2;
   bool allow_nev_above_k = false;
 
   void validate() const;

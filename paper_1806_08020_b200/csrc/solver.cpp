@@ -326,6 +326,7 @@ FirstCycle first_cycle(const LinearOperator& a, const LinearOperator& op, const 
   PoolBuffer v0 = sv.take(rng::kArnoldiStart);
   FirstCycle f;
   f.st = arnoldi_init(v0.get(), n, cfg.m, rec);
+  f.st.ortho = cfg.orthogonalization;
   f.start_dim = f.st.cur_dim;
   arnoldi_extend(f.st, op, cfg.m, rec);
   f.set = select_pairs(f.st, cfg, ordering);
@@ -345,6 +346,7 @@ void run_cycles(const LinearOperator& a, const LinearOperator& op, const SolveCo
   } else {
     PoolBuffer v0 = sv.take(rng::kArnoldiStart);
     st = arnoldi_init(v0.get(), n, cfg.m, rec);
+    st.ortho = cfg.orthogonalization;
   }
   (void)ctx;
   std::vector<double> best;

@@ -439,12 +439,8 @@ def test_build_gmres_poly_vs_oracle(cuda, gen, deg):
 
 
 @pytest.fixture(params=["cgs2", "dcgs2"])
-def ortho(request, monkeypatch):
+def ortho(request):
     """Run a test under classic CGS2 and under delayed CGS2 (arnoldi.cpp)."""
-    if request.param == "dcgs2":
-        monkeypatch.setenv("PPA_FORCE_DCGS2", "1")
-    else:
-        monkeypatch.setenv("PPA_DISABLE_DCGS2", "1")
     return request.param
 
 
@@ -456,6 +452,7 @@ def test_arnoldi_relation_and_orthonormality(cuda, ortho):
     v0 = O.normal_vector(n, 3, 3)
     rec = ppa.CostRecord()
     st = ppa.arnoldi_init(dev(cuda, v0), n, m, rec)
+    st.set_orthogonalization(ortho)
     st.extend(A, m, rec)
     assert st.cur_dim == m and not st.breakdown
     Vh = _read_V(cuda, st, n, m + 1)
@@ -499,6 +496,7 @@ def test_breakdown_diag_e1(cuda, ortho):
     e1[0] = 1.0
     rec = ppa.CostRecord()
     st = ppa.arnoldi_init(dev(cuda, e1), 6, 3, rec)
+    st.set_orthogonalization(ortho)
     st.extend(A, 3, rec)
     assert st.breakdown and st.cur_dim == 1 and st.H[1, 0] == 0.0
     # counters as the reference's MGS2: one application, no scaling charge
@@ -511,6 +509,7 @@ def test_thick_restart_preserves_pairs(cuda, ortho):
     A = ppa.make_diagonal(d)
     v0 = O.normal_vector(100, 4, 3)
     st = ppa.arnoldi_init(dev(cuda, v0), 100, 20)
+    st.set_orthogonalization(ortho)
     st.extend(A, 20)
     vals, res = st.ritz_pairs(ppa.SMALLEST_MAGNITUDE)
     kk = st.thick_restart(8, ppa.SMALLEST_MAGNITUDE)
@@ -536,6 +535,7 @@ def test_breakdown_late_invariant_subspace(cuda, ortho):
     A = ppa.make_diagonal(d)
     rec = ppa.CostRecord()
     st = ppa.arnoldi_init(dev(cuda, v0), 300, 10, rec)
+    st.set_orthogonalization(ortho)
     st.extend(A, 10, rec)
     assert st.breakdown and st.cur_dim == 4
     assert rec.mvps == 4
@@ -550,7 +550,8 @@ def test_poly_solve_both_orthogonalisations(cuda, ortho):
     # the oracle under either orthogonalisation
     P = ppa.CsrMatrix.convection_diffusion(40)
     A = ppa.make_csr_operator(P)
-    cfg = ppa.SolveConfig(m=40, k=20, nev=8, degree=12, seed=5, max_cycles=60)
+    cfg = ppa.SolveConfig(m=40, k=20, nev=8, degree=12, seed=5, max_cycles=60,
+                          orthogonalization=ortho)
     r = ppa.solve(A, cfg)
     o = O.solve(O.csr_operator(O.Csr.convection_diffusion(40)), 40, 20, 8, degree=12, seed=5,
                 max_cycles=60)
