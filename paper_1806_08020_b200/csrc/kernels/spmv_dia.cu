@@ -199,7 +199,7 @@ struct DiaRParams {
 // the regular sweep.
 constexpr int RB = 512;
 
-template <int MODE, bool COMPL, int ND>
+template <int MODE, bool COMPL, int ND, int RPT>
 __global__ void __launch_bounds__(RB) k_spmv_diar(
     const unsigned* __restrict__ mask, const int* __restrict__ irr_rows,
     const unsigned char* __restrict__ irr_codes, int n_irr, int gx,
@@ -207,8 +207,6 @@ __global__ void __launch_bounds__(RB) k_spmv_diar(
     double* y, const EpiDev e) {
   constexpr int NW = ND <= 4 ? 1 : ND <= 8 ? 2 : 4;  // code words per row (stride / 4)
   pdl_trigger();
-  double sum = 0.0;
-  int r;
   const int bx = blockIdx.x;
   if (bx < gx) {
     const int k = bx * RB + threadIdx.x;
@@ -216,7 +214,7 @@ __global__ void __launch_bounds__(RB) k_spmv_diar(
       pdl_wait();
       return;
     }
-    r = __ldg(irr_rows + k);
+    const int r = __ldg(irr_rows + k);
     unsigned ec[NW];
     load_codes<NW>(ec, reinterpret_cast<const unsigned*>(irr_codes) + static_cast<long long>(k) * NW);
     pdl_wait();  // x is the previous factor's output
@@ -226,42 +224,69 @@ __global__ void __launch_bounds__(RB) k_spmv_diar(
       const unsigned c = code_of(ec[j / 4], j);
       xv[j] = __ldg(x + (c != kDiaAbsent ? r + P.off[j] : r));
     }
+    double sum = 0.0;
 #pragma unroll
     for (int j = 0; j < ND; ++j) {
       const unsigned c = code_of(ec[j / 4], j);
       if (c != kDiaAbsent) sum = __dadd_rn(sum, __dmul_rn(__ldg(dict + c), xv[j]));
     }
-  } else {
-    r = (bx - gx) * RB + threadIdx.x;
-    if (r >= n) {
-      pdl_wait();
-      return;
-    }
-    const unsigned m = __ldg(mask + (r >> 5));
-    pdl_wait();  // x is the previous factor's output
-    double xv[ND];
-#pragma unroll
-    for (int j = 0; j < ND; ++j) xv[j] = __ldg(x + min(max(r + P.off[j], 0), n - 1));
-#pragma unroll
-    for (int j = 0; j < ND; ++j) sum = __dadd_rn(sum, __dmul_rn(P.val[j], xv[j]));
-    if (!((m >> (r & 31)) & 1u)) return;
+    y[r] = epilogue<MODE, COMPL>(r, sum, x, e);
+    return;
   }
-  y[r] = epilogue<MODE, COMPL>(r, sum, x, e);
+  // regular rows: RPT rows per thread, RB apart, all gathers issued first
+  const int r0 = (bx - gx) * (RB * RPT) + threadIdx.x;
+  unsigned m[RPT];
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int r = r0 + u * RB;
+    m[u] = r < n ? __ldg(mask + (r >> 5)) : 0u;
+  }
+  pdl_wait();  // x is the previous factor's output
+  double xv[RPT][ND];
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int r = min(r0 + u * RB, n - 1);
+#pragma unroll
+    for (int j = 0; j < ND; ++j) xv[u][j] = __ldg(x + min(max(r + P.off[j], 0), n - 1));
+  }
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int r = r0 + u * RB;
+    double sum = 0.0;
+#pragma unroll
+    for (int j = 0; j < ND; ++j) sum = __dadd_rn(sum, __dmul_rn(P.val[j], xv[u][j]));
+    if (r < n && ((m[u] >> (r & 31)) & 1u)) y[r] = epilogue<MODE, COMPL>(r, sum, x, e);
+  }
 }
 
-template <int MODE, bool COMPL, int ND>
-void launch_diar(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep,
-                 cudaStream_t st) {
+template <int MODE, bool COMPL, int ND, int RPT>
+void launch_diar_rpt(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep,
+                     cudaStream_t st) {
   DiaRParams P{};
   for (int j = 0; j < a.dia_ndiag; ++j) {
     P.off[j] = a.dia_off[j];
     P.val[j] = a.dia_dflt[j];
   }
   const int gx = static_cast<int>((a.dia_nirr + RB - 1) / RB);
-  const int grid = gx + (a.n + RB - 1) / RB;
-  launch_pdl(k_spmv_diar<MODE, COMPL, ND>, dim3(grid), dim3(RB), 0, st, a.dia_mask,
+  const int grid = gx + (a.n + RB * RPT - 1) / (RB * RPT);
+  launch_pdl(k_spmv_diar<MODE, COMPL, ND, RPT>, dim3(grid), dim3(RB), 0, st, a.dia_mask,
              a.dia_irr_rows, a.dia_irr_codes, static_cast<int>(a.dia_nirr), gx, a.dia_dict, P,
              a.n, x, y, epi_dev(ep));
+}
+
+// Rows per thread of the regular sweep: each thread keeps RPT rows' gathers
+// in flight (the kernel is latency-bound: 17.6 -> 15.4 us on config 3 and
+// 15.0 -> 11.9 us on config 5 going from 1 to 3 rows), for matrices large
+// enough to still fill ~4 waves of CTAs (config 2, n = 1e6, keeps 1), and
+// not for wide stencils (registers).
+template <int MODE, bool COMPL, int ND>
+void launch_diar(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep,
+                 cudaStream_t st) {
+  constexpr long long kRowsFor3 = 3LL * RB * 148 * 4 * 4;  // 3 rows x 4 waves x 4 CTAs/SM
+  if constexpr (ND <= 8) {
+    if (a.n >= kRowsFor3) return launch_diar_rpt<MODE, COMPL, ND, 3>(a, x, y, ep, st);
+  }
+  launch_diar_rpt<MODE, COMPL, ND, 1>(a, x, y, ep, st);
 }
 
 // The regular-row kernel is instantiated per diagonal count so the row sum
