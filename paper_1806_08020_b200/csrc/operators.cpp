@@ -295,6 +295,14 @@ class Block2Operator final : public LinearOperator {
   double nnzr() const override { return a_->nnzr(); }
   void apply(const double* x, double* y, CostRecord& rec) const override {
     const long long n = a_->dim();
+    if (const auto* csr = dynamic_cast<const CsrOperator*>(a_.get())) {
+      // both halves in one pass over the matrix (multi-RHS SpMV; each column
+      // bit-identical to the single SpMV)
+      if (x == y) throw std::invalid_argument("Block2Operator::apply: x and y alias");
+      rec.mvps += 2;
+      kern::spmm(csr->device(), x, n, 2, y, n, current_context().stream());
+      return;
+    }
     a_->apply(x, y, rec);
     a_->apply(x + n, y + n, rec);
   }

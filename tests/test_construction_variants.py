@@ -125,11 +125,14 @@ def test_example6_damping_oracle():
 
 # ----------------------------------------------------------------- GPU parity --
 @pytest.mark.gpu
-def test_block2_shifted_gpu(cuda):
+@pytest.mark.parametrize("gen", [lambda M: M.convection_diffusion(30),   # diagonal layout
+                                 lambda M: M.bidiagonal(900),           # SELL-32
+                                 lambda M: M.random_poisson(5000, 8.0, 3)])  # packed SELL
+def test_block2_shifted_gpu(cuda, gen):
     import paper_1806_08020_b200 as ppa
 
-    P = ppa.CsrMatrix.convection_diffusion(30)
-    Q = O.Csr.convection_diffusion(30)
+    P = gen(ppa.CsrMatrix)
+    Q = gen(O.Csr)
     n = P.n
     x = np.concatenate([O.normal_vector(n, 1, 1), O.normal_vector(n, 2, 1)])
     B = ppa.make_block2(ppa.make_csr_operator(P))
