@@ -72,7 +72,7 @@ def lib():
             "orc_solve": [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int,
                           C.c_int, C.c_int, C.c_int, C.c_int, C.c_ulonglong, C.c_int,
                           C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, C.c_double,
-                          C.POINTER(_SolveOut)],
+                          C.c_int, C.POINTER(_SolveOut)],
             "orc_block2_operator": [vp, C.POINTER(vp)],
             "orc_shifted_operator": [vp, C.c_double, C.POINTER(vp)],
             "orc_build_two_vector_poly": [vp, vp, vp, C.c_int, vp, vp, _ip, vp],
@@ -368,7 +368,7 @@ def read_matrix_market(path) -> Csr:
 def solve(a: Op, m, k, nev, degree=0, rtol_multiplier=1e-8, rtol_absolute=0.0, stability=False,
           double=None, max_cycles=100, seed=1, allow_nev_above_k=False, damping=0,
           damping_alpha=0.0, damping_power=1, mid_cycle_stride=0, stagnation_window=0,
-          stagnation_rtol=0.01):
+          stagnation_rtol=0.01, variant="ritz"):
     """mid_cycle_stride > 0 turns on check_mid_cycle; stagnation_window > 0
     turns on stagnation_stop (SolveConfig, inc/solver.hpp:45-52)."""
     cap_r, cap_c = 4096, max(max_cycles, 1)
@@ -387,7 +387,8 @@ def solve(a: Op, m, k, nev, degree=0, rtol_multiplier=1e-8, rtol_absolute=0.0, s
                         1 if double else 0, d1, d2, max_cycles, seed, int(allow_nev_above_k),
                         int(damping), C.c_double(damping_alpha), int(damping_power),
                         int(mid_cycle_stride), int(stagnation_window),
-                        C.c_double(stagnation_rtol), C.byref(o)))
+                        C.c_double(stagnation_rtol), 1 if variant == "harmonic" else 0,
+                        C.byref(o)))
     ne = min(o.n_eig, nev)
     return {
         "eigenvalues": er[:ne] + 1j * ei[:ne], "residuals": rs[:ne].copy(),

@@ -762,6 +762,55 @@ std::vector<cd> harmonic_ritz_values(const State& st) {
   return w;
 }
 
+// src/arnoldi.cpp:208-246: harmonic selection for restarting.  The
+// eigenpairs of H_d + h^2 f e_d^T (f = H_d^{-T} e_d), unit vectors, and the
+// exact subspace residual ||[H_d g - theta g ; h g_d]||.
+Ritz harmonic_restart_selection(const State& st, int ord) {
+  const int d = st.cur_dim;
+  if (d < 1) throw std::invalid_argument("harmonic_restart_selection: empty");
+  const Mat Hd = lead(st, d);
+  Mat M = Hd;
+  const double hsub = st.H(d, d - 1);
+  if (hsub != 0.0) {
+    Mat T(d, d);
+    for (int i = 0; i < d; ++i)
+      for (int j = 0; j < d; ++j) T(i, j) = Hd(j, i);
+    Vec f(d, 0.0);
+    f[d - 1] = 1.0;
+    if (!fullpiv_solve(T, f))
+      throw std::runtime_error(
+          "harmonic_restart_selection: singular projection; try a different starting vector");
+    for (int i = 0; i < d; ++i) M(i, d - 1) += (hsub * hsub) * f[i];
+  }
+  Ritz s;
+  s.ordering = ord;
+  s.d = d;
+  if (!eigen(M, s.values, &s.vec))
+    throw std::runtime_error("harmonic_restart_selection: eigensolver failed");
+  s.residuals.resize(d);
+  for (int i = 0; i < d; ++i) {
+    double nn = 0.0;
+    for (int r = 0; r < d; ++r) nn += std::norm(s.g(r, i));
+    nn = std::sqrt(nn);
+    for (int r = 0; r < d; ++r) s.g(r, i) /= nn;
+    double top2 = 0.0;
+    for (int r = 0; r < d; ++r) {
+      cd acc = 0.0;
+      for (int q = 0; q < d; ++q) acc += Hd(r, q) * s.g(q, i);
+      top2 += std::norm(acc - s.values[i] * s.g(r, i));
+    }
+    const cd last = hsub * s.g(d - 1, i);
+    s.residuals[i] = std::sqrt(top2 + std::norm(last));
+  }
+  sort_pairs(s);
+  return s;
+}
+
+// The solve's restart selection (SolveConfig::variant, inc/solver.hpp:31).
+Ritz select_pairs(const State& st, int ord, int variant) {
+  return variant == 1 ? harmonic_restart_selection(st, ord) : ritz_pairs(st, ord);
+}
+
 // src/arnoldi.cpp:252-265: unit Ritz vector (re, im parts).
 void ritz_vector(const State& st, const Ritz& s, int j, Vec& yr, Vec& yi, bool& cplx, Cost& c) {
   const int d = s.d;
@@ -862,6 +911,91 @@ int thick_restart(State& st, const Ritz& keep, int k, Cost& c) {
   for (int cc = 0; cc < kk; ++cc) {
     for (int r = 0; r < kk; ++r) st.H(r, cc) = Hk(r, cc);
     st.H(kk, cc) = rn * hrow[cc];
+  }
+  st.cur_dim = kk;
+  st.restart_k = kk;
+  ++st.cycle_count;
+  return kk;
+}
+
+// Harmonic thick restart (our decision for RestartVariant::harmonic,
+// DESIGN.md section 5; SPEC.md:178 asks the restart to keep the Krylov
+// property): keep span{[G; 0], p} with p = [-h f; 1], H_m^T f = e_m, the
+// direction every harmonic residual Hbar g - theta [g; 0] lies along.
+int harmonic_thick_restart(State& st, const Ritz& keep, int k, Cost& c) {
+  const int m = st.cur_dim;
+  if (m != st.max_dim) throw std::invalid_argument("thick_restart: cycle not at full dimension");
+  if (k <= 0 || k >= m) throw std::invalid_argument("thick_restart: bad k");
+  if (keep.count() < k) throw std::invalid_argument("thick_restart: selection smaller than k");
+  const double hm = st.H(m, m - 1);
+  if (hm == 0.0) throw std::runtime_error("thick_restart: no residual vector (breakdown)");
+  Mat G(m, k);
+  int col = 0, j = 0;
+  while (col < k && j < keep.count()) {
+    if (!a_is_complex(keep.values[j])) {
+      for (int r = 0; r < m; ++r) G(r, col) = keep.g(r, j).real();
+      ++col;
+      ++j;
+    } else {
+      if (col + 2 > k) break;
+      for (int r = 0; r < m; ++r) {
+        G(r, col) = keep.g(r, j).real();
+        G(r, col + 1) = keep.g(r, j).imag();
+      }
+      col += 2;
+      j += 2;
+    }
+  }
+  const int kk = col;
+  if (kk == 0) throw std::invalid_argument("thick_restart: k too small");
+  Mat T(m, m);
+  for (int r = 0; r < m; ++r)
+    for (int q = 0; q < m; ++q) T(r, q) = st.H(q, r);
+  Vec f(m, 0.0);
+  f[m - 1] = 1.0;
+  if (!fullpiv_solve(T, f))
+    throw std::runtime_error("harmonic_restart_selection: singular projection; try a different starting vector");
+  Mat P(m + 1, kk + 1);
+  for (int cc = 0; cc < kk; ++cc)
+    for (int r = 0; r < m; ++r) P(r, cc) = G(r, cc);
+  for (int r = 0; r < m; ++r) P(r, kk) = -hm * f[r];
+  P(m, kk) = 1.0;
+  const Mat Qh = thin_q(P);
+  // Hn = Qh^T Hbar Qh(0:m, 0:kk), (kk+1) x kk
+  Mat HQ(m + 1, kk), Hn(kk + 1, kk);
+  for (int cc = 0; cc < kk; ++cc)
+    for (int q = 0; q < m; ++q)
+      for (int r = 0; r <= m; ++r) HQ(r, cc) += st.H(r, q) * Qh(q, cc);
+  for (int cc = 0; cc < kk; ++cc)
+    for (int r = 0; r <= kk; ++r) {
+      double s = 0.0;
+      for (int q = 0; q <= m; ++q) s += Qh(q, r) * HQ(q, cc);
+      Hn(r, cc) = s;
+    }
+  // V(:,0:kk+1) = V(:,0:m+1) Qh
+  const long n = st.n;
+  Vec NV(static_cast<size_t>(n) * (kk + 1), 0.0);
+#pragma omp parallel for schedule(static)
+  for (long i = 0; i < n; ++i)
+    for (int cc = 0; cc <= kk; ++cc) {
+      double s = 0.0;
+      for (int q = 0; q <= m; ++q) s += st.V[static_cast<size_t>(q) * n + i] * Qh(q, cc);
+      NV[static_cast<size_t>(cc) * n + i] = s;
+    }
+  std::copy(NV.begin(), NV.end(), st.V.begin());
+  c.vops += static_cast<long long>(m + 1) * (kk + 1);
+  Vec corr(kk, 0.0);
+  for (int i = 0; i < kk; ++i) {
+    const double h = dot(st.col(i), st.col(kk), n, c);
+    corr[i] = h;
+    axpy(-h, st.col(i), st.col(kk), n, c);
+  }
+  const double rn = norm(st.col(kk), n, c);
+  scale(st.col(kk), 1.0 / rn, n, c);
+  std::fill(st.H.a.begin(), st.H.a.end(), 0.0);
+  for (int cc = 0; cc < kk; ++cc) {
+    for (int r = 0; r < kk; ++r) st.H(r, cc) = Hn(r, cc) + corr[r] * Hn(kk, cc);
+    st.H(kk, cc) = rn * Hn(kk, cc);
   }
   st.cur_dim = kk;
   st.restart_k = kk;
@@ -1126,6 +1260,7 @@ struct Config {
   double damping_alpha = 0.0;
   int damping_power = 1;
   int mid_stride = 0;  // > 0: check_mid_cycle with this stride
+  int variant = 0;  // RestartVariant: 0 ritz, 1 harmonic (inc/solver.hpp:17)
   int stag_window = 0;  // > 0: stagnation_stop over this many cycles
   double stag_rtol = 0.01;
 };
@@ -1285,7 +1420,7 @@ Result solve(const OpPtr& A, const Config& g) {
         OpPtr pop = std::make_shared<PolyOp>(A, p, false);
         State ps = arnoldi_init(rng::gauss_vec(n, g.seed, rng::ARNOLDI), g.m, c);
         arnoldi_extend(ps, *pop, g.m, c);
-        Ritz pset = ritz_pairs(ps, TARGET_ONE);
+        Ritz pset = select_pairs(ps, TARGET_ONE, g.variant);
         Result tmp;
         tmp.rtol = R.rtol;
         bool all_k;
@@ -1349,17 +1484,17 @@ Result solve(const OpPtr& A, const Config& g) {
         arnoldi_extend(st, *op, to, c);
         if (st.breakdown || st.cur_dim >= g.m) break;
         if (st.cur_dim < g.nev) continue;
-        s = ritz_pairs(st, ord);
+        s = select_pairs(st, ord, g.variant);
         check_and_record(st, s, g.nev, *A, R, all, mx, c);
         if (all) break;
       }
       if (!all) {
-        s = ritz_pairs(st, ord);
+        s = select_pairs(st, ord, g.variant);
         check_and_record(st, s, g.nev, *A, R, all, mx, c);
       }
     } else {
       arnoldi_extend(st, *op, g.m, c);
-      s = ritz_pairs(st, ord);
+      s = select_pairs(st, ord, g.variant);
       check_and_record(st, s, g.nev, *A, R, all, mx, c);
     }
     R.cycles = cyc;
@@ -1374,7 +1509,11 @@ Result solve(const OpPtr& A, const Config& g) {
       R.converged = all;
       break;
     }
-    thick_restart(st, s, g.k, c);
+    if (g.variant == 1) {
+      harmonic_thick_restart(st, s, g.k, c);
+    } else {
+      thick_restart(st, s, g.k, c);
+    }
   }
   c.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   R.cost = c;
@@ -1657,9 +1796,11 @@ struct orc_solve_out {
 int orc_solve(const orc_op* a, int m, int k, int nev, int degree, double rtol_mult, double rtol_abs,
               int stability, int use_double, int d1, int d2, int max_cycles, unsigned long long seed,
               int allow_nev_above_k, int damping, double damping_alpha, int damping_power,
-              int mid_stride, int stag_window, double stag_rtol, orc_solve_out* out) {
+              int mid_stride, int stag_window, double stag_rtol, int variant,
+              orc_solve_out* out) {
   return wrap([&] {
     orc::Config g;
+    g.variant = variant;
     g.mid_stride = mid_stride;
     g.stag_window = stag_window;
     if (stag_rtol > 0) g.stag_rtol = stag_rtol;

@@ -98,8 +98,11 @@ dense::Mat harmonic_matrix(const ArnoldiState& st, const char* who) {
     std::vector<double> ed(d, 0.0), f;
     ed[d - 1] = 1.0;
     if (!dense::solve_transpose_full_pivot(M, ed, f)) {
+      // message texts of src/arnoldi.cpp:189-192 and 217-221
+      const bool sel = std::string(who) == "harmonic_restart_selection";
       throw std::runtime_error(std::string(who) +
-                               ": singular projection (GMRES stagnation); "
+                               (sel ? ": singular projection; "
+                                    : ": singular projection (GMRES stagnation); ") +
                                "try a different starting vector");
     }
     for (int i = 0; i < d; ++i) M(i, d - 1) += (hsub * hsub) * f[i];
@@ -526,6 +529,101 @@ int thick_restart(ArnoldiState& st, const RitzSet& keep, int k, CostRecord& rec)
   for (int c = 0; c < kk; ++c) {
     for (int r = 0; r < kk; ++r) st.h(r, c) = Hk(r, c);
     st.h(kk, c) = rn * hrow[c];
+  }
+  st.cur_dim = kk;
+  st.restart_k = kk;
+  ++st.cycle_count;
+  ctx.sync();  // qdev is released on return
+  return kk;
+}
+
+// Harmonic thick restart (the solve's RestartVariant::harmonic).  The
+// reference solve would pass harmonic_restart_selection's vectors to
+// thick_restart (src/arnoldi.cpp:267-334), which keeps v_{m+1} as the
+// residual direction - correct for Ritz vectors only: for harmonic pairs
+// Hbar g - theta [g; 0] is parallel to p = [-h f; 1] (f = H^{-T} e_m), not to
+// e_{m+1}, so the compressed factorisation stops being an Arnoldi relation
+// and the iteration stalls (diag(1..1000): max residual stuck at 15.25 for
+// 300 cycles in both implementations).  SPEC.md:178 requires the Krylov
+// property to survive the restart, so the harmonic variant keeps
+// span{[G; 0], p} instead (Morgan's GMRES-DR construction): with Qh the
+// orthonormal basis of [[G; 0], p], A V_m Q = V_{m+1} Qh (Qh^T Hbar Q)
+// exactly.  Counters follow thick_restart's (basis compression, one
+// reorthogonalisation pass of the carried vector).
+int harmonic_thick_restart(ArnoldiState& st, const RitzSet& keep, int k, CostRecord& rec) {
+  const int m = st.cur_dim;
+  if (m != st.max_dim) throw std::invalid_argument("thick_restart: cycle not at full dimension");
+  if (k <= 0 || k >= m) throw std::invalid_argument("thick_restart: bad k");
+  if (keep.count() < k) throw std::invalid_argument("thick_restart: selection smaller than k");
+  const double hm = st.h(m, m - 1);
+  if (hm == 0.0) throw std::runtime_error("thick_restart: no residual vector (breakdown)");
+  dense::Mat G(m, k);
+  int col = 0, j = 0;
+  while (col < k && j < keep.count()) {
+    if (!ritz_is_complex(keep.values[j])) {
+      for (int r = 0; r < m; ++r) G(r, col) = keep.vectors_h(r, j).real();
+      ++col;
+      j += 1;
+    } else {
+      if (col + 2 > k) break;
+      for (int r = 0; r < m; ++r) {
+        G(r, col) = keep.vectors_h(r, j).real();
+        G(r, col + 1) = keep.vectors_h(r, j).imag();
+      }
+      col += 2;
+      j += 2;
+    }
+  }
+  const int kk = col;
+  if (kk == 0) throw std::invalid_argument("thick_restart: k too small");
+  // p = [-h f; 1], H_m^T f = e_m
+  const dense::Mat Hm = leading_block(st, m);
+  std::vector<double> em(m, 0.0), f;
+  em[m - 1] = 1.0;
+  if (!dense::solve_transpose_full_pivot(Hm, em, f)) {
+    throw std::runtime_error("harmonic_restart_selection: singular projection; "
+                             "try a different starting vector");
+  }
+  dense::Mat P(m + 1, kk + 1);
+  for (int c = 0; c < kk; ++c)
+    for (int r = 0; r < m; ++r) P(r, c) = G(r, c);
+  for (int r = 0; r < m; ++r) P(r, kk) = -hm * f[r];
+  P(m, kk) = 1.0;
+  const dense::Mat Qh = dense::householder_q(P);  // (m+1) x (kk+1)
+  dense::Mat Hbar(m + 1, m);
+  for (int c = 0; c < m; ++c)
+    for (int r = 0; r <= m; ++r) Hbar(r, c) = st.h(r, c);
+  dense::Mat Qm(m, kk);
+  for (int c = 0; c < kk; ++c)
+    for (int r = 0; r < m; ++r) Qm(r, c) = Qh(r, c);
+  const dense::Mat Hn = dense::matmul_tn(Qh, dense::matmul(Hbar, Qm));  // (kk+1) x kk
+
+  Context& ctx = current_context();
+  const cudaStream_t s = ctx.stream();
+  Scratch qdev(Qh.a.size());
+  PPA_CUDA(cudaMemcpyAsync(qdev.get(), Qh.a.data(), Qh.a.size() * sizeof(double),
+                           cudaMemcpyHostToDevice, s));
+  kern::ts_combine(st.V.get(), st.ld, st.n, m + 1, qdev.get(), kk + 1, st.V.get(), st.ld, s);
+  rec.vops += static_cast<long long>(m + 1) * (kk + 1);
+
+  // one reorthogonalisation pass of the new column kk; corrections folded
+  // into H as in thick_restart (v = rn v_new + V_k c)
+  double* dres = ctx.results();
+  Scratch corr(static_cast<size_t>(kk) + 1);
+  kern::cgs1_pass(st.V.get(), st.ld, st.n, kk, st.col(kk), corr.get(), dres, ctx.ws(),
+                  ctx.sm_count(), s);
+  double* h = ctx.pinned(static_cast<size_t>(kk) + 1);
+  PPA_CUDA(cudaMemcpyAsync(h, corr.get(), kk * sizeof(double), cudaMemcpyDeviceToHost, s));
+  PPA_CUDA(cudaMemcpyAsync(h + kk, dres, sizeof(double), cudaMemcpyDeviceToHost, s));
+  ctx.sync();
+  const double rn = h[kk];
+  rec.dots += kk + 1;
+  rec.vops += 2LL * kk + 2;
+  kern::scale(st.col(kk), 1.0 / rn, st.n, s);
+  std::fill(st.H.begin(), st.H.end(), 0.0);
+  for (int c = 0; c < kk; ++c) {
+    for (int r = 0; r < kk; ++r) st.h(r, c) = Hn(r, c) + h[r] * Hn(kk, c);
+    st.h(kk, c) = rn * Hn(kk, c);
   }
   st.cur_dim = kk;
   st.restart_k = kk;

@@ -70,6 +70,10 @@ DeviceComplexVector ritz_vector(const ArnoldiState& state, const RitzSet& set, i
 
 /// src/arnoldi.cpp:267-334; V(:,0:kk) = V(:,0:m) Q runs in place on the device.
 int thick_restart(ArnoldiState& state, const RitzSet& keep, int k, CostRecord& rec);
+/// Thick restart for harmonic keep-sets (the solve's harmonic variant): keeps
+/// span{harmonic vectors, harmonic residual direction} so the compressed
+/// factorisation stays an Arnoldi relation (arnoldi.cpp).
+int harmonic_thick_restart(ArnoldiState& state, const RitzSet& keep, int k, CostRecord& rec);
 
 /// Ritz-value classification used by sort_pairs / thick_restart
 /// (src/arnoldi.cpp:18-25).

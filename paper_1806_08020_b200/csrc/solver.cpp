@@ -428,7 +428,8 @@ void run_cycles(const LinearOperator& a, const LinearOperator& op, const SolveCo
       break;
     }
     t0 = Clock::now();
-    cs.restart_k = thick_restart(st, set, cfg.k, rec);
+    cs.restart_k = set.harmonic ? harmonic_thick_restart(st, set, cfg.k, rec)
+                                : thick_restart(st, set, cfg.k, rec);
     res.timing.restart += seconds_since(t0);
     res.history.push_back(cs);
   }

@@ -96,3 +96,28 @@ def test_eigenvectors_output(cuda):
     # eigenvectors are off unless requested
     r2 = ppa.solve(A, ppa.SolveConfig(m=40, k=20, nev=8, degree=8, seed=2, max_cycles=60))
     assert "eigenvectors" not in r2
+
+
+def test_harmonic_variant_matches_oracle(cuda):
+    # SolveConfig::variant = harmonic: restart selection from the harmonic
+    # Ritz pairs (src/arnoldi.cpp:208-246) on the device path and the oracle
+    d = np.arange(1.0, 1001.0)
+    cfg = ppa.SolveConfig(m=40, k=20, nev=10, degree=0, seed=3, max_cycles=300,
+                          variant="harmonic")
+    r = ppa.solve(ppa.make_diagonal(d), cfg)
+    o = O.solve(O.diagonal_operator(d), 40, 20, 10, degree=0, seed=3, max_cycles=300,
+                variant="harmonic")
+    assert r["converged"] and o["converged"]
+    assert np.allclose(np.sort(r["eigenvalues"].real), np.arange(1.0, 11.0), rtol=1e-8)
+    assert abs(r["cost"]["mvps"] - o["cost"]["mvps"]) <= 0.05 * o["cost"]["mvps"]
+    # and with a polynomial on a nonsymmetric matrix
+    P = ppa.CsrMatrix.convection_diffusion(40)
+    cfg = ppa.SolveConfig(m=40, k=20, nev=8, degree=12, seed=5, max_cycles=60,
+                          variant="harmonic")
+    r = ppa.solve(ppa.make_csr_operator(P), cfg)
+    o = O.solve(O.csr_operator(O.Csr.convection_diffusion(40)), 40, 20, 8, degree=12, seed=5,
+                max_cycles=60, variant="harmonic")
+    assert r["converged"] and o["converged"]
+    got, ref = np.sort_complex(r["eigenvalues"]), np.sort_complex(o["eigenvalues"])
+    assert np.max(np.abs(got - ref) / np.abs(ref)) < 1e-8
+    assert abs(r["cost"]["mvps"] - o["cost"]["mvps"]) <= 0.05 * o["cost"]["mvps"]

@@ -345,3 +345,15 @@ def test_oracle_mid_cycle_and_stagnation():
     best = np.minimum.accumulate(stag["cycle_max_residual"])
     assert stag["cycles"] < 200 and best[-1] > 0.99 * best[-4]
     assert np.all(best[3:-1] <= 0.99 * best[:-4])
+
+
+def test_oracle_harmonic_variant_solve():
+    # RestartVariant::harmonic (inc/solver.hpp:17, src/arnoldi.cpp:208-246):
+    # restarts on harmonic Ritz vectors; same smallest eigenvalues
+    A = O.diagonal_operator(np.arange(1.0, 1001.0))
+    r = O.solve(A, 40, 20, 10, degree=0, seed=3, max_cycles=300, variant="harmonic")
+    p = O.solve(A, 40, 20, 10, degree=0, seed=3, max_cycles=300)
+    assert r["converged"] and p["converged"]
+    assert np.allclose(np.sort(r["eigenvalues"].real), np.arange(1.0, 11.0), rtol=1e-8)
+    assert r["cycles"] != p["cycles"] or r["cost"]["mvps"] != p["cost"]["mvps"] or \
+        not np.array_equal(r["eigenvalues"], p["eigenvalues"])
