@@ -83,6 +83,9 @@ int ppa_host_csr_info(const ppa_host_csr* m, int* n, long long* nnz,
 int ppa_host_csr_arrays(const ppa_host_csr* m, const int** row_ptr, const int** col_idx,
                         const double** values);
 void ppa_host_csr_free(ppa_host_csr* m);
+/* CsrMatrix::multiply (inc/operators.hpp:27-28): y = A x, uncounted, device
+   vectors (a device copy of the matrix is built per call) */
+int ppa_host_csr_multiply(const ppa_host_csr* m, const double* x_dev, double* y_dev);
 /* Seeded N(0,1) vector (host), stream ids as in DESIGN.md */
 int ppa_normal_vector(long long n, unsigned long long seed, unsigned long long stream,
                       double* out);

@@ -115,6 +115,7 @@ def lib():
             "ppa_op_apply_host_batch": [vp, C.c_int, vp, vp, C.POINTER(CostRecord)],
             "ppa_csr_model_bytes": [vp, _dp, C.POINTER(C.c_longlong)],
             "ppa_csr_layout": [vp, _ip, _dp, _ip, _ip],
+            "ppa_host_csr_multiply": [vp, vp, vp],
             "ppa_csr_operator_layout": [vp, C.c_int, C.POINTER(vp)],
             "ppa_arnoldi_set_orthogonalization": [vp, C.c_int],
             "ppa_apply_poly": [vp, vp, C.c_int, vp, vp, vp, C.POINTER(CostRecord)],
@@ -281,6 +282,10 @@ class CsrMatrix:
 
     def fingerprint(self) -> int:
         return self.info()[2]
+
+    def multiply(self, x, y) -> None:
+        """CsrMatrix::multiply: y = A x on device vectors, uncounted."""
+        _check(lib().ppa_host_csr_multiply(self._h, _ptr(x), _ptr(y)))
 
     def arrays(self):
         """Copies of (row_ptr, col_idx, values)."""

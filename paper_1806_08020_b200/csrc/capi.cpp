@@ -249,6 +249,15 @@ int ppa_normal_vector(long long n, unsigned long long seed, unsigned long long s
   });
 }
 
+int ppa_host_csr_multiply(const ppa_host_csr* m, const double* x, double* y) {
+  return guard([&] {
+    need(m, "ppa_host_csr_multiply");
+    need(x, "ppa_host_csr_multiply");
+    need(y, "ppa_host_csr_multiply");
+    m->m.multiply(x, y);
+  });
+}
+
 int ppa_csr_operator_layout(const ppa_host_csr* m, int layout, ppa_op** out) {
   return guard([&] {
     need(m, "ppa_csr_operator_layout");

@@ -70,6 +70,13 @@ CsrMatrix CsrMatrix::from_triplets(int n, std::vector<std::tuple<int, int, doubl
   return m;
 }
 
+bool SpectrumSpec::real_only(double tol) const {
+  for (const auto& z : eigenvalues) {
+    if (std::abs(z.imag()) > tol) return false;
+  }
+  return true;
+}
+
 // ------------------------------------------------------------ operator --
 
 CsrOperator::CsrOperator(const CsrMatrix& m, OperatorKind kind, std::vector<double> diag,
@@ -264,6 +271,13 @@ void CsrOperator::apply(const double* x, double* y, CostRecord& rec) const {
   if (x == y) throw std::invalid_argument("CsrOperator::apply: x and y alias");
   ++rec.mvps;
   kern::spmv(dev_, x, y, kern::EpiArgs{}, current_context().stream());
+}
+
+void CsrMatrix::multiply(const double* x_dev, double* y_dev) const {
+  const CsrOperator op(*this, OperatorKind::csr, {}, CsrLayout::csr);
+  CostRecord scratch;  // uncounted
+  op.apply(x_dev, y_dev, scratch);
+  current_context().sync();
 }
 
 OperatorPtr make_csr_operator(const CsrMatrix& matrix, CsrLayout layout) {

@@ -5,6 +5,7 @@
 // device pointers of length dim() instead of Eigen::Ref<VectorXd> (SURVEY
 // §8b "Constraint": host vectors would force a 32 MB H2D/D2H per apply).
 
+#include <complex>
 #include <memory>
 #include <string>
 #include <tuple>
@@ -35,6 +36,21 @@ struct CsrMatrix {
   /// (src/operators.cpp:50-78; the sort is stable here so duplicate sums
   /// are deterministic).
   static CsrMatrix from_triplets(int n, std::vector<std::tuple<int, int, double>> t);
+
+  /// y = A x, uncounted (inc/operators.hpp:27-28); device vectors.  Builds a
+  /// device copy of the matrix per call - use CsrOperator for repeated,
+  /// counted applies.
+  void multiply(const double* x_dev, double* y_dev) const;
+};
+
+/// Known eigenvalue list of a test matrix, conjugate-closed
+/// (inc/operators.hpp:35-41).
+struct SpectrumSpec {
+  std::vector<std::complex<double>> eigenvalues;
+
+  int dim() const { return static_cast<int>(eigenvalues.size()); }
+  /// True when every eigenvalue has |Im| <= tol (src/operators.cpp:80-85).
+  bool real_only(double tol = 0.0) const;
 };
 
 enum class OperatorKind { csr, diagonal, shifted, block2, poly, composite };

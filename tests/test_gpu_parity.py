@@ -235,6 +235,15 @@ def test_packed_fp64_values_and_perm(cuda):
     assert np.array_equal(host(out), O.apply_poly(roots, O.csr_operator(Q), x))
 
 
+def test_csr_matrix_multiply_uncounted(cuda):
+    # CsrMatrix::multiply (inc/operators.hpp:27-28): plain y = A x
+    P, Q = ppa.CsrMatrix.convection_diffusion(33), O.Csr.convection_diffusion(33)
+    x = O.normal_vector(P.n, 1, 2)
+    y = cuda.empty(P.n, dtype=cuda.float64, device="cuda")
+    P.multiply(dev(cuda, x), y)
+    assert np.array_equal(host(y), O.csr_operator(Q).apply(x))
+
+
 def test_spmv_long_rows(cuda):
     # rows longer than one row block (2048 nnz) take the block-reduction path
     n = 6000
