@@ -183,6 +183,7 @@ def _edge_matrices():
         cols += [i - 1, i]
         vals += [-1.0, 2.0]
     out["tail_empty"] = (n, rows, cols, vals)
+    out["all_empty"] = (40, [], [], [])  # nnz = 0: y = 0 (or the epilogue of 0)
     return out
 
 
@@ -204,6 +205,17 @@ def test_edge_matrices_every_layout(cuda, cap, name):
     out = cuda.empty(n, dtype=cuda.float64, device="cuda")
     ppa.apply_poly(roots, A, dev(cuda, x), out)
     assert np.array_equal(host(out), O.apply_poly(roots, O.csr_operator(Q), x))
+
+
+def test_empty_dimension_operator(cuda):
+    # n = 0 is a valid CsrMatrix (src/operators.cpp:12-37): a no-op operator
+    P = ppa.CsrMatrix.from_arrays(0, [0], [], [])
+    A = ppa.make_csr_operator(P)
+    assert A.dim() == 0
+    x = cuda.empty(1, dtype=cuda.float64, device="cuda")
+    y = cuda.empty(1, dtype=cuda.float64, device="cuda")
+    rec = A.apply(x, y)
+    assert rec.mvps == 1
 
 
 def test_packed_fp64_values_and_perm(cuda):
