@@ -510,6 +510,24 @@ def _read_V(torch, st, n, cols):
     return host(buf).reshape(cols, ld)[:, :n].T.copy()
 
 
+def test_arnoldi_m100(cuda, ortho):
+    # the largest basis the north star keeps on the host side (m <= 100):
+    # widest TMA tiles (c up to 100) in every CGS kernel
+    P = ppa.CsrMatrix.convection_diffusion(45)
+    n = P.n
+    A = ppa.make_csr_operator(P)
+    m = 100
+    rec = ppa.CostRecord()
+    st = ppa.arnoldi_init(dev(cuda, O.normal_vector(n, 9, 3)), n, m, rec)
+    st.set_orthogonalization(ortho)
+    st.extend(A, m, rec)
+    assert st.cur_dim == m and not st.breakdown
+    Vh = _read_V(cuda, st, n, m + 1)
+    assert np.linalg.norm(Vh.T @ Vh - np.eye(m + 1)) <= 1e-10
+    R = _dense(P) @ Vh[:, :m] - Vh @ st.H
+    assert np.linalg.norm(R) <= 1e-9 * max(1.0, np.linalg.norm(st.H))
+
+
 def test_breakdown_diag_e1(cuda, ortho):
     # diag[1..6] with e1 breaks down at dimension 1
     A = ppa.make_diagonal(np.arange(1.0, 7.0))
