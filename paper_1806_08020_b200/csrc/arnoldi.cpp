@@ -156,7 +156,7 @@ void extend_cgs2(ArnoldiState& st, const LinearOperator& op, int to_dim, CostRec
   Scratch hdev(slot);
   double* Hcol = hdev.get();
   int* flag = reinterpret_cast<int*>(hdev.get() + st.max_dim + 2);
-  double* host = ctx.pinned(2 * slot);
+  double* host = ctx.pinned_aux(2 * slot);
   cudaEvent_t ev[2];
   PPA_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
   PPA_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
@@ -254,7 +254,7 @@ void extend_dcgs2(ArnoldiState& st, const LinearOperator& op, int to_dim, CostRe
   Scratch dbuf(static_cast<size_t>(4 * M + 8));
   double* dout = dbuf.get();               // 2c reductions (or c + norm)
   double* dcoef = dbuf.get() + 2 * M + 4;  // 2j + 2 coefficients
-  double* host = ctx.pinned(static_cast<size_t>(4 * M + 8));
+  double* host = ctx.pinned_aux(static_cast<size_t>(4 * M + 8));
   double* hout = host;
   double* hcoef = host + 2 * M + 4;
   double* V = st.V.get();

@@ -109,6 +109,10 @@ class Context {
 
   /// Pinned host staging for small device->host reads.
   double* pinned(size_t count);
+  /// A second pinned area, owned by arnoldi_extend's in-flight Hessenberg
+  /// columns, so an operator that uses pinned() inside apply() cannot
+  /// clobber them.
+  double* pinned_aux(size_t count);
 
   /// Small synchronous helpers (device reduction + read-back).
   double nrm2_sync(const double* x, long long n);
@@ -122,6 +126,8 @@ class Context {
   int sm_count_ = 148;
   double* pinned_ = nullptr;
   size_t pinned_count_ = 0;
+  double* pinned_aux_ = nullptr;
+  size_t pinned_aux_count_ = 0;
   DBuffer<double> results_;
   MpWork mp_;
 

@@ -25,6 +25,7 @@ Context::Context(cudaStream_t s) : stream_(s) {
 
 Context::~Context() {
   if (pinned_) cudaFreeHost(pinned_);
+  if (pinned_aux_) cudaFreeHost(pinned_aux_);
 }
 
 void Context::sync() const { PPA_CUDA(cudaStreamSynchronize(stream_)); }
@@ -51,6 +52,20 @@ double* Context::pinned(size_t count) {
     pinned_count_ = c;
   }
   return pinned_;
+}
+
+double* Context::pinned_aux(size_t count) {
+  if (count > pinned_aux_count_) {
+    if (pinned_aux_) {
+      PPA_CUDA(cudaStreamSynchronize(stream_));
+      cudaFreeHost(pinned_aux_);
+      pinned_aux_ = nullptr;
+    }
+    const size_t c = count < 4096 ? 4096 : count;
+    PPA_CUDA(cudaMallocHost(&pinned_aux_, c * sizeof(double)));
+    pinned_aux_count_ = c;
+  }
+  return pinned_aux_;
 }
 
 double* Context::results() { return results_.get(); }
