@@ -411,12 +411,14 @@ void launch_pipe(PipeArgs a, ReduceWorkspace& ws, int sm_count, cudaStream_t st)
     stages = static_cast<int>(std::max<size_t>(2, std::min<size_t>(6, budget / stage_bytes)));
   }
   const size_t smem = 128 + stage_bytes * stages;
-  static size_t configured = 0;
-  if (smem > configured) {
+  // raise the dynamic shared-memory cap once per instantiation (thread-safe
+  // static initialisation; the launch's own size sets the occupancy)
+  static const bool capped = [] {
     PPA_CUDA(cudaFuncSetAttribute(k_tspipe<MODE, CPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(std::max<size_t>(smem, 48 * 1024))));
-    configured = std::max<size_t>(smem, 48 * 1024);
-  }
+                                  max_dynamic_smem(k_tspipe<MODE, CPW>)));
+    return true;
+  }();
+  (void)capped;
   {
     // never more CTAs than can be resident: the kernel is persistent
     int fit = 0;

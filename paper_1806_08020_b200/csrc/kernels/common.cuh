@@ -7,6 +7,24 @@
 #include <cstdint>
 
 namespace ppa {
+namespace kern {
+
+/// Largest dynamic shared memory a launch of `kernel` may request: the
+/// device's opt-in per-block limit minus the kernel's static shared memory.
+template <typename K>
+inline int max_dynamic_smem(K kernel) {
+  int dev = 0, optin = 0;
+  cudaFuncAttributes fa{};
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
+      cudaFuncGetAttributes(&fa, kernel) != cudaSuccess) {
+    return 48 * 1024;
+  }
+  return optin - static_cast<int>(fa.sharedSizeBytes);
+}
+
+}  // namespace kern
+
 namespace dev {
 
 constexpr unsigned kFull = 0xffffffffu;

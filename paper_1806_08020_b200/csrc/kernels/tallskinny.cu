@@ -288,12 +288,12 @@ void ts_combine(const double* V, long long ldv, int n, int d, const double* G, i
   if (Out == V && p > d) throw std::invalid_argument("ts_combine: in-place needs p <= d");
   const size_t smem = (static_cast<size_t>(d) * kCombineRows + static_cast<size_t>(d) * p) *
                       sizeof(double);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
+  static const bool capped = [] {  // once, thread-safe
     PPA_CUDA(cudaFuncSetAttribute(k_ts_combine, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(std::min<size_t>(smem, 227 * 1024))));
-    configured = smem;
-  }
+                                  max_dynamic_smem(k_ts_combine)));
+    return true;
+  }();
+  (void)capped;
   if (smem > 227 * 1024) throw std::invalid_argument("ts_combine: d*p too large");
   k_ts_combine<<<ceil_div(n, kCombineRows), kCombineRows, smem, st>>>(V, ldv, n, d, G, p, Out,
                                                                       ldo);

@@ -121,3 +121,32 @@ def test_harmonic_variant_matches_oracle(cuda):
     got, ref = np.sort_complex(r["eigenvalues"]), np.sort_complex(o["eigenvalues"])
     assert np.max(np.abs(got - ref) / np.abs(ref)) < 1e-8
     assert abs(r["cost"]["mvps"] - o["cost"]["mvps"]) <= 0.05 * o["cost"]["mvps"]
+
+
+def test_concurrent_solves_two_threads(cuda):
+    # one context (stream, workspaces, pinned staging) per host thread: two
+    # threads solving at once on their own streams get exactly the results of
+    # the sequential solves (SPEC.md: concurrent solves need independent
+    # CostRecords; operators are reentrant)
+    import threading
+
+    P = ppa.CsrMatrix.convection_diffusion(36)
+    A = ppa.make_csr_operator(P)
+    cfgs = [ppa.SolveConfig(m=30, k=15, nev=6, degree=8, seed=s, max_cycles=80) for s in (1, 2)]
+    seq = [ppa.solve(A, c) for c in cfgs]
+    out = [None, None]
+
+    def run(i):
+        s = cuda.cuda.Stream()
+        ppa.set_stream(s)
+        out[i] = ppa.solve(A, cfgs[i])
+        s.synchronize()
+
+    th = [threading.Thread(target=run, args=(i,)) for i in (0, 1)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for a, b in zip(out, seq):
+        assert np.array_equal(a["eigenvalues"], b["eigenvalues"])
+        assert a["cost"]["mvps"] == b["cost"]["mvps"] and a["cycles"] == b["cycles"]
