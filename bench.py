@@ -422,6 +422,57 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+def run_sharded(args):
+    """Strong scaling of config-3 pi(A)v over row blocks (dist.py): every rank
+    owns n/N rows and exchanges halos per SpMV.  Not the driver's contract
+    (that is the replica run above); for maintainers with several GPUs."""
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(ws))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1806_08020_b200 as ppa
+    from paper_1806_08020_b200.dist import CudaBackend, HaloPlan, ShardedPoly
+
+    stream = torch.cuda.current_stream()
+    ppa.set_stream(stream)
+    csr = ppa.CsrMatrix.config(3)
+    n, nnz, _ = csr.info()
+    bspmv = 12.0 * nnz + 4.0 * (n + 1) + 16.0 * n
+    roots = load_golden_poly()
+    plan = HaloPlan.build(*csr.arrays(), n, dist)
+    sp = ShardedPoly(plan, CudaBackend(plan), dist)
+    r0, r1 = plan.ranges[rank]
+    v = torch.tensor(ppa.normal_vector(n, 2, ppa.STREAM_ARNOLDI)[r0:r1], device="cuda")
+    for _ in range(max(args.warmup, 3)):
+        sp.apply(roots, v)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        sp.apply(roots, v)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = reduce_max(e0.elapsed_time(e1), ws, "cuda") / args.steps
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC + " (row-block sharded)", "value": round(len(roots) * bspmv / (ms * 1e-3) / 1e9, 3),
+            "unit": "GB/s", "n_gpus": ws, "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+            "dtype": "f64", "data": "synthetic (seeded generator; BASELINE config 3)",
+            "config": {"workload": "config3-laplace3d-160^3-pi(A)v", "parallelism": f"rowblock{ws}",
+                       "halo_rows_per_rank": plan.n_left + plan.n_right},
+        }), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -430,9 +481,13 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="strong-scaling row-block sharded pi(A)v (dist.py) instead of replicas")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.sharded:
+        run_sharded(args)
     else:
         run_b200(args)
 

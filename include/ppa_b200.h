@@ -168,6 +168,17 @@ void ppa_arnoldi_free(ppa_arnoldi* st);
 /* ---- raw device kernels -------------------------------------------------- */
 /* y = A x with a CSR operator (src/operators.cpp:39-48) */
 int ppa_spmv(const ppa_op* a, const double* x_dev, double* y_dev);
+/* One fused polynomial factor (the epilogues of apply_poly,
+   src/gmres_poly.cpp:129-143, 306-308): mode 0 y = Ax, 1 y = x + c0 Ax,
+   2 y = (o + c1 x) + c0 Ax; base != NULL then y = base - y.  The building
+   block of the row-sharded pi(A)v (paper_1806_08020_b200/dist.py). */
+int ppa_spmv_factor(const ppa_op* a, const double* x_dev, double* y_dev, int mode, double c0,
+                    double c1, const double* o_dev, const double* base_dev);
+/* apply_poly's factor plan (src/gmres_poly.cpp:126-143): per factor pair flag
+   and coefficients (real root: c0 = -1/Re theta; pair: c0 = 1/|theta|^2,
+   c1 = -2 Re theta/|theta|^2); capacity >= nroots */
+int ppa_factor_plan(const double* re, const double* im, int nroots, int* pair, double* c0,
+                    double* c1, int* nfactors);
 /* AY = A Y for p column-major device vectors (multi-RHS SELL SpMM; each column
    bit-identical to ppa_spmv); the solver's batched convergence check */
 int ppa_spmm(const ppa_op* a, const double* Y_dev, long long ldy, int p, double* AY_dev,

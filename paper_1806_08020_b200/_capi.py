@@ -115,6 +115,8 @@ def lib():
             "ppa_op_apply_host_batch": [vp, C.c_int, vp, vp, C.POINTER(CostRecord)],
             "ppa_csr_model_bytes": [vp, _dp, C.POINTER(C.c_longlong)],
             "ppa_csr_layout": [vp, _ip, _dp, _ip, _ip],
+            "ppa_spmv_factor": [vp, vp, vp, C.c_int, C.c_double, C.c_double, vp, vp],
+            "ppa_factor_plan": [vp, vp, C.c_int, _ip, vp, vp, _ip],
             "ppa_host_csr_multiply": [vp, vp, vp],
             "ppa_csr_operator_layout": [vp, C.c_int, C.POINTER(vp)],
             "ppa_arnoldi_set_orthogonalization": [vp, C.c_int],
@@ -418,6 +420,27 @@ def make_poly_complement_operator(a: LinearOperator, roots, base_degree=None) ->
 
 def spmv(a: LinearOperator, x, y) -> None:
     _check(lib().ppa_spmv(a._h, _ptr(x), _ptr(y)))
+
+
+def spmv_factor(a: LinearOperator, x, y, mode: int = 0, c0: float = 0.0, c1: float = 0.0,
+                o=None, base=None) -> None:
+    """One fused polynomial factor on device vectors (ppa_spmv_factor)."""
+    _check(lib().ppa_spmv_factor(a._h, _ptr(x), _ptr(y), int(mode), C.c_double(c0),
+                                 C.c_double(c1), _ptr(o) if o is not None else None,
+                                 _ptr(base) if base is not None else None))
+
+
+def factor_plan(roots):
+    """apply_poly's factor plan: list of (pair, c0, c1) (ppa_factor_plan)."""
+    r = np.ascontiguousarray(np.real(roots), dtype=np.float64)
+    i = np.ascontiguousarray(np.imag(roots), dtype=np.float64)
+    k = len(r)
+    pair = np.zeros(max(k, 1), dtype=np.int32)
+    c0, c1 = np.zeros(max(k, 1)), np.zeros(max(k, 1))
+    nf = C.c_int()
+    _check(lib().ppa_factor_plan(_np_ptr(r), _np_ptr(i), k, pair.ctypes.data_as(_ip),
+                                 _np_ptr(c0), _np_ptr(c1), C.byref(nf)))
+    return [(bool(pair[j]), float(c0[j]), float(c1[j])) for j in range(nf.value)]
 
 
 def spmm(a: LinearOperator, Y, ldy: int, p: int, AY, ldo: int) -> None:

@@ -645,6 +645,39 @@ int ppa_spmv(const ppa_op* a, const double* x, double* y) {
   });
 }
 
+int ppa_spmv_factor(const ppa_op* a, const double* x, double* y, int mode, double c0, double c1,
+                    const double* o, const double* base) {
+  return guard([&] {
+    need(a, "ppa_spmv_factor");
+    const auto* c = dynamic_cast<const ppa::CsrOperator*>(a->p.get());
+    if (!c) throw std::invalid_argument("ppa_spmv_factor: not a CSR operator");
+    if (mode < 0 || mode > 2) throw std::invalid_argument("ppa_spmv_factor: mode");
+    if (mode == 2 && !o) throw std::invalid_argument("ppa_spmv_factor: pair needs o");
+    if (x == y) throw std::invalid_argument("ppa_spmv_factor: x and y alias");
+    ppa::kern::EpiArgs ep;
+    ep.mode = static_cast<ppa::kern::Epi>(mode);
+    ep.c0 = c0;
+    ep.c1 = c1;
+    ep.o = o;
+    ep.base = base;
+    ppa::kern::spmv(c->device(), x, y, ep, ppa::current_context().stream());
+  });
+}
+
+int ppa_factor_plan(const double* re, const double* im, int nroots, int* pair, double* c0,
+                    double* c1, int* nfactors) {
+  return guard([&] {
+    need(nfactors, "ppa_factor_plan");
+    const std::vector<ppa::PolyFactor> plan = ppa::factor_plan(poly_of(re, im, nroots, nroots));
+    for (size_t i = 0; i < plan.size(); ++i) {
+      if (pair) pair[i] = plan[i].pair ? 1 : 0;
+      if (c0) c0[i] = plan[i].c0;
+      if (c1) c1[i] = plan[i].c1;
+    }
+    *nfactors = static_cast<int>(plan.size());
+  });
+}
+
 int ppa_spmm(const ppa_op* a, const double* Y, long long ldy, int p, double* AY, long long ldo) {
   return guard([&] {
     need(a, "ppa_spmm");

@@ -1,0 +1,171 @@
+"""Row-block sharded pi(A)v (paper_1806_08020_b200/dist.py): the halo plan and
+exchange logic on CPU over gloo with world sizes 2 and 3, the local arithmetic
+supplied by an oracle-backed test backend; and the product CUDA backend at
+world size 1 on the GPU.  Every owned row is summed in the CSR's column order,
+so the sharded result must equal the unsharded oracle pi(A)v bit for bit."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CASES = {
+    "laplace3d": lambda O: O.Csr.laplacian_3d(11),
+    "convdiff": lambda O: O.Csr.convection_diffusion(25),
+    "random": lambda O: O.Csr.random_poisson(1500, 6.0, 9),
+    "bidiag": lambda O: O.Csr.bidiagonal(701),
+}
+
+
+def _roots(O):
+    return O.leja_order([3.0, 900.0, 450.0 + 120.0j, 450.0 - 120.0j, 75.0])
+
+
+class OracleBackend:
+    """Test-only CPU backend: torch CPU vectors, the oracle's CSR loop for the
+    products and numpy for the (FMA-free) factor epilogues."""
+
+    def __init__(self, plan, O):
+        m = O.Csr.from_arrays(plan.n_ext, plan.row_ptr, plan.col_idx, plan.values)
+        self.op = O.csr_operator(m)
+
+    def empty(self, n):
+        return torch.empty(n, dtype=torch.float64)
+
+    def zeros(self, n):
+        return torch.zeros(n, dtype=torch.float64)
+
+    def gather(self, t, idx):
+        return t[torch.as_tensor(idx)].contiguous()
+
+    def copy_(self, dst, src):
+        dst.copy_(src)
+
+    def factor(self, x, y, mode, c0=0.0, c1=0.0, o=None):
+        xs = x.numpy()
+        s = self.op.apply(xs)
+        if mode == 0:
+            z = s
+        elif mode == 1:
+            z = xs + c0 * s
+        else:
+            z = (o.numpy() + c1 * xs) + c0 * s
+        y.copy_(torch.from_numpy(z))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, ws, port, case, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(ws))
+    import torch.distributed as dist
+
+    from oracle import oracle as O
+    from paper_1806_08020_b200.dist import HaloPlan, ShardedPoly
+
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    try:
+        O.set_threads(1)
+        P = CASES[case](O)
+        n = P.info()[0]
+        rp, ci, va = P.arrays()
+        plan = HaloPlan.build(rp, ci, va, n, dist)
+        sp = ShardedPoly(plan, OracleBackend(plan, O), dist)
+        v = O.normal_vector(n, 3, 3)
+        r0, r1 = plan.ranges[rank]
+        out = sp.apply(_roots(O), torch.tensor(v[r0:r1]))
+        q.put((rank, r0, r1, out.numpy().copy(), sorted(plan.send), sorted(plan.recv)))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ws", [2, 3])
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_sharded_pi_gloo(ws, case):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    from oracle import oracle as O
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, ws, port, case, q)) for r in range(ws)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=180) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    P = CASES[case](O)
+    n = P.info()[0]
+    ref = O.apply_poly(_roots(O), O.csr_operator(P), O.normal_vector(n, 3, 3))
+    got = np.zeros(n)
+    for rank, r0, r1, out, send, recv in res:
+        got[r0:r1] = out
+    assert np.array_equal(got, ref)
+    if case in ("laplace3d", "convdiff", "bidiag"):  # banded: neighbours only
+        for rank, r0, r1, out, send, recv in res:
+            assert set(send) <= {rank - 1, rank + 1} and set(recv) <= {rank - 1, rank + 1}
+
+
+def test_partition_and_local_part():
+    import sys
+
+    sys.path.insert(0, ROOT)
+    from oracle import oracle as O
+    from paper_1806_08020_b200.dist import HaloPlan, partition_rows
+
+    assert partition_rows(10, 3) == [(0, 4), (4, 7), (7, 10)]
+    assert partition_rows(2, 4) == [(0, 1), (1, 2), (2, 2), (2, 2)]
+    P = O.Csr.laplacian_3d(6)
+    rp, ci, va = P.arrays()
+    ranges = partition_rows(216, 3)
+    nl, nloc, nr, lrp, lci, vals, recv, wants = HaloPlan.local_part(rp, ci, va, ranges, 1)
+    assert nloc == 72 and nl == 36 and nr == 36  # one 6x6 plane each side
+    # monotone renumbering: local columns increase along every owned row
+    for i in range(nl, nl + nloc):
+        row = lci[lrp[i]:lrp[i + 1]]
+        assert np.all(np.diff(row) > 0)
+    assert recv == {0: (0, 36), 2: (nl + nloc, nl + nloc + 36)}
+    assert wants[0] == list(range(36, 72)) and wants[2] == list(range(144, 180))
+
+
+@pytest.mark.gpu
+def test_sharded_cuda_backend_ws1(cuda):
+    # the product backend at world size 1 (no halo): the sharded driver and
+    # ppa_spmv_factor reproduce apply_poly bit for bit
+    import torch.distributed as dist
+
+    import paper_1806_08020_b200 as ppa
+    from oracle import oracle as O
+    from paper_1806_08020_b200.dist import CudaBackend, HaloPlan, ShardedPoly
+
+    if not dist.is_initialized():
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()), RANK="0",
+                          WORLD_SIZE="1")
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        P = ppa.CsrMatrix.laplacian_3d(14)
+        n = P.n
+        rp, ci, va = P.arrays()
+        plan = HaloPlan.build(rp, ci, va, n, dist)
+        sp = ShardedPoly(plan, CudaBackend(plan), dist)
+        v = O.normal_vector(n, 3, 3)
+        out = sp.apply(_roots(O), torch.tensor(v, device="cuda"))
+        ref = O.apply_poly(_roots(O), O.csr_operator(O.Csr.laplacian_3d(14)), v)
+        assert np.array_equal(out.cpu().numpy(), ref)
+    finally:
+        dist.destroy_process_group()
