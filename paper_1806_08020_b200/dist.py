@@ -225,3 +225,223 @@ class ShardedPoly:
                 self.b.factor(t1, nxt, 2, c0, c1, cur)
             cur, nxt = nxt, cur
         return cur[p.owned]
+
+
+# ------------------------------------------------------------ sharded solve --
+# Thick-restarted Arnoldi with the Krylov basis sharded by rows.  Every
+# reduction (CGS2 coefficients, norms, Rayleigh quotients, residuals) is a
+# local partial sum followed by an all-reduce, so every rank holds the same
+# Hessenberg matrix and the replicated host work (Ritz pairs, restart QR,
+# Leja order) makes identical decisions on every rank.  Vector arithmetic is
+# plain torch on the backend's device (CUDA tensors under NCCL, CPU tensors
+# under gloo); the operator is the sharded pi(A)v above.  Same algorithm and
+# counters as the single-GPU solve (csrc/solver.cpp) except
+# that the summation order of the reductions differs (results agree to
+# roundoff, not bit for bit).
+
+_PAIR_TOL = 1e-10  # src/arnoldi.cpp:16
+
+
+def _is_complex(z: complex) -> bool:
+    return abs(z.imag) > _PAIR_TOL * max(1.0, abs(z))
+
+
+def _arrange(values, vectors, ordering: str):
+    """sort_pairs (src/arnoldi.cpp:40-95): stable by key, conjugate mates
+    adjacent, +imag first."""
+    key = (lambda z: abs(1.0 - z)) if ordering == "target_one" else abs
+    idx = sorted(range(len(values)), key=lambda i: key(values[i]))
+    used, out = set(), []
+    for i in idx:
+        if i in used:
+            continue
+        used.add(i)
+        if not _is_complex(values[i]):
+            out.append(i)
+            continue
+        mate = next((j for j in idx if j not in used and
+                     abs(values[i] - np.conj(values[j])) <= _PAIR_TOL * max(1.0, abs(values[i]))),
+                    None)
+        if mate is None:
+            out.append(i)
+            continue
+        used.add(mate)
+        out += [i, mate] if values[i].imag >= 0.0 else [mate, i]
+    return np.asarray(values)[out], np.asarray(vectors)[:, out]
+
+
+class ShardedSolver:
+    """solve() over row-sharded vectors (collective: every rank calls it)."""
+
+    def __init__(self, plan: HaloPlan, backend, dist, group=None):
+        import torch
+
+        self.torch = torch
+        self.plan = plan
+        self.b = backend
+        self.dist = dist
+        self.group = group
+        self.sp = ShardedPoly(plan, backend, dist, group)
+        self.mvps = 0
+
+    # -- reductions ----------------------------------------------------------
+    def _allreduce(self, t):
+        self.dist.all_reduce(t, group=self.group)
+        return t
+
+    def _dots(self, Vc, w):
+        return self._allreduce(Vc @ w)
+
+    def _norm(self, w):
+        return float(self._allreduce((w @ w).reshape(1)).sqrt().item())
+
+    # -- operators -----------------------------------------------------------
+    def _spmv(self, x):
+        p = self.plan
+        xe = self.b.zeros(p.n_ext)
+        ye = self.b.zeros(p.n_ext)
+        self.b.copy_(xe[p.owned], x)
+        self.sp.exchange(xe)
+        self.b.factor(xe, ye, 0)
+        self.mvps += 1
+        return ye[p.owned].clone()
+
+    def _op(self, x):
+        if self.roots is None:
+            return self._spmv(x)
+        self.mvps += len(self.roots)
+        return self.sp.apply(self.roots, x).clone()
+
+    # -- Arnoldi -------------------------------------------------------------
+    def _init(self, v0, m):
+        t = self.torch
+        V = t.zeros((m + 1, self.plan.n_local), dtype=t.float64, device=v0.device)
+        V[0] = v0 / self._norm(v0)
+        return V, np.zeros((m + 1, m))
+
+    def _extend(self, V, H, j0, m, op):
+        """CGS2 steps j0..m-1; returns (cur_dim, breakdown)."""
+        for j in range(j0, m):
+            w = op(V[j])
+            Vc = V[:j + 1]
+            h1 = self._dots(Vc, w)
+            w = w - Vc.T @ h1
+            h2 = self._dots(Vc, w)
+            w = w - Vc.T @ h2
+            hsub = self._norm(w)
+            col = (h1 + h2).cpu().numpy()
+            H[:j + 1, j] = col
+            if not np.isfinite(hsub) or hsub <= 1e-14 * np.sqrt(col @ col + hsub * hsub):
+                H[j + 1, j] = 0.0
+                return j + 1, True
+            H[j + 1, j] = hsub
+            V[j + 1] = w / hsub
+        return m, False
+
+    def _ritz(self, H, d, ordering):
+        vals, vecs = np.linalg.eig(H[:d, :d])
+        vecs = vecs / np.linalg.norm(vecs, axis=0)
+        return _arrange(vals, vecs, ordering)
+
+    def _check(self, V, d, vals, vecs, nev):
+        """Rayleigh quotients and true residuals of the first nev pairs."""
+        t = self.torch
+        mus, res = [], []
+        i = 0
+        while i < min(nev, len(vals)):
+            g = vecs[:, i]
+            yr = V[:d].T @ t.as_tensor(np.ascontiguousarray(g.real), device=V.device)
+            if not _is_complex(vals[i]):
+                nrm = self._norm(yr)
+                yr = yr / nrm
+                ay = self._spmv(yr)
+                mu = float(self._allreduce((yr @ ay).reshape(1)).item())
+                res.append(self._norm(ay - mu * yr))
+                mus.append(complex(mu, 0.0))
+                i += 1
+                continue
+            yi = V[:d].T @ t.as_tensor(np.ascontiguousarray(g.imag), device=V.device)
+            nrm = np.sqrt(self._norm(yr) ** 2 + self._norm(yi) ** 2)
+            yr, yi = yr / nrm, yi / nrm
+            ar, ai = self._spmv(yr), self._spmv(yi)
+            # mu = y^H A y for unit y = yr + i yi
+            re = float(self._allreduce((yr @ ar + yi @ ai).reshape(1)).item())
+            im = float(self._allreduce((yr @ ai - yi @ ar).reshape(1)).item())
+            r = np.sqrt(self._norm(ar - re * yr + im * yi) ** 2 +
+                        self._norm(ai - re * yi - im * yr) ** 2)
+            mus += [complex(re, im), complex(re, -im)]
+            res += [r, r]
+            i += 2
+        return mus[:nev], res[:nev]
+
+    def _restart(self, V, H, m, vals, vecs, k):
+        """thick_restart (src/arnoldi.cpp:267-334) on the sharded basis."""
+        t = self.torch
+        cols, j = [], 0
+        while len(cols) < k and j < len(vals):
+            if not _is_complex(vals[j]):
+                cols.append(vecs[:, j].real)
+                j += 1
+            else:
+                if len(cols) + 2 > k:
+                    break
+                cols += [vecs[:, j].real, vecs[:, j].imag]
+                j += 2
+        kk = len(cols)
+        Q, _ = np.linalg.qr(np.stack(cols, axis=1))
+        Hk = Q.T @ H[:m, :m] @ Q
+        hrow = H[m, m - 1] * Q[m - 1]
+        Qt = t.as_tensor(np.ascontiguousarray(Q), device=V.device)
+        V[:kk] = (V[:m].T @ Qt).T
+        V[kk] = V[m]
+        c = self._dots(V[:kk], V[kk])
+        V[kk] = V[kk] - V[:kk].T @ c
+        rn = self._norm(V[kk])
+        V[kk] = V[kk] / rn
+        Hk = Hk + np.outer(c.cpu().numpy(), hrow)
+        H[:] = 0.0
+        H[:kk, :kk] = Hk
+        H[kk, :kk] = rn * hrow
+        return kk
+
+    # -- driver ----------------------------------------------------------------
+    def solve(self, v0_poly, v0_arnoldi, v0_norm, m, k, nev, degree=0, rtol_multiplier=1e-8,
+              max_cycles=100, stability=False):
+        from . import _capi as C
+
+        self.roots = None
+        # norm estimate: five power steps (DESIGN.md §5)
+        x = v0_norm / self._norm(v0_norm)
+        est = 0.0
+        for it in range(5):
+            y = self._spmv(x)
+            est = self._norm(y)
+            if est == 0.0:
+                break
+            x = y / est
+        rtol = rtol_multiplier * est
+        ordering = "smallest_magnitude"
+        if degree > 0:
+            Vb, Hb = self._init(v0_poly, degree)
+            d, _ = self._extend(Vb, Hb, 0, degree, self._spmv)
+            Hd = Hb[:d, :d].copy()
+            hs = Hb[d, d - 1]
+            if hs != 0.0:
+                f = np.linalg.solve(Hd.T, np.eye(d)[:, d - 1])
+                Hd[:, d - 1] += hs * hs * f
+            self.roots = C.leja_order(np.linalg.eigvals(Hd))
+            if stability and len(self.roots) >= 2:
+                self.roots = C.add_stability_roots(self.roots, len(self.roots))
+            ordering = "target_one"
+        V, H = self._init(v0_arnoldi, m)
+        cur, cycles, mus, res = 0, 0, [], []
+        for cycles in range(1, max_cycles + 1):
+            d, bd = self._extend(V, H, cur, m, self._op)
+            vals, vecs = self._ritz(H, d, ordering)
+            mus, res = self._check(V, d, vals, vecs, nev)
+            if all(r <= rtol for r in res) or bd or cycles == max_cycles:
+                break
+            cur = self._restart(V, H, m, vals, vecs, k)
+        return {"eigenvalues": np.asarray(mus), "residuals": np.asarray(res), "rtol": rtol,
+                "converged": bool(len(res) == nev and all(r <= rtol for r in res)),
+                "cycles": cycles, "mvps": self.mvps, "poly": self.roots}
