@@ -150,3 +150,19 @@ def test_concurrent_solves_two_threads(cuda):
     for a, b in zip(out, seq):
         assert np.array_equal(a["eigenvalues"], b["eigenvalues"])
         assert a["cost"]["mvps"] == b["cost"]["mvps"] and a["cycles"] == b["cycles"]
+
+
+@pytest.mark.parametrize("degree", [0, 3])
+def test_breakdown_inside_solve_matches_oracle(cuda, degree):
+    # five distinct eigenvalues: every Krylov space breaks down at dimension 5,
+    # inside the first cycle (the pipelined CGS2 extend has already enqueued
+    # the next step); the solve checks that cycle's pairs and stops
+    d = np.repeat([1.0, 2.0, 4.0, 7.0, 11.0], 100)
+    cfg = ppa.SolveConfig(m=30, k=15, nev=3, degree=degree, seed=4, max_cycles=10)
+    r = ppa.solve(ppa.make_diagonal(d), cfg)
+    o = O.solve(O.diagonal_operator(d), 30, 15, 3, degree=degree, seed=4, max_cycles=10)
+    assert r["converged"] == o["converged"] and r["cycles"] == o["cycles"] == 1
+    assert (r["cost"]["mvps"], r["cost"]["dots"], r["cost"]["vops"]) == \
+        (o["cost"]["mvps"], o["cost"]["dots"], o["cost"]["vops"])
+    assert np.allclose(np.sort(r["eigenvalues"].real), np.sort(o["eigenvalues"].real),
+                       rtol=1e-10)
