@@ -26,7 +26,7 @@ CONFIGS = {
 }
 
 
-def config_solve_config(k: int, **over) -> SolveConfig:
-    kw = dict(CONFIGS[k]["solve"])
+def config_solve_config(config: int, **over) -> SolveConfig:
+    kw = dict(CONFIGS[config]["solve"])
     kw.update(over)
     return SolveConfig(**kw)
