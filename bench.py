@@ -310,7 +310,7 @@ def run_b200(args):
         "roofline": {"bound": "hbm", "achieved": round(kbytes / auto_launch_s / 1e9, 2),
                      "peak": peak, "unit": "GB/s",
                      "frac": round(kbytes / auto_launch_s / 1e9 / peak, 4),
-                     "kernel": "k_spmv_diar (regular-row diagonal form, fused real-root factor)",
+                     "kernel": "k_spmv_diam (regular-row diagonal form, marching over the +-plane diagonals, fused real-root factor)",
                      "algorithmic_bytes_per_launch": kbytes,
                      "bytes_note": "matrix stream of this layout + 8n x + 8n y"},
         "bit_identical_to_sell32": auto_match,

@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <unordered_map>
@@ -199,13 +200,41 @@ struct DiaRParams {
 // the regular sweep.
 constexpr int RB = 512;
 
+// One irregular row from the exception list: codes, gathers, sum in
+// diagonal order (shared by the regular-row and marching sweeps).
+template <int MODE, bool COMPL, int ND>
+__device__ __forceinline__ void irregular_row(const int* __restrict__ irr_rows,
+                                              const unsigned char* __restrict__ irr_codes,
+                                              int k, const double* __restrict__ dict,
+                                              const DiaRParams& P, const double* __restrict__ x,
+                                              double* y, const EpiDev& e) {
+  constexpr int NW = ND <= 4 ? 1 : ND <= 8 ? 2 : 4;
+  const int r = __ldg(irr_rows + k);
+  unsigned ec[NW];
+  load_codes<NW>(ec, reinterpret_cast<const unsigned*>(irr_codes) + static_cast<long long>(k) * NW);
+  pdl_wait();  // x is the previous factor's output
+  double xv[ND];
+#pragma unroll
+  for (int j = 0; j < ND; ++j) {
+    const unsigned c = code_of(ec[j / 4], j);
+    xv[j] = __ldg(x + (c != kDiaAbsent ? r + P.off[j] : r));
+  }
+  double sum = 0.0;
+#pragma unroll
+  for (int j = 0; j < ND; ++j) {
+    const unsigned c = code_of(ec[j / 4], j);
+    if (c != kDiaAbsent) sum = __dadd_rn(sum, __dmul_rn(__ldg(dict + c), xv[j]));
+  }
+  y[r] = epilogue<MODE, COMPL>(r, sum, x, e);
+}
+
+
 template <int MODE, bool COMPL, int ND, int RPT>
 __global__ void __launch_bounds__(RB) k_spmv_diar(
     const unsigned* __restrict__ mask, const int* __restrict__ irr_rows,
     const unsigned char* __restrict__ irr_codes, int n_irr, int gx,
     const double* __restrict__ dict, const DiaRParams P, int n, const double* __restrict__ x,
     double* y, const EpiDev e) {
-  constexpr int NW = ND <= 4 ? 1 : ND <= 8 ? 2 : 4;  // code words per row (stride / 4)
   pdl_trigger();
   const int bx = blockIdx.x;
   if (bx < gx) {
@@ -214,23 +243,7 @@ __global__ void __launch_bounds__(RB) k_spmv_diar(
       pdl_wait();
       return;
     }
-    const int r = __ldg(irr_rows + k);
-    unsigned ec[NW];
-    load_codes<NW>(ec, reinterpret_cast<const unsigned*>(irr_codes) + static_cast<long long>(k) * NW);
-    pdl_wait();  // x is the previous factor's output
-    double xv[ND];
-#pragma unroll
-    for (int j = 0; j < ND; ++j) {
-      const unsigned c = code_of(ec[j / 4], j);
-      xv[j] = __ldg(x + (c != kDiaAbsent ? r + P.off[j] : r));
-    }
-    double sum = 0.0;
-#pragma unroll
-    for (int j = 0; j < ND; ++j) {
-      const unsigned c = code_of(ec[j / 4], j);
-      if (c != kDiaAbsent) sum = __dadd_rn(sum, __dmul_rn(__ldg(dict + c), xv[j]));
-    }
-    y[r] = epilogue<MODE, COMPL>(r, sum, x, e);
+    irregular_row<MODE, COMPL, ND>(irr_rows, irr_codes, k, dict, P, x, y, e);
     return;
   }
   // regular rows: RPT rows per thread, RB apart, all gathers issued first
@@ -274,6 +287,133 @@ void launch_diar_rpt(const CsrDevice& a, const double* x, double* y, const EpiAr
              a.n, x, y, epi_dev(ep));
 }
 
+// ---- marching form ----------------------------------------------------------
+// When the outermost diagonals are +-D (a stencil's +-plane, or +-row in 2D),
+// row r needs x[r - D] and x[r + D], which are the centres of rows r - D and
+// r + D.  A thread that owns column c of the "plane" [0, D) and walks T
+// consecutive planes, rows r_t = (q0 + t) D + c, loads the T + 2 plane values
+// once and uses each up to three times, so the two outer gathers per row
+// shrink to one load per row plus two per T rows.  The middle diagonals are
+// gathered as in k_spmv_diar; the row sum visits the diagonals in the same
+// increasing-offset order (bit-identical).  For symmetric stencils the
+// centre x[r] is the middle plane value, reused by the epilogue too.  In the
+// 50-factor chain (tools/spmv_ab.py, PPA_DIA_MARCH=0 turns it off): config 3
+// 15.4 -> 14.5 us, config 5 11.9 -> 10.6 us, config 2 5.0 -> 4.6 us.
+constexpr int MB = 256;  // threads per CTA of the marching sweep
+
+template <int MODE, bool COMPL, int ND, int T, bool HC>
+__global__ void __launch_bounds__(MB) k_spmv_diam(
+    const unsigned* __restrict__ mask, const int* __restrict__ irr_rows,
+    const unsigned char* __restrict__ irr_codes, int n_irr, int gx,
+    const double* __restrict__ dict, const DiaRParams P, int n, int D, int G,
+    const double* __restrict__ x, double* y, const EpiDev e) {
+  static_assert(ND >= 3, "marching needs two outer diagonals and a middle one");
+  pdl_trigger();
+  const int bx = blockIdx.x;
+  if (bx < gx) {
+    const int k = bx * MB + threadIdx.x;
+    if (k >= n_irr) {
+      pdl_wait();
+      return;
+    }
+    irregular_row<MODE, COMPL, ND>(irr_rows, irr_codes, k, dict, P, x, y, e);
+    return;
+  }
+  // 32-bit rows: the launcher guarantees n + (T + 1) D < 2^31
+  const int w = (bx - gx) * (MB / 32) + (threadIdx.x >> 5);
+  const int g = w / G;
+  const int c = (w - g * G) * 32 + (threadIdx.x & 31);
+  const int rb = g * T * D + c;
+  const bool col = c < D;
+  unsigned m[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    const int r = rb + t * D;
+    m[t] = (col && r < n) ? __ldg(mask + (r >> 5)) : 0u;
+  }
+  pdl_wait();  // x is the previous factor's output
+  double pl[T + 2];
+  double xv[T][ND - 2];
+#pragma unroll
+  for (int t = 0; t < T + 2; ++t) pl[t] = __ldg(x + min(max(rb + (t - 1) * D, 0), n - 1));
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    const int r = min(rb + t * D, n - 1);
+#pragma unroll
+    for (int j = 1; j < ND - 1; ++j) {
+      // HC: diagonal (ND - 1) / 2 is offset 0, i.e. this row's plane value
+      xv[t][j - 1] = HC && j == (ND - 1) / 2 ? pl[t + 1]
+                                             : __ldg(x + min(max(r + P.off[j], 0), n - 1));
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    const int r = rb + t * D;
+    double sum = __dadd_rn(0.0, __dmul_rn(P.val[0], pl[t]));
+#pragma unroll
+    for (int j = 1; j < ND - 1; ++j) sum = __dadd_rn(sum, __dmul_rn(P.val[j], xv[t][j - 1]));
+    sum = __dadd_rn(sum, __dmul_rn(P.val[ND - 1], pl[t + 2]));
+    if ((m[t] >> (r & 31)) & 1u) {
+      y[r] = HC ? epilogue_x<MODE, COMPL>(r, sum, pl[t + 1], e) : epilogue<MODE, COMPL>(r, sum, x, e);
+    }
+  }
+}
+
+constexpr int kMarchT = 4;  // minimum planes per thread
+
+// Marching applies when the outer diagonals are a symmetric pair +-D with
+// enough columns per plane to fill warps and enough planes to walk.
+bool march_applies(const CsrDevice& a) {
+  static const bool enabled = [] {
+    const char* v = std::getenv("PPA_DIA_MARCH");
+    return !(v && v[0] == '0');
+  }();
+  if (!enabled || a.dia_ndiag < 3) return false;
+  const int D = a.dia_off[a.dia_ndiag - 1];
+  return D >= 256 && a.dia_off[0] == -D && a.n / D >= 2 * kMarchT &&
+         static_cast<long long>(a.n) + 10LL * D < (1LL << 31);
+}
+
+template <int MODE, bool COMPL, int ND, int T>
+void launch_diam_t(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep,
+                   cudaStream_t st) {
+  DiaRParams P{};
+  for (int j = 0; j < a.dia_ndiag; ++j) {
+    P.off[j] = a.dia_off[j];
+    P.val[j] = a.dia_dflt[j];
+  }
+  const int D = a.dia_off[ND - 1];
+  const int G = (D + 31) / 32;
+  const int nq = (a.n + D - 1) / D;
+  const long long warps = static_cast<long long>(G) * ((nq + T - 1) / T);
+  const int gx = static_cast<int>((a.dia_nirr + MB - 1) / MB);
+  const int grid = gx + static_cast<int>((warps + MB / 32 - 1) / (MB / 32));
+  // symmetric stencils (odd ND, offset 0 in the middle) reuse the centre
+  const bool hc = (ND % 2 == 1) && a.dia_off[(ND - 1) / 2] == 0;
+  auto kernel = hc ? k_spmv_diam<MODE, COMPL, ND, T, true> : k_spmv_diam<MODE, COMPL, ND, T, false>;
+  launch_pdl(kernel, dim3(grid), dim3(MB), 0, st, a.dia_mask, a.dia_irr_rows, a.dia_irr_codes,
+             static_cast<int>(a.dia_nirr), gx, a.dia_dict, P, a.n, D, G, x, y, epi_dev(ep));
+}
+
+// Planes per thread: 8 (config 3: 14.7 -> 14.5 us, config 5: 11.0 -> 10.6)
+// while that still leaves a full wave of warps (64 per SM), else 4 (config
+// 2, n = 1e6: 4.6 us with 4, 5.8 with 8).  PPA_DIA_MARCH_T=2|4|8 overrides.
+template <int MODE, bool COMPL, int ND>
+void launch_diam(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep,
+                 cudaStream_t st) {
+  static const int forced = [] {
+    const char* v = std::getenv("PPA_DIA_MARCH_T");
+    return v ? std::atoi(v) : 0;
+  }();
+  const int D = a.dia_off[ND - 1];
+  const long long nq = (a.n + D - 1) / D;
+  const long long warps8 = static_cast<long long>((D + 31) / 32) * ((nq + 7) / 8);
+  const int t = forced ? forced : warps8 >= 64LL * device_sms() ? 8 : 4;
+  if (t == 2) return launch_diam_t<MODE, COMPL, ND, 2>(a, x, y, ep, st);
+  if (t == 8) return launch_diam_t<MODE, COMPL, ND, 8>(a, x, y, ep, st);
+  launch_diam_t<MODE, COMPL, ND, 4>(a, x, y, ep, st);
+}
+
 // Rows per thread of the regular sweep: each thread keeps RPT rows' gathers
 // in flight (the kernel is latency-bound: 17.6 -> 15.4 us on config 3 and
 // 15.0 -> 11.9 us on config 5 going from 1 to 3 rows), for matrices large
@@ -283,6 +423,9 @@ template <int MODE, bool COMPL, int ND>
 void launch_diar(const CsrDevice& a, const double* x, double* y, const EpiArgs& ep,
                  cudaStream_t st) {
   constexpr long long kRowsFor3 = 3LL * RB * 148 * 4 * 4;  // 3 rows x 4 waves x 4 CTAs/SM
+  if constexpr (ND >= 3 && ND <= 8) {
+    if (march_applies(a)) return launch_diam<MODE, COMPL, ND>(a, x, y, ep, st);
+  }
   if constexpr (ND <= 8) {
     if (a.n >= kRowsFor3) return launch_diar_rpt<MODE, COMPL, ND, 3>(a, x, y, ep, st);
   }

@@ -29,16 +29,16 @@ inline EpiDev epi_dev(const EpiArgs& a) {
   return EpiDev{a.c0, a.c1, a.o, a.base, a.outer, a.oc0, a.oc1, a.oo};
 }
 
+// xr = x[r], already in a register (the gather kernels hold the centre).
 template <int MODE, bool COMPL>
-__device__ __forceinline__ double epilogue(int r, double s, const double* __restrict__ x,
-                                           const EpiDev& e) {
+__device__ __forceinline__ double epilogue_x(int r, double s, double xr, const EpiDev& e) {
   double z;
   if (MODE == 0) {
     z = s;
   } else if (MODE == 1) {
-    z = __dadd_rn(__ldg(x + r), __dmul_rn(e.c0, s));
+    z = __dadd_rn(xr, __dmul_rn(e.c0, s));
   } else {
-    z = __dadd_rn(__dadd_rn(e.o[r], __dmul_rn(e.c1, __ldg(x + r))), __dmul_rn(e.c0, s));
+    z = __dadd_rn(__dadd_rn(e.o[r], __dmul_rn(e.c1, xr)), __dmul_rn(e.c0, s));
   }
   if (COMPL) {
     const double b = e.base[r];
@@ -50,6 +50,12 @@ __device__ __forceinline__ double epilogue(int r, double s, const double* __rest
     }
   }
   return z;
+}
+
+template <int MODE, bool COMPL>
+__device__ __forceinline__ double epilogue(int r, double s, const double* __restrict__ x,
+                                           const EpiDev& e) {
+  return epilogue_x<MODE, COMPL>(r, s, MODE == 0 ? 0.0 : __ldg(x + r), e);
 }
 
 }  // namespace kern

@@ -154,6 +154,46 @@ def test_dia_diagonal_counts_bit_exact(cuda, offsets):
         assert np.array_equal(AY[j, :n], O.csr_operator(Q).apply(Y[j, :n]))
 
 
+def _banded_csr(n, offsets, vals, irregular=()):
+    """_banded as CSR arrays, vectorised (multi-million-row cases)."""
+    offs = np.asarray(offsets)
+    cols = np.arange(n)[:, None] + offs[None, :]
+    keep = (cols >= 0) & (cols < n)
+    v = np.broadcast_to(np.asarray(vals, dtype=np.float64), cols.shape).copy()
+    v[list(irregular)] *= 1.5
+    rp = np.concatenate([[0], np.cumsum(keep.sum(axis=1))]).astype(np.int32)
+    return rp, cols[keep].astype(np.int32), v[keep]
+
+
+@pytest.mark.parametrize("n,offsets", [
+    (300 * 13 + 7, (-300, -1, 0, 1, 300)),               # centre in the middle, ragged tail
+    (300 * 12, (-300, -1, 1, 300)),                      # even count: no centre reuse
+    (256 * 9 + 100, (-256, -2, -1, 7, 256)),             # odd count, middle is not offset 0
+    (400 * 10, (-400, -20, -1, 0, 1, 20, 400)),          # 7-point, 3-D-like
+    (2048 * 1200 + 77, (-2048, -1, 0, 1, 2048)),         # enough warps for 8 planes per thread
+])
+def test_dia_march_bit_exact(cuda, n, offsets):
+    # the marching sweep (outer diagonals +-D, D >= 256): SpMV, pi(A)v with
+    # real and pair roots, and the complement, against the oracle
+    vals = [float(k + 2) * (-1) ** k for k in range(len(offsets))]
+    rp, ci, vv = _banded_csr(n, offsets, vals, irregular=[3, n // 2, n - 5])
+    P = ppa.CsrMatrix.from_arrays(n, rp, ci, vv)
+    Q = O.Csr.from_arrays(n, rp, ci, vv)
+    A = ppa.make_csr_operator(P)
+    assert A.layout()["layout"] == "dia_coded"
+    x = O.normal_vector(n, 6, 3)
+    y = cuda.empty(n, dtype=cuda.float64, device="cuda")
+    A.apply(dev(cuda, x), y)
+    assert np.array_equal(host(y), O.csr_operator(Q).apply(x))
+    roots = _roots_mixed()
+    out = cuda.empty(n, dtype=cuda.float64, device="cuda")
+    ppa.apply_poly(roots, A, dev(cuda, x), out)
+    assert np.array_equal(host(out), O.apply_poly(roots, O.csr_operator(Q), x))
+    T = ppa.make_poly_complement_operator(A, roots)
+    T.apply(dev(cuda, x), out)
+    assert np.array_equal(host(out), O.poly_operator(O.csr_operator(Q), roots, complement=True).apply(x))
+
+
 def _edge_matrices():
     rng = np.random.default_rng(11)
     out = {}

@@ -151,6 +151,45 @@ __global__ void k_march(const unsigned* __restrict__ mask, const double* __restr
   }
 }
 
+// the march with every load of the T planes issued up front
+template <int T>
+__global__ void k_march_u(const unsigned* __restrict__ mask, const double* __restrict__ x,
+                          double* __restrict__ y, int n, double c0, int S, int G, int NQ) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int g = w % G, ch = w / G;
+  const int p = g * 32 + lane;
+  const int q0 = ch * T;
+  if (q0 >= NQ) return;
+  const int rb = q0 * S + p;
+  double pl[T + 2], xv[T][4];
+  unsigned m[T];
+#pragma unroll
+  for (int t = 0; t < T + 2; ++t) pl[t] = __ldg(x + min(max(rb + (t - 1) * S, 0), n - 1));
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    const int r = rb + t * S;
+    m[t] = __ldg(mask + (min(r, n - 1) >> 5));
+    xv[t][0] = __ldg(x + min(max(r - N, 0), n - 1));
+    xv[t][1] = __ldg(x + min(max(r - 1, 0), n - 1));
+    xv[t][2] = __ldg(x + min(r + 1, n - 1));
+    xv[t][3] = __ldg(x + min(r + N, n - 1));
+  }
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    const int r = rb + t * S;
+    double s = 0.0;
+    s = __dadd_rn(s, __dmul_rn(-1.0, pl[t]));
+    s = __dadd_rn(s, __dmul_rn(-1.0, xv[t][0]));
+    s = __dadd_rn(s, __dmul_rn(-1.0, xv[t][1]));
+    s = __dadd_rn(s, __dmul_rn(6.0, pl[t + 1]));
+    s = __dadd_rn(s, __dmul_rn(-1.0, xv[t][2]));
+    s = __dadd_rn(s, __dmul_rn(-1.0, xv[t][3]));
+    s = __dadd_rn(s, __dmul_rn(-1.0, pl[t + 2]));
+    if (q0 + t < NQ && r < n && ((m[t] >> (r & 31)) & 1u)) y[r] = __dadd_rn(pl[t + 1], __dmul_rn(c0, s));
+  }
+}
+
 template <typename F>
 float timeit(F f, int reps) {
   cudaEvent_t a, b;
@@ -208,6 +247,17 @@ int main() {
       if (T == 8) tm = timeit([&] { k_march<8><<<blocks, 256>>>(mask, x, y, NN, 0.5, S, G, NQ); std::swap(x, y); }, 50);
       if (T == 16) tm = timeit([&] { k_march<16><<<blocks, 256>>>(mask, x, y, NN, 0.5, S, G, NQ); std::swap(x, y); }, 50);
       printf("march T=%d: %.2f us\n", T, tm);
+    }
+    for (int T : {2, 4, 8}) {
+      const int warps = G * ((NQ + T - 1) / T);
+      for (int bs2 : {128, 256, 512}) {
+        const int blocks = (warps * 32 + bs2 - 1) / bs2;
+        float tm = 0;
+        if (T == 2) tm = timeit([&] { k_march_u<2><<<blocks, bs2>>>(mask, x, y, NN, 0.5, S, G, NQ); std::swap(x, y); }, 50);
+        if (T == 4) tm = timeit([&] { k_march_u<4><<<blocks, bs2>>>(mask, x, y, NN, 0.5, S, G, NQ); std::swap(x, y); }, 50);
+        if (T == 8) tm = timeit([&] { k_march_u<8><<<blocks, bs2>>>(mask, x, y, NN, 0.5, S, G, NQ); std::swap(x, y); }, 50);
+        printf("march_u T=%d bs=%d: %.2f us\n", T, bs2, tm);
+      }
     }
   }
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
