@@ -183,31 +183,73 @@ __global__ void k_fill(double* x, double v, long long n) {
 
 inline int ew_grid(long long n) { return std::max(1, std::min(ceil_div(n, 256), 148 * 16)); }
 
-// Out[:,0:p] = V[:,0:d] * G, one row per thread, the block's rows staged
-// in shared memory first (so Out may alias V).
-constexpr int kCombineRows = 128;
+// Out[:,0:p] = V[:,0:d] * G.  One row per thread with its p accumulators in
+// registers: the row's d values are streamed once (8 columns of loads in
+// flight) and G comes from shared memory, row-major with an even row
+// length, two columns per broadcast 16-byte read.  A row's outputs are
+// written only after all of its d inputs were read, by the same thread, so
+// Out may alias V (the in-place thick restart, p <= d).  Per output: fma over
+// j = 0..d-1 in order (the same arithmetic as the row-staged kernel it
+// replaces, which was shared-memory-bound: 0.54 ms for d = 40, p = 20 on
+// config 3).
+constexpr int CB = 256;  // threads per CTA
 
-__global__ void __launch_bounds__(kCombineRows) k_ts_combine(const double* V, long long ldv, int n,
-                                                             int d, const double* __restrict__ G,
-                                                             int p, double* Out, long long ldo) {
-  extern __shared__ double sm[];
-  double* tile = sm;                       // [d][kCombineRows]
-  double* gs = sm + d * kCombineRows;      // [d*p] column-major
-  for (int k = threadIdx.x; k < d * p; k += kCombineRows) gs[k] = G[k];
-  const int r0 = blockIdx.x * kCombineRows;
-  const int i = r0 + threadIdx.x;
-  const bool live = i < n;
-  for (int j = 0; j < d; ++j) {
-    tile[j * kCombineRows + threadIdx.x] = live ? V[i + static_cast<long long>(j) * ldv] : 0.0;
+template <int PB>
+__global__ void __launch_bounds__(CB) k_ts_combine(const double* V, long long ldv, int n, int d,
+                                                   const double* __restrict__ G, int p,
+                                                   double* Out, long long ldo) {
+  static_assert(PB % 2 == 0, "column pairs");
+  extern __shared__ double2 gs2[];  // G row-major: row j = columns 0..PB-1 (zero-padded)
+  double* gs = reinterpret_cast<double*>(gs2);
+  for (int k = threadIdx.x; k < d * PB; k += CB) {
+    const int j = k / PB, c = k - j * PB;
+    gs[k] = c < p ? G[static_cast<long long>(c) * d + j] : 0.0;
   }
   __syncthreads();
-  if (!live) return;
-  for (int col = 0; col < p; ++col) {
-    const double* g = gs + col * d;
-    double acc = 0.0;
-    for (int j = 0; j < d; ++j) acc = fma(tile[j * kCombineRows + threadIdx.x], g[j], acc);
-    Out[i + static_cast<long long>(col) * ldo] = acc;
+  const long long i = static_cast<long long>(blockIdx.x) * CB + threadIdx.x;
+  const bool live = i < n;
+  const long long row = live ? i : n - 1;  // clamped loads, no store
+  double acc[PB];
+#pragma unroll
+  for (int c = 0; c < PB; ++c) acc[c] = 0.0;
+  // columns p..PB-1 of G are zero in shared memory: no per-column test
+  auto step = [&](double v, const double2* g) {
+#pragma unroll
+    for (int c = 0; c < PB / 2; ++c) {
+      const double2 gv = g[c];
+      acc[2 * c] = fma(v, gv.x, acc[2 * c]);
+      acc[2 * c + 1] = fma(v, gv.y, acc[2 * c + 1]);
+    }
+  };
+  constexpr int JU = 8;
+  const double* vr = V + row;
+  int j0 = 0;
+  for (; j0 + JU <= d; j0 += JU) {
+    double v[JU];
+#pragma unroll
+    for (int jj = 0; jj < JU; ++jj) v[jj] = vr[static_cast<long long>(j0 + jj) * ldv];
+    const double2* g = gs2 + j0 * (PB / 2);
+#pragma unroll
+    for (int jj = 0; jj < JU; ++jj) step(v[jj], g + jj * (PB / 2));
   }
+  for (; j0 < d; ++j0) step(vr[static_cast<long long>(j0) * ldv], gs2 + j0 * (PB / 2));
+  if (!live) return;
+#pragma unroll
+  for (int c = 0; c < PB; ++c) {
+    if (c < p) Out[row + static_cast<long long>(c) * ldo] = acc[c];
+  }
+}
+
+template <int PB>
+void launch_combine(const double* V, long long ldv, int n, int d, const double* G, int p,
+                    double* Out, long long ldo, size_t smem, cudaStream_t st) {
+  static const bool capped = [] {  // once per instantiation, thread-safe
+    PPA_CUDA(cudaFuncSetAttribute(k_ts_combine<PB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  max_dynamic_smem(k_ts_combine<PB>)));
+    return true;
+  }();
+  (void)capped;
+  k_ts_combine<PB><<<ceil_div(n, CB), CB, smem, st>>>(V, ldv, n, d, G, p, Out, ldo);
 }
 
 }  // namespace
@@ -286,18 +328,43 @@ void ts_combine(const double* V, long long ldv, int n, int d, const double* G, i
   if (n <= 0 || p <= 0) return;
   if (d < 1) throw std::invalid_argument("ts_combine: d < 1");
   if (Out == V && p > d) throw std::invalid_argument("ts_combine: in-place needs p <= d");
-  const size_t smem = (static_cast<size_t>(d) * kCombineRows + static_cast<size_t>(d) * p) *
-                      sizeof(double);
-  static const bool capped = [] {  // once, thread-safe
-    PPA_CUDA(cudaFuncSetAttribute(k_ts_combine, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  max_dynamic_smem(k_ts_combine)));
-    return true;
-  }();
-  (void)capped;
-  if (smem > 227 * 1024) throw std::invalid_argument("ts_combine: d*p too large");
-  k_ts_combine<<<ceil_div(n, kCombineRows), kCombineRows, smem, st>>>(V, ldv, n, d, G, p, Out,
-                                                                      ldo);
-  PPA_CUDA(cudaGetLastError());
+  if (static_cast<size_t>(d) * std::min(p, 32) * sizeof(double) > 200 * 1024) {
+    throw std::invalid_argument("ts_combine: d too large");
+  }
+  if (Out == V && p > 32) {
+    // wide in-place restart (k > 32): combine into a stream-ordered
+    // temporary in 32-column passes, then copy back over V
+    double* tmp = nullptr;
+    const long long ldt = (static_cast<long long>(n) + 31) / 32 * 32;
+    PPA_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp),
+                             static_cast<size_t>(ldt) * p * sizeof(double), st));
+    ts_combine(V, ldv, n, d, G, p, tmp, ldt, st);
+    PPA_CUDA(cudaMemcpy2DAsync(Out, static_cast<size_t>(ldo) * sizeof(double), tmp,
+                               static_cast<size_t>(ldt) * sizeof(double),
+                               static_cast<size_t>(n) * sizeof(double), p,
+                               cudaMemcpyDeviceToDevice, st));
+    PPA_CUDA(cudaFreeAsync(tmp, st));
+    return;
+  }
+  // accumulator count bucketed so registers stay <= ~128 per thread; the
+  // passes only read V, so they are independent (in place: one pass)
+  for (int c0 = 0; c0 < p; c0 += 32) {
+    const int pc = std::min(32, p - c0);
+    const double* g = G + static_cast<long long>(c0) * d;
+    double* out = Out + static_cast<long long>(c0) * ldo;
+    auto sm = [&](int pb) { return static_cast<size_t>(d) * pb * sizeof(double); };
+    switch ((pc + 3) / 4) {  // accumulators rounded up to a multiple of 4
+      case 1: launch_combine<4>(V, ldv, n, d, g, pc, out, ldo, sm(4), st); break;
+      case 2: launch_combine<8>(V, ldv, n, d, g, pc, out, ldo, sm(8), st); break;
+      case 3: launch_combine<12>(V, ldv, n, d, g, pc, out, ldo, sm(12), st); break;
+      case 4: launch_combine<16>(V, ldv, n, d, g, pc, out, ldo, sm(16), st); break;
+      case 5: launch_combine<20>(V, ldv, n, d, g, pc, out, ldo, sm(20), st); break;
+      case 6: launch_combine<24>(V, ldv, n, d, g, pc, out, ldo, sm(24), st); break;
+      case 7: launch_combine<28>(V, ldv, n, d, g, pc, out, ldo, sm(28), st); break;
+      default: launch_combine<32>(V, ldv, n, d, g, pc, out, ldo, sm(32), st); break;
+    }
+    PPA_CUDA(cudaGetLastError());
+  }
 }
 
 }  // namespace kern

@@ -703,3 +703,30 @@ def test_spmm_columns_bit_exact(cuda, name, gen, p):
     Ao = O.csr_operator(Q)
     for j in range(p):
         assert np.array_equal(AY[j, :n], Ao.apply(Y[j, :n]))
+
+
+@pytest.mark.parametrize("d,p,inplace", [(5, 1, False), (40, 15, False), (40, 20, True),
+                                         (41, 21, True), (7, 7, True), (60, 45, True),
+                                         (60, 45, False), (129, 33, False), (33, 30, True)])
+def test_ts_combine_shapes(cuda, d, p, inplace):
+    # V*G (thick restart in place, Ritz vectors out of place): every
+    # accumulator bucket, the >32-column passes and the wide in-place path,
+    # against the host product (fma-chain roundoff: 1e-13 relative per term)
+    n = 3001
+    ld = (n + 31) // 32 * 32
+    rng = np.random.default_rng(d * 100 + p)
+    Vh = np.zeros((d + 1, ld))
+    Vh[:, :n] = rng.standard_normal((d + 1, n))
+    Gh = rng.standard_normal((p, d))  # column-major d x p
+    V = cuda.tensor(Vh.ravel(), device="cuda")
+    if inplace:
+        ppa.ts_combine(V, ld, n, d, cuda.tensor(Gh.ravel(), device="cuda"), p, V, ld)
+        got = host(V).reshape(d + 1, ld)[:p, :n]
+    else:
+        Out = cuda.zeros(p * ld, dtype=cuda.float64, device="cuda")
+        ppa.ts_combine(V, ld, n, d, cuda.tensor(Gh.ravel(), device="cuda"), p, Out, ld)
+        got = host(Out).reshape(p, ld)[:, :n]
+    ref = Gh @ Vh[:d, :n]
+    assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(ref)) * d
+    if inplace:  # columns p..d untouched
+        assert np.array_equal(host(V).reshape(d + 1, ld)[p:, :n], Vh[p:, :n])
