@@ -4,10 +4,15 @@
 #include "ppa/gmres_poly.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <limits>
+#include <map>
+#include <mutex>
+#include <optional>
+#include <unordered_map>
 #include <stdexcept>
 
 namespace ppa {
@@ -201,9 +206,17 @@ namespace {
 // `complement_base`, when set, is folded into that last pass (tau = I - pi,
 // y = base - pi(A) x).  Counters charge the reference's per-factor
 // increments (src/gmres_poly.cpp:129-143).
+// Work vectors of one chain, supplied by the caller when the chain is
+// captured into a CUDA graph (the graph must not own stream-ordered scratch).
+struct ChainBuffers {
+  double* other = nullptr;  // ping-pong partner of dst
+  double* t1 = nullptr;     // a pair's A x
+};
+
 void apply_poly_csr(const std::vector<PolyFactor>& plan, const CsrOperator& a, const double* v,
                     double* dst, const double* complement_base, CostRecord& rec,
-                    const kern::EpiArgs* outer_fold = nullptr) {
+                    const kern::EpiArgs* outer_fold = nullptr,
+                    const ChainBuffers* cb = nullptr) {
   Context& ctx = current_context();
   const cudaStream_t st = ctx.stream();
   const long long n = a.dim();
@@ -243,9 +256,11 @@ void apply_poly_csr(const std::vector<PolyFactor>& plan, const CsrOperator& a, c
     }
   }
   const int P = static_cast<int>(passes.size());
-  Scratch other(static_cast<size_t>(n));
-  Scratch t1buf(any_two ? static_cast<size_t>(n) : 1);
-  double* bufs[2] = {dst, other.get()};
+  std::optional<Scratch> s_other, s_t1;
+  double* other = cb ? cb->other : (s_other.emplace(static_cast<size_t>(n)), s_other->get());
+  double* t1p = cb ? cb->t1
+                   : (s_t1.emplace(any_two ? static_cast<size_t>(n) : 1), s_t1->get());
+  double* bufs[2] = {dst, other};
   const double* cur = v;
   for (int q = 0; q < P; ++q) {
     const Pass& ps = passes[q];
@@ -262,8 +277,7 @@ void apply_poly_csr(const std::vector<PolyFactor>& plan, const CsrOperator& a, c
         m.a0 = f.c0;
         m.b0 = plan[ps.first + 1].c0;
       }
-      kern::spmv_mp2(a.device(), m, cur, t1buf.get(), out, base, ctx.mp_work(), ctx.sm_count(),
-                     st);
+      kern::spmv_mp2(a.device(), m, cur, t1p, out, base, ctx.mp_work(), ctx.sm_count(), st);
     } else {
       kern::EpiArgs ep;
       ep.base = base;
@@ -278,12 +292,12 @@ void apply_poly_csr(const std::vector<PolyFactor>& plan, const CsrOperator& a, c
         ep.c0 = f.c0;
         kern::spmv(a.device(), cur, out, ep, st);
       } else {
-        kern::spmv(a.device(), cur, t1buf.get(), kern::EpiArgs{}, st);
+        kern::spmv(a.device(), cur, t1p, kern::EpiArgs{}, st);
         ep.mode = kern::Epi::pair;
         ep.c0 = f.c0;
         ep.c1 = f.c1;
         ep.o = cur;
-        kern::spmv(a.device(), t1buf.get(), out, ep, st);
+        kern::spmv(a.device(), t1p, out, ep, st);
       }
     }
     const int mv = f.pair ? 2 : ps.count;
@@ -326,7 +340,8 @@ void apply_poly_generic(const std::vector<PolyFactor>& plan, const LinearOperato
 // between `out` and one scratch vector, assigned backwards so the last one
 // lands in `out`; counters are those of the generic path.
 void apply_nested_csr(const std::vector<PolyFactor>& outer, const std::vector<PolyFactor>& inner,
-                      const CsrOperator& a, const double* v, double* out, CostRecord& rec) {
+                      const CsrOperator& a, const double* v, double* out, CostRecord& rec,
+                      const ChainBuffers* ob = nullptr, const ChainBuffers* ib = nullptr) {
   const long long n = a.dim();
   const int Q = static_cast<int>(outer.size());
   if (Q == 0) {
@@ -335,9 +350,10 @@ void apply_nested_csr(const std::vector<PolyFactor>& outer, const std::vector<Po
   }
   bool any_pair = false;
   for (const PolyFactor& f : outer) any_pair |= f.pair;
-  Scratch other(static_cast<size_t>(n));
-  Scratch t1(any_pair ? static_cast<size_t>(n) : 1);
-  double* bufs[2] = {out, other.get()};
+  std::optional<Scratch> s_other, s_t1;
+  double* other = ob ? ob->other : (s_other.emplace(static_cast<size_t>(n)), s_other->get());
+  double* t1 = ob ? ob->t1 : (s_t1.emplace(any_pair ? static_cast<size_t>(n) : 1), s_t1->get());
+  double* bufs[2] = {out, other};
   const double* cur = v;
   for (int q = 0; q < Q; ++q) {
     const PolyFactor& f = outer[q];
@@ -347,13 +363,13 @@ void apply_nested_csr(const std::vector<PolyFactor>& outer, const std::vector<Po
     fold.oc0 = f.c0;
     if (!f.pair) {
       fold.outer = 1;
-      apply_poly_csr(inner, a, cur, next, cur, rec, &fold);
+      apply_poly_csr(inner, a, cur, next, cur, rec, &fold, ib);
       rec.vops += 2;  // tau's complement + the outer axpy
     } else {
-      apply_poly_csr(inner, a, cur, t1.get(), cur, rec);
+      apply_poly_csr(inner, a, cur, t1, cur, rec, nullptr, ib);
       fold.outer = 2;
       fold.oc1 = f.c1;
-      apply_poly_csr(inner, a, t1.get(), next, t1.get(), rec, &fold);
+      apply_poly_csr(inner, a, t1, next, t1, rec, &fold, ib);
       rec.vops += 4;  // two complements + two outer axpys
     }
     cur = next;
@@ -442,10 +458,59 @@ PolyPrecond add_stability_roots(const PolyPrecond& p, int max_copies_per_root) {
 
 namespace {
 
+// CUDA-graph launch of the fused factor chain (opt-in: PPA_CHAIN_GRAPHS=1).
+// Each apply records its chain (d launches, or d1*d2 for the nested
+// operator) on a private capture stream - recording costs 5-130 us of host
+// time, nothing runs - and updates one instantiated graph per (operator,
+// stream) in place with cudaGraphExecUpdate (same topology, new x / y), then
+// launches it; only the first apply pays for instantiation.  The chain's
+// work vectors belong to the per-stream cache (a graph must not own
+// stream-ordered scratch); the counters are those the recorded chain
+// charged; results are bit-identical to direct launches.  In an isolated
+// 50-factor chain the kernels run back to back without per-launch gaps
+// (config 3: 14.5 -> 13.9 us per factor, config 1: 4.3 -> 1.7 us), but
+// inside a solve the gain is 1-5 % of the extend phase (configs 1, 3, 5) or
+// negative (config 2: the graph boundary stops PDL overlap with the CGS2
+// kernels around it), within run-to-run noise (tools/graph_ab.py) - so
+// chains launch directly by default.
+bool graphs_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("PPA_CHAIN_GRAPHS");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
+struct ChainGraph {
+  cudaStream_t capture = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  DBuffer<double> buf[4];
+  double t_capture = 0.0, t_update = 0.0;  // host microseconds (PPA_GRAPH_DEBUG)
+  long long launches = 0, instantiations = 0;
+
+  ~ChainGraph() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (capture) cudaStreamDestroy(capture);
+  }
+};
+
 class PolyOperator final : public LinearOperator {
  public:
   PolyOperator(OperatorPtr a, PolyPrecond p, bool complement)
       : a_(std::move(a)), p_(std::move(p)), complement_(complement), plan_(factor_plan(p_)) {}
+  ~PolyOperator() override {
+    if (graphs_.empty()) return;
+    cudaDeviceSynchronize();  // no launched chain still reads the buffers
+    static const bool dbg = std::getenv("PPA_GRAPH_DEBUG") != nullptr;
+    for (const auto& kv : graphs_) {
+      const ChainGraph& g = *kv.second;
+      if (dbg && g.launches) {
+        std::fprintf(stderr, "chain graph: %lld launches, %lld instantiations, capture %.1f us, "
+                     "update %.1f us per launch\n", g.launches, g.instantiations,
+                     g.t_capture / g.launches, g.t_update / g.launches);
+      }
+    }
+  }
   int dim() const override { return a_->dim(); }
   OperatorKind kind() const override {
     return complement_ ? OperatorKind::composite : OperatorKind::poly;
@@ -456,21 +521,16 @@ class PolyOperator final : public LinearOperator {
   void apply(const double* x, double* y, CostRecord& rec) const override {
     if (x == y) throw std::invalid_argument("PolyOperator::apply: x and y alias");
     const auto* csr = dynamic_cast<const CsrOperator*>(a_.get());
-    if (csr) {
-      // The complement y = x - w folds into the last fused launch.
-      apply_poly_csr(plan_, *csr, x, y, complement_ ? x : nullptr, rec);
-      if (complement_) rec.vops += 1;
+    const PolyOperator* tau = nested_tau();
+    if ((csr || tau) && graphs_enabled()) {
+      apply_graphed(x, y, rec);
+      return;
+    }
+    if (csr || tau) {
+      run_chain(x, y, rec, nullptr);
       return;
     }
     if (!complement_) {
-      const auto* tau = dynamic_cast<const PolyOperator*>(a_.get());
-      const auto* base_csr = tau ? dynamic_cast<const CsrOperator*>(tau->a_.get()) : nullptr;
-      const char* mpk_env = std::getenv("PPA_ENABLE_MPK");
-      if (tau && tau->complement_ && base_csr && !tau->plan_.empty() &&
-          !(mpk_env && mpk_env[0] == '1')) {
-        apply_nested_csr(plan_, tau->plan_, *base_csr, x, y, rec);
-        return;
-      }
       apply_poly_generic(plan_, *a_, x, y, rec);
       return;
     }
@@ -481,10 +541,105 @@ class PolyOperator final : public LinearOperator {
   }
 
  private:
+  // phi(tau(A)) with tau = I - pi_1 over a CSR matrix: the nested fold.
+  const PolyOperator* nested_tau() const {
+    if (complement_) return nullptr;
+    const auto* tau = dynamic_cast<const PolyOperator*>(a_.get());
+    const auto* base_csr = tau ? dynamic_cast<const CsrOperator*>(tau->a_.get()) : nullptr;
+    const char* mpk_env = std::getenv("PPA_ENABLE_MPK");
+    if (tau && tau->complement_ && base_csr && !tau->plan_.empty() &&
+        !(mpk_env && mpk_env[0] == '1')) {
+      return tau;
+    }
+    return nullptr;
+  }
+
+  // The fused chain on the context's stream; `g` supplies its work vectors.
+  void run_chain(const double* x, double* y, CostRecord& rec, ChainGraph* g) const {
+    if (const auto* csr = dynamic_cast<const CsrOperator*>(a_.get())) {
+      ChainBuffers cb;
+      if (g) cb = ChainBuffers{g->buf[0].get(), g->buf[1].get()};
+      // The complement y = x - w folds into the last fused launch.
+      apply_poly_csr(plan_, *csr, x, y, complement_ ? x : nullptr, rec, nullptr, g ? &cb : nullptr);
+      if (complement_) rec.vops += 1;
+      return;
+    }
+    const PolyOperator* tau = nested_tau();
+    const auto& base_csr = dynamic_cast<const CsrOperator&>(*tau->a_);
+    ChainBuffers ob, ib;
+    if (g) {
+      ob = ChainBuffers{g->buf[0].get(), g->buf[1].get()};
+      ib = ChainBuffers{g->buf[2].get(), g->buf[3].get()};
+    }
+    apply_nested_csr(plan_, tau->plan_, base_csr, x, y, rec, g ? &ob : nullptr,
+                     g ? &ib : nullptr);
+  }
+
+  void apply_graphed(const double* x, double* y, CostRecord& rec) const {
+    Context& ctx = current_context();
+    const cudaStream_t st = ctx.stream();
+    ChainGraph* g;
+    {
+      std::lock_guard<std::mutex> lock(gmu_);
+      std::unique_ptr<ChainGraph>& slot = graphs_[st];
+      if (!slot) slot = std::make_unique<ChainGraph>();
+      g = slot.get();
+    }
+    if (!g->capture) {
+      PPA_CUDA(cudaStreamCreateWithFlags(&g->capture, cudaStreamNonBlocking));
+      for (auto& b : g->buf) b.resize(static_cast<size_t>(dim()));
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaGraph_t graph = nullptr;
+    CostRecord d;
+    const cudaStream_t prev = ctx.swap_stream(g->capture);
+    PPA_CUDA(cudaStreamBeginCapture(g->capture, cudaStreamCaptureModeThreadLocal));
+    try {
+      run_chain(x, y, d, g);
+    } catch (...) {
+      cudaStreamEndCapture(g->capture, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      ctx.swap_stream(prev);
+      throw;
+    }
+    const cudaError_t ce = cudaStreamEndCapture(g->capture, &graph);
+    ctx.swap_stream(prev);
+    PPA_CUDA(ce);
+    const auto t1 = std::chrono::steady_clock::now();
+    bool updated = false;
+    if (g->exec) {
+      cudaGraphExecUpdateResultInfo info;
+      updated = cudaGraphExecUpdate(g->exec, graph, &info) == cudaSuccess;
+      if (!updated) {
+        cudaGetLastError();
+        cudaGraphExecDestroy(g->exec);
+        g->exec = nullptr;
+      }
+    }
+    if (!updated) {
+      const cudaError_t ie = cudaGraphInstantiate(&g->exec, graph, 0);
+      if (ie != cudaSuccess) cudaGraphDestroy(graph);
+      PPA_CUDA(ie);
+      ++g->instantiations;
+    }
+    cudaGraphDestroy(graph);
+    const auto t2 = std::chrono::steady_clock::now();
+    // replays on one stream are ordered, so they can share g->buf
+    PPA_CUDA(cudaGraphLaunch(g->exec, st));
+    ++g->launches;
+    g->t_capture += std::chrono::duration<double, std::micro>(t1 - t0).count();
+    g->t_update += std::chrono::duration<double, std::micro>(t2 - t1).count();
+    rec.mvps += d.mvps;
+    rec.dots += d.dots;
+    rec.vops += d.vops;
+  }
+
   OperatorPtr a_;
   PolyPrecond p_;
   bool complement_;
   std::vector<PolyFactor> plan_;
+  mutable std::mutex gmu_;
+  mutable std::map<cudaStream_t, std::unique_ptr<ChainGraph>> graphs_;
 };
 
 }  // namespace

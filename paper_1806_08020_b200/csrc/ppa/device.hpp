@@ -99,6 +99,13 @@ class Context {
       stream_ = s;
     }
   }
+  /// Replace the stream without draining the old one: only for recording a
+  /// launch sequence into a CUDA graph on a capture stream (nothing runs).
+  cudaStream_t swap_stream(cudaStream_t s) {
+    const cudaStream_t old = stream_;
+    stream_ = s;
+    return old;
+  }
   ReduceWorkspace& ws() { return ws_; }
   int sm_count() const { return sm_count_; }
   void sync() const;

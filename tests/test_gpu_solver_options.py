@@ -166,3 +166,41 @@ def test_breakdown_inside_solve_matches_oracle(cuda, degree):
         (o["cost"]["mvps"], o["cost"]["dots"], o["cost"]["vops"])
     assert np.allclose(np.sort(r["eigenvalues"].real), np.sort(o["eigenvalues"].real),
                        rtol=1e-10)
+
+
+_GRAPH_CHILD = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, %r)
+import paper_1806_08020_b200 as ppa
+A = ppa.make_csr_operator(ppa.CsrMatrix.convection_diffusion_const(70, 0.5))
+out = {}
+r = ppa.solve(A, ppa.SolveConfig(m=30, k=15, nev=6, degree=12, seed=4, max_cycles=40))
+out["single"] = [r["eigenvalues"].real.tolist(), r["eigenvalues"].imag.tolist(),
+                 r["residuals"].tolist(), r["cost"], r["cycles"]]
+r = ppa.solve_double(A, ppa.SolveConfig(m=30, k=15, nev=6, double_d1=4, double_d2=5, seed=4,
+                                        max_cycles=40))
+out["double"] = [r["eigenvalues"].real.tolist(), r["eigenvalues"].imag.tolist(),
+                 r["residuals"].tolist(), r["cost"], r["cycles"]]
+print(json.dumps(out))
+"""
+
+
+def test_chain_graphs_bit_identical(cuda):
+    # PPA_CHAIN_GRAPHS=1 (recorded chains, one graph updated in place per
+    # operator and stream): same eigenpairs, residuals and counters, bit for
+    # bit, as direct launches - single and nested polynomial operators
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for flag in ("0", "1"):
+        env = dict(os.environ, PPA_CHAIN_GRAPHS=flag)
+        p = subprocess.run([sys.executable, "-c", _GRAPH_CHILD % root], env=env,
+                           capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stderr[-2000:]
+        res[flag] = json.loads(p.stdout.strip().splitlines()[-1])
+    assert res["0"] == res["1"]
