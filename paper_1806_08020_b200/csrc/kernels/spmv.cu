@@ -273,55 +273,6 @@ void spmm(const CsrDevice& a, const double* Y, long long ldy, int p, double* AY,
   PPA_CUDA(cudaGetLastError());
 }
 
-bool build_sell32(const int* row_ptr, const int* col_idx, const double* values, int n, int sigma,
-                  std::vector<long long>& slice_ptr, std::vector<int>& cols,
-                  std::vector<double>& vals, std::vector<int>& perm) {
-  const int ns = (n + 31) / 32;
-  auto len = [&](int r) { return row_ptr[r + 1] - row_ptr[r]; };
-  perm.clear();
-  if (sigma > 1) {
-    // sort rows by decreasing length inside each sigma-window (stable, so
-    // the layout is deterministic); rows never leave their window
-    perm.resize(n);
-    for (int i = 0; i < n; ++i) perm[i] = i;
-    for (int w0 = 0; w0 < n; w0 += sigma) {
-      const int w1 = std::min(n, w0 + sigma);
-      std::stable_sort(perm.begin() + w0, perm.begin() + w1,
-                       [&](int a, int b) { return len(a) > len(b); });
-    }
-  }
-  auto row_of = [&](int idx) { return perm.empty() ? idx : perm[idx]; };
-  slice_ptr.assign(static_cast<size_t>(ns) + 1, 0);
-  long long total = 0;
-  for (int s = 0; s < ns; ++s) {
-    int w = 0;
-    for (int i = s * 32; i < std::min(n, s * 32 + 32); ++i) w = std::max(w, len(row_of(i)));
-    total += 32LL * w;
-    slice_ptr[s + 1] = total;
-  }
-  const long long nnz = row_ptr[n];
-  if (static_cast<double>(total) > kSellMaxPadding * static_cast<double>(nnz) + 32.0 * 64) {
-    slice_ptr.clear();
-    perm.clear();
-    return false;
-  }
-  cols.assign(static_cast<size_t>(total), -1);
-  vals.assign(static_cast<size_t>(total), 0.0);
-  for (int s = 0; s < ns; ++s) {
-    const long long b0 = slice_ptr[s];
-    for (int l = 0; l < 32; ++l) {
-      const int i = s * 32 + l;
-      if (i >= n) break;
-      const int r = row_of(i);
-      for (int p = row_ptr[r], k = 0; p < row_ptr[r + 1]; ++p, ++k) {
-        cols[b0 + 32LL * k + l] = col_idx[p];
-        vals[b0 + 32LL * k + l] = values[p];
-      }
-    }
-  }
-  return true;
-}
-
 void build_row_blocks(const int* row_ptr, int n, int max_rows, int max_nnz,
                       std::vector<int>& blk_row) {
   blk_row.clear();

@@ -23,8 +23,6 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
-#include <map>
-#include <unordered_map>
 #include <vector>
 
 #include "common.cuh"
@@ -534,103 +532,6 @@ void spmm_dia(const CsrDevice& a, const double* Y, long long ldy, int p, double*
     default: launch_spmm_dia_nw<8>(a, Y, ldy, p, AY, ldo, st); break;
   }
   PPA_CUDA(cudaGetLastError());
-}
-
-bool build_dia(const int* row_ptr, const int* col_idx, const double* values, int n,
-               std::vector<int>& offsets, int& stride, std::vector<unsigned char>& codes,
-               std::vector<double>& dict) {
-  offsets.clear();
-  codes.clear();
-  dict.clear();
-  const long long nnz = row_ptr[n];
-  if (n <= 0 || nnz <= 0) return false;
-  std::map<long long, long long> diag;  // offset -> count (sorted)
-  for (int r = 0; r < n; ++r) {
-    for (int p = row_ptr[r]; p < row_ptr[r + 1]; ++p) {
-      ++diag[static_cast<long long>(col_idx[p]) - r];
-      if (static_cast<int>(diag.size()) > kDiaMaxDiag) return false;
-    }
-  }
-  const int nd = static_cast<int>(diag.size());
-  // every diagonal must be well filled: the gathers of absent entries are
-  // predicated off, but their code bytes are still streamed
-  if (static_cast<double>(nd) * n > kDiaMaxFill * static_cast<double>(nnz)) return false;
-  std::unordered_map<uint64_t, int> index;
-  for (long long p = 0; p < nnz; ++p) {
-    uint64_t bits;
-    std::memcpy(&bits, values + p, sizeof bits);
-    if (index.count(bits)) continue;
-    if (static_cast<int>(index.size()) == kDiaMaxDict) return false;
-    index.emplace(bits, static_cast<int>(dict.size()));
-    dict.push_back(values[p]);
-  }
-  stride = nd <= 4 ? 4 : nd <= 8 ? 8 : nd <= 16 ? 16 : 32;
-  std::unordered_map<long long, int> slot;
-  for (const auto& kv : diag) {
-    slot.emplace(kv.first, static_cast<int>(offsets.size()));
-    offsets.push_back(static_cast<int>(kv.first));
-  }
-  const long long rows = (static_cast<long long>(n) + 31) / 32 * 32;
-  codes.assign(static_cast<size_t>(rows * stride), static_cast<unsigned char>(kDiaAbsent));
-  for (int r = 0; r < n; ++r) {
-    for (int p = row_ptr[r]; p < row_ptr[r + 1]; ++p) {
-      uint64_t bits;
-      std::memcpy(&bits, values + p, sizeof bits);
-      const int j = slot.at(static_cast<long long>(col_idx[p]) - r);
-      codes[static_cast<size_t>(r) * stride + j] = static_cast<unsigned char>(index.at(bits));
-    }
-  }
-  return true;
-}
-
-bool build_dia_regular(const std::vector<unsigned char>& codes, int n, int ndiag, int stride,
-                       const std::vector<double>& dict, std::vector<unsigned>& mask,
-                       std::vector<int>& irr_rows, std::vector<unsigned char>& irr_codes,
-                       std::vector<double>& dflt) {
-  mask.clear();
-  irr_rows.clear();
-  irr_codes.clear();
-  dflt.clear();
-  if (ndiag > kDiaRegularMaxDiag || n <= 0) return false;
-  // default code of a diagonal: its most frequent present code
-  std::vector<int> dcode(ndiag, -1);
-  for (int j = 0; j < ndiag; ++j) {
-    std::vector<long long> cnt(256, 0);
-    for (int r = 0; r < n; ++r) ++cnt[codes[static_cast<size_t>(r) * stride + j]];
-    long long best = 0;
-    for (int c = 0; c < static_cast<int>(kDiaAbsent); ++c) {
-      if (cnt[c] > best) {
-        best = cnt[c];
-        dcode[j] = c;
-      }
-    }
-    if (dcode[j] < 0) return false;
-    dflt.push_back(dict[dcode[j]]);
-  }
-  auto regular = [&](int r) {
-    for (int j = 0; j < ndiag; ++j) {
-      if (codes[static_cast<size_t>(r) * stride + j] != dcode[j]) return false;
-    }
-    return true;
-  };
-  mask.assign(static_cast<size_t>((n + 31) / 32), 0u);
-  for (int r = 0; r < n; ++r) {
-    if (regular(r)) {
-      mask[r >> 5] |= 1u << (r & 31);
-    } else {
-      irr_rows.push_back(r);
-      irr_codes.insert(irr_codes.end(), codes.begin() + static_cast<long long>(r) * stride,
-                       codes.begin() + static_cast<long long>(r + 1) * stride);
-    }
-  }
-  if (2 * static_cast<long long>(irr_rows.size()) > n) {
-    mask.clear();
-    irr_rows.clear();
-    irr_codes.clear();
-    dflt.clear();
-    return false;
-  }
-  return true;
 }
 
 }  // namespace kern

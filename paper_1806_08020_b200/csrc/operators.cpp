@@ -119,97 +119,70 @@ CsrOperator::CsrOperator(const CsrMatrix& m, OperatorKind kind, std::vector<doub
   }
   dev_.bandwidth = bw;
 
-  std::vector<long long> sp;
-  std::vector<int> sc, perm;
-  std::vector<double> sv;
-  bool sell = false;
-  int sigma = 1;
-  if (layout != CsrLayout::csr && !std::getenv("PPA_DISABLE_SELL")) {
-    sell = kern::build_sell32(m.row_ptr.data(), m.col_idx.data(), m.values.data(), n_, 1, sp, sc,
-                              sv, perm);
-    if (!sell && !std::getenv("PPA_DISABLE_SIGMA")) {
-      sigma = kern::kSellSigma;
-      sell = kern::build_sell32(m.row_ptr.data(), m.col_idx.data(), m.values.data(), n_, sigma,
-                                sp, sc, sv, perm);
-    }
+  // Layouts are built on the device from the CSR copy (kernels/layout_build.cu):
+  // the diagonal-coded form first when allowed (stencils; it needs no SELL
+  // copy), else SELL-32 (sigma-sorted when unsorted slices pad too much),
+  // then packed SELL-32 over its row order.
+  if (layout == CsrLayout::csr || std::getenv("PPA_DISABLE_SELL")) return;
+  const cudaStream_t st = current_context().stream();
+  const bool dia_ok = layout == CsrLayout::automatic || layout == CsrLayout::dia;
+  const bool packed_ok = dia_ok || layout == CsrLayout::sell32_packed;
+  if (dia_ok && upload_dia(st)) {
+    dev_.nslices = (n_ + 31) / 32;
+    return;
   }
-  if (sell) {
-    slice_ptr_.resize(sp.size());
-    sell_col_.resize(sc.size() + 32);
-    sell_val_.resize(sv.size() + 32);
-    PPA_CUDA(cudaMemcpy(slice_ptr_.get(), sp.data(), sp.size() * sizeof(long long),
-                        cudaMemcpyHostToDevice));
-    if (!sc.empty()) {
-      PPA_CUDA(cudaMemcpy(sell_col_.get(), sc.data(), sc.size() * sizeof(int),
-                          cudaMemcpyHostToDevice));
-      PPA_CUDA(cudaMemcpy(sell_val_.get(), sv.data(), sv.size() * sizeof(double),
-                          cudaMemcpyHostToDevice));
+  int sigma = 1;
+  bool sell = kern::build_sell32_device(row_ptr_.get(), col_idx_.get(), values_.get(), n_, nnz_,
+                                        1, sell_, st);
+  if (!sell && !std::getenv("PPA_DISABLE_SIGMA")) {
+    sigma = kern::kSellSigma;
+    sell = kern::build_sell32_device(row_ptr_.get(), col_idx_.get(), values_.get(), n_, nnz_,
+                                     sigma, sell_, st);
+  }
+  if (!sell) return;
+  dev_.slice_ptr = sell_.slice_ptr.get();
+  dev_.sell_col = sell_.cols.get();
+  dev_.sell_val = sell_.vals.get();
+  dev_.sell_perm = sell_.perm.size() ? sell_.perm.get() : nullptr;
+  dev_.nslices = sell_.nslices;
+  dev_.sell_entries = sell_.total;
+  dev_.sell_sigma = sigma;
+  if (packed_ok) {
+    std::vector<int> perm;
+    if (dev_.sell_perm) {
+      perm.resize(static_cast<size_t>(n_));
+      PPA_CUDA(cudaMemcpyAsync(perm.data(), dev_.sell_perm, perm.size() * sizeof(int),
+                               cudaMemcpyDeviceToHost, st));
+      PPA_CUDA(cudaStreamSynchronize(st));
     }
-    if (!perm.empty()) {
-      sell_perm_.resize(perm.size());
-      PPA_CUDA(cudaMemcpy(sell_perm_.get(), perm.data(), perm.size() * sizeof(int),
-                          cudaMemcpyHostToDevice));
-      dev_.sell_perm = sell_perm_.get();
-    }
-    dev_.slice_ptr = slice_ptr_.get();
-    dev_.sell_col = sell_col_.get();
-    dev_.sell_val = sell_val_.get();
-    dev_.nslices = static_cast<int>(sp.size()) - 1;
-    dev_.sell_entries = sp.back();
-    dev_.sell_sigma = sigma;
-    const bool dia_ok = layout == CsrLayout::automatic || layout == CsrLayout::dia;
-    const bool packed_ok = dia_ok || layout == CsrLayout::sell32_packed;
-    if (!(dia_ok && upload_dia(m)) && packed_ok) upload_packed(m, perm);
+    upload_packed(m, perm);
   }
 }
 
-// Diagonal-coded layout for stencil matrices (kernels/spmv_dia.cu);
-// PPA_DISABLE_DIA skips it.
-bool CsrOperator::upload_dia(const CsrMatrix& m) {
+// Diagonal-coded layout for stencil matrices (kernels/spmv_dia.cu), built on
+// the device; PPA_DISABLE_DIA skips it, PPA_DISABLE_DIA_REGULAR keeps every
+// row's codes.
+bool CsrOperator::upload_dia(cudaStream_t st) {
   if (std::getenv("PPA_DISABLE_DIA")) return false;
-  std::vector<int> offs;
-  std::vector<unsigned char> codes;
-  std::vector<double> dict;
-  int stride = 0;
-  if (!kern::build_dia(m.row_ptr.data(), m.col_idx.data(), m.values.data(), n_, offs, stride,
-                       codes, dict)) {
+  if (!kern::build_dia_device(row_ptr_.get(), col_idx_.get(), values_.get(), n_, nnz_,
+                              !std::getenv("PPA_DISABLE_DIA_REGULAR"), dia_, st)) {
     return false;
   }
-  dia_code_.resize(codes.size());
-  PPA_CUDA(cudaMemcpy(dia_code_.get(), codes.data(), codes.size(), cudaMemcpyHostToDevice));
-  dia_dict_.resize(dict.size());
-  PPA_CUDA(cudaMemcpy(dia_dict_.get(), dict.data(), dict.size() * sizeof(double),
+  dia_dict_.resize(dia_.dict.size());
+  PPA_CUDA(cudaMemcpy(dia_dict_.get(), dia_.dict.data(), dia_.dict.size() * sizeof(double),
                       cudaMemcpyHostToDevice));
-  dev_.dia_code = dia_code_.get();
+  dev_.dia_code = dia_.codes.get();
   dev_.dia_dict = dia_dict_.get();
-  dev_.dia_ndict = static_cast<int>(dict.size());
-  dev_.dia_ndiag = static_cast<int>(offs.size());
-  dev_.dia_stride = stride;
-  for (size_t j = 0; j < offs.size(); ++j) dev_.dia_off[j] = offs[j];
-  std::vector<unsigned> mask;
-  std::vector<int> irr;
-  std::vector<unsigned char> irr_codes;
-  std::vector<double> dflt;
-  if (!std::getenv("PPA_DISABLE_DIA_REGULAR") &&
-      kern::build_dia_regular(codes, n_, dev_.dia_ndiag, stride, dict, mask, irr, irr_codes,
-                              dflt)) {
-    dia_mask_.resize(mask.size());
-    PPA_CUDA(cudaMemcpy(dia_mask_.get(), mask.data(), mask.size() * sizeof(unsigned),
-                        cudaMemcpyHostToDevice));
-    // one row of slack: the irregular list may be empty
-    dia_irr_rows_.resize(irr.size() + 1);
-    dia_irr_codes_.resize(irr_codes.size() + static_cast<size_t>(stride));
-    if (!irr.empty()) {
-      PPA_CUDA(cudaMemcpy(dia_irr_rows_.get(), irr.data(), irr.size() * sizeof(int),
-                          cudaMemcpyHostToDevice));
-      PPA_CUDA(cudaMemcpy(dia_irr_codes_.get(), irr_codes.data(), irr_codes.size(),
-                          cudaMemcpyHostToDevice));
-    }
-    dev_.dia_mask = dia_mask_.get();
-    dev_.dia_irr_rows = dia_irr_rows_.get();
-    dev_.dia_irr_codes = dia_irr_codes_.get();
-    dev_.dia_nirr = static_cast<long long>(irr.size());
-    for (size_t j = 0; j < dflt.size(); ++j) dev_.dia_dflt[j] = dflt[j];
+  dev_.dia_ndict = static_cast<int>(dia_.dict.size());
+  dev_.dia_ndiag = dia_.ndiag;
+  dev_.dia_stride = dia_.stride;
+  for (int j = 0; j < dia_.ndiag; ++j) dev_.dia_off[j] = dia_.offsets[j];
+  if (dia_.regular) {
+    dev_.dia_mask = dia_.mask.get();
+    dev_.dia_irr_rows = dia_.irr_rows.get();
+    dev_.dia_irr_codes = dia_.irr_codes.get();
+    dev_.dia_nirr = dia_.nirr;
+    for (int j = 0; j < dia_.ndiag; ++j) dev_.dia_dflt[j] = dia_.defaults[j];
   }
   return true;
 }

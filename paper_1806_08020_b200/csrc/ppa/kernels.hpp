@@ -72,21 +72,8 @@ constexpr unsigned kDiaAbsent = 0xffu;
 /// Largest (diagonals x n) / nnz accepted for the diagonal layout.
 constexpr double kDiaMaxFill = 1.5;
 
-/// Host-side diagonal-coded construction; false when the matrix has more
-/// than kDiaMaxDiag diagonals, more than kDiaMaxDict distinct values or a
-/// fill above kDiaMaxFill.
-bool build_dia(const int* row_ptr, const int* col_idx, const double* values, int n,
-               std::vector<int>& offsets, int& stride, std::vector<unsigned char>& codes,
-               std::vector<double>& dict);
 /// Largest diagonal count of the regular-row kernel.
 constexpr int kDiaRegularMaxDiag = 16;
-/// Regular-row form from build_dia's codes; false unless at least half the
-/// rows are regular (and ndiag <= kDiaRegularMaxDiag).
-bool build_dia_regular(const std::vector<unsigned char>& codes, int n, int ndiag, int stride,
-                       const std::vector<double>& dict, std::vector<unsigned>& mask,
-                       std::vector<int>& irr_rows, std::vector<unsigned char>& irr_codes,
-                       std::vector<double>& dflt);
-
 /// Entries per lane per packed load group and the padding marker.
 constexpr int kPackChunk = 4;
 constexpr short kPackPad = -32768;
@@ -124,12 +111,41 @@ constexpr double kSellMaxPadding = 1.15;
 /// Sorting window used when unsorted SELL-32 pads too much (irregular rows).
 constexpr int kSellSigma = 16384;
 
-/// Host-side SELL-32 construction from CSR.  sigma > 1 sorts rows by length
-/// inside sigma-row windows and returns the slice-row -> row permutation.
-/// Returns false when the padding exceeds kSellMaxPadding.
-bool build_sell32(const int* row_ptr, const int* col_idx, const double* values, int n, int sigma,
-                  std::vector<long long>& slice_ptr, std::vector<int>& cols,
-                  std::vector<double>& vals, std::vector<int>& perm);
+/// Device-built SELL-32 (layout_build.cu): owns the arrays CsrDevice points to.
+struct DevSell {
+  DBuffer<long long> slice_ptr;  // [nslices+1]
+  DBuffer<int> cols;             // [total+32], padding -1
+  DBuffer<double> vals;          // [total+32], padding 0
+  DBuffer<int> perm;             // empty when sigma == 1
+  long long total = 0;
+  int nslices = 0;
+};
+/// SELL-32 from the device CSR; sigma > 1 stably sorts rows by decreasing
+/// length inside sigma-row windows (same order as a host stable sort).
+/// False (nothing kept) when the padding exceeds kSellMaxPadding.
+bool build_sell32_device(const int* row_ptr, const int* col_idx, const double* values, int n,
+                         long long nnz, int sigma, DevSell& out, cudaStream_t st);
+
+/// Device-built diagonal-coded layout and, when `regular`, its regular-row form.
+struct DevDia {
+  std::vector<int> offsets;  // increasing
+  std::vector<double> dict;  // ascending bit patterns
+  int ndiag = 0;
+  int stride = 0;
+  DBuffer<unsigned char> codes;  // [round32(n) * stride]
+  bool regular = false;
+  std::vector<double> defaults;  // per diagonal
+  DBuffer<unsigned> mask;
+  DBuffer<int> irr_rows;
+  DBuffer<unsigned char> irr_codes;
+  long long nirr = 0;
+};
+/// Diagonal-coded layout from the device CSR; false when the matrix has more
+/// than kDiaMaxDiag diagonals, more than kDiaMaxDict distinct values or a
+/// fill above kDiaMaxFill.  The regular-row form is added when `want_regular`,
+/// ndiag <= kDiaRegularMaxDiag and at least half the rows are regular.
+bool build_dia_device(const int* row_ptr, const int* col_idx, const double* values, int n,
+                      long long nnz, bool want_regular, DevDia& out, cudaStream_t st);
 
 /// Row-block capacities of the streaming SpMV (must match spmv.cu).
 constexpr int kSpmvThreads = 256;

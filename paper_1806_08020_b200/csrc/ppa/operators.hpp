@@ -115,18 +115,18 @@ class CsrOperator final : public LinearOperator {
   double nnzr_ = 0.0;
   OperatorKind kind_;
   std::vector<double> diag_;
-  DBuffer<int> row_ptr_, col_idx_, blk_row_, sell_col_, sell_perm_;
-  DBuffer<double> values_, sell_val_;
-  DBuffer<long long> slice_ptr_, pk_ptr_;
+  DBuffer<int> row_ptr_, col_idx_, blk_row_;
+  DBuffer<double> values_;
+  DBuffer<long long> pk_ptr_;
+  kern::DevSell sell_;
+  kern::DevDia dia_;
   DBuffer<short> pk_col_;
-  DBuffer<unsigned char> pk_code_, dia_code_, dia_irr_codes_;
-  DBuffer<unsigned> dia_mask_;
-  DBuffer<int> dia_irr_rows_;
+  DBuffer<unsigned char> pk_code_;
   DBuffer<double> pk_val_, pk_dict_, dia_dict_;
   kern::CsrDevice dev_;
 
   void upload_packed(const CsrMatrix& m, const std::vector<int>& perm);
-  bool upload_dia(const CsrMatrix& m);
+  bool upload_dia(cudaStream_t st);
 };
 
 OperatorPtr make_csr_operator(const CsrMatrix& matrix,
