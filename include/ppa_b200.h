@@ -121,6 +121,11 @@ int ppa_csr_model_bytes(const ppa_op* op, double* bytes, long long* nnz);
    dict_size = value-table size (0: fp64 values) */
 int ppa_csr_layout(const ppa_op* op, int* layout, double* stream_bytes, int* sigma,
                    int* dict_size);
+/* CSR operators: *supported = 1 when consecutive polynomial factors (two real
+   roots, or a conjugate pair) run as one temporally blocked pass over the
+   diagonal layout (stencils).  No reference
+   counterpart: an introspection hook next to ppa_csr_layout. */
+int ppa_csr_two_factor_pass(const ppa_op* op, int* supported);
 
 /* ---- polynomial -------------------------------------------------------- */
 /* apply_poly (src/gmres_poly.cpp:117-147): out_dev = pi(A) v_dev */

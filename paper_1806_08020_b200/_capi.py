@@ -119,6 +119,7 @@ def lib():
             "ppa_factor_plan": [vp, vp, C.c_int, _ip, vp, vp, _ip],
             "ppa_host_csr_multiply": [vp, vp, vp],
             "ppa_csr_operator_layout": [vp, C.c_int, C.POINTER(vp)],
+            "ppa_csr_two_factor_pass": [vp, _ip],
             "ppa_arnoldi_set_orthogonalization": [vp, C.c_int],
             "ppa_apply_poly": [vp, vp, C.c_int, vp, vp, vp, C.POINTER(CostRecord)],
             "ppa_build_gmres_poly": [vp, vp, C.c_int, vp, vp, _ip, _ip, C.POINTER(CostRecord)],
@@ -377,8 +378,11 @@ class LinearOperator:
         sb = C.c_double()
         _check(lib().ppa_csr_layout(self._h, C.byref(lay), C.byref(sb), C.byref(sig),
                                     C.byref(nd)))
+        two = C.c_int()
+        _check(lib().ppa_csr_two_factor_pass(self._h, C.byref(two)))
         return {"layout": ("csr", "sell32", "sell32_packed", "dia_coded")[lay.value],
-                "stream_bytes": sb.value, "sigma": sig.value, "dict_size": nd.value}
+                "stream_bytes": sb.value, "sigma": sig.value, "dict_size": nd.value,
+                "two_factor_pass": bool(two.value)}
 
 
 LAYOUTS = {"auto": 0, "csr": 1, "sell32": 2, "sell32_packed": 3, "dia_coded": 4}

@@ -439,6 +439,16 @@ int ppa_csr_layout(const ppa_op* op, int* layout, double* stream_bytes, int* sig
   });
 }
 
+int ppa_csr_two_factor_pass(const ppa_op* op, int* supported) {
+  return guard([&] {
+    need(op, "ppa_csr_two_factor_pass");
+    need(supported, "ppa_csr_two_factor_pass");
+    const auto* c = dynamic_cast<const ppa::CsrOperator*>(op->p.get());
+    if (!c) throw std::invalid_argument("ppa_csr_two_factor_pass: not a CSR operator");
+    *supported = ppa::kern::dia2_supported(c->device()) ? 1 : 0;
+  });
+}
+
 int ppa_apply_poly(const double* re, const double* im, int nroots, const ppa_op* a,
                    const double* v, double* out, ppa_cost* cost) {
   return guard([&] {

@@ -235,6 +235,14 @@ void apply_poly_csr(const std::vector<PolyFactor>& plan, const CsrOperator& a, c
   // launches on B200.
   const char* mpk_env = std::getenv("PPA_ENABLE_MPK");
   const bool mp = mpk_env && mpk_env[0] == '1' && kern::mp2_supported(a.device()) && !outer_fold;
+  std::optional<Scratch> s_other, s_t1;
+  double* other = cb ? cb->other : (s_other.emplace(static_cast<size_t>(n)), s_other->get());
+  // Temporal blocking over stencils (kernels/spmv_dia2.cu): two real roots or
+  // one pair per pass, x read once.  Its bulk copies need 16-byte aligned
+  // sources (the chain's inputs: v and the ping-pong pair).
+  auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  const bool d2 = !mp && kern::dia2_supported(a.device()) && aligned(v) && aligned(dst) &&
+                  aligned(other);
   struct Pass {
     int first;
     int count;  // factors in the pass (1 or 2 real roots, or 1 pair)
@@ -246,7 +254,7 @@ void apply_poly_csr(const std::vector<PolyFactor>& plan, const CsrOperator& a, c
       passes.push_back({k, 1});
       any_two = true;
       k += 1;
-    } else if (mp && k + 1 < K && !plan[k + 1].pair) {
+    } else if ((mp || d2) && k + 1 < K && !plan[k + 1].pair) {
       passes.push_back({k, 2});
       any_two = true;
       k += 2;
@@ -255,9 +263,13 @@ void apply_poly_csr(const std::vector<PolyFactor>& plan, const CsrOperator& a, c
       k += 1;
     }
   }
+  // the outer fold of a nested polynomial rides on a single-factor launch
+  if (d2 && outer_fold && passes.back().count == 2) {
+    const int k = passes.back().first;
+    passes.back().count = 1;
+    passes.push_back({k + 1, 1});
+  }
   const int P = static_cast<int>(passes.size());
-  std::optional<Scratch> s_other, s_t1;
-  double* other = cb ? cb->other : (s_other.emplace(static_cast<size_t>(n)), s_other->get());
   double* t1p = cb ? cb->t1
                    : (s_t1.emplace(any_two ? static_cast<size_t>(n) : 1), s_t1->get());
   double* bufs[2] = {dst, other};
@@ -267,7 +279,18 @@ void apply_poly_csr(const std::vector<PolyFactor>& plan, const CsrOperator& a, c
     double* out = bufs[(P - 1 - q) & 1];  // the last pass lands in dst
     const double* base = (q == P - 1) ? complement_base : nullptr;
     const PolyFactor& f = plan[ps.first];
-    if (ps.count == 2 || (f.pair && mp)) {
+    const bool fold_here = base && outer_fold;
+    if (d2 && !fold_here && (ps.count == 2 || f.pair)) {
+      kern::Mp2Pass m;
+      m.pair = f.pair;
+      m.a0 = f.c0;
+      if (f.pair) {
+        m.a1 = f.c1;
+      } else {
+        m.b0 = plan[ps.first + 1].c0;
+      }
+      kern::spmv_dia2(a.device(), m, cur, out, base, st);
+    } else if (ps.count == 2 || (f.pair && mp)) {
       kern::Mp2Pass m;
       m.pair = f.pair;
       if (f.pair) {

@@ -262,6 +262,26 @@ __global__ void k_dia_regular(const unsigned char* __restrict__ codes, int n, in
   if ((threadIdx.x & 31) == 0) mask[i >> 5] = b;
 }
 
+// presence byte per row (bit j: an entry on diagonal j); *bad set when a
+// present entry differs from its diagonal's default code
+__global__ void k_dia_presence(const unsigned char* __restrict__ codes, int n, int stride,
+                               const DiaDefaults d, unsigned char* __restrict__ pres,
+                               int* __restrict__ bad) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned b = 0;
+  bool ok = true;
+  for (int j = 0; j < d.ndiag; ++j) {
+    const unsigned c = codes[i * stride + j];
+    if (c != kDiaAbsent) {
+      b |= 1u << j;
+      ok = ok && c == d.code[j];
+    }
+  }
+  pres[i] = static_cast<unsigned char>(b);
+  if (!ok) atomicOr(bad, 1);
+}
+
 __global__ void k_gather_codes(const unsigned char* __restrict__ codes, const int* __restrict__ rows,
                                long long nrows, int stride, unsigned char* __restrict__ out) {
   const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -470,6 +490,28 @@ bool build_dia_device(const int* row_ptr, const int* col_idx, const double* valu
   }
   out.nirr = nirr;
   out.regular = true;
+  out.pres.release();
+  if (nd <= 8 && n > 0) {
+    // zero padding of 4 D + 64 rows (a multiple of 16) on both sides (D = the
+    // widest offset): the two-factor pass copies presence bytes of rows just
+    // outside the matrix, from 16-byte aligned starts
+    const long long D = std::max(std::abs(static_cast<long long>(out.offsets.front())),
+                                 std::abs(static_cast<long long>(out.offsets.back())));
+    out.pres_pad = (4 * D + 64 + 15) & ~15LL;
+    const size_t total = static_cast<size_t>(n + 2 * out.pres_pad + 16);
+    out.pres.resize(total);
+    PPA_CUDA(cudaMemsetAsync(out.pres.get(), 0, total, st));
+    Tmp bad(sizeof(int), st);
+    PPA_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+    k_dia_presence<<<blocks_for(n, 256), 256, 0, st>>>(out.codes.get(), n, stride, d,
+                                                       out.pres.get() + out.pres_pad,
+                                                       bad.as<int>());
+    PPA_CUDA(cudaGetLastError());
+    int hbad = 0;
+    PPA_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof hbad, cudaMemcpyDeviceToHost, st));
+    PPA_CUDA(cudaStreamSynchronize(st));
+    if (hbad) out.pres.release();
+  }
   PPA_CUDA(cudaStreamSynchronize(st));
   return true;
 }

@@ -64,6 +64,12 @@ struct CsrDevice {
   const unsigned char* dia_irr_codes = nullptr;
   long long dia_nirr = 0;
   double dia_dflt[32] = {};
+  // Presence form (spmv_dia2.cu): bit j of dia_pres[r] set when row r has an
+  // entry on diagonal j; only built when at most 8 diagonals and every
+  // present entry carries its diagonal's default value.  nullptr otherwise.
+  // Rows [-4D - 64, n + 4D + 64) are readable (zero outside the matrix);
+  // dia_pres is 16-byte aligned.
+  const unsigned char* dia_pres = nullptr;
 };
 
 constexpr int kDiaMaxDiag = 32;
@@ -105,6 +111,15 @@ bool mp2_supported(const CsrDevice& a);
 void spmv_mp2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y1, double* y2,
               const double* base, MpWork& w, int sm_count, cudaStream_t st);
 
+/// True when two factors can run as one temporally blocked pass over the
+/// diagonal layout (spmv_dia2.cu): presence form, outer diagonals +-D, even n
+/// and D, in-plane offsets small against D.  PPA_DISABLE_DIA2=1 turns it off.
+bool dia2_supported(const CsrDevice& a);
+/// One two-factor pass (Mp2Pass semantics, y2 only; t / y1 never stored).
+/// x and y distinct and 16-byte aligned; `base` folds the complement.
+void spmv_dia2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y,
+               const double* base, cudaStream_t st);
+
 /// SELL-32 is used when its padded entry count is at most this factor of nnz.
 constexpr double kSellMaxPadding = 1.15;
 
@@ -139,6 +154,8 @@ struct DevDia {
   DBuffer<int> irr_rows;
   DBuffer<unsigned char> irr_codes;
   long long nirr = 0;
+  DBuffer<unsigned char> pres;  // presence form, pres_pad zero rows each side; may be empty
+  long long pres_pad = 0;
 };
 /// Diagonal-coded layout from the device CSR; false when the matrix has more
 /// than kDiaMaxDiag diagonals, more than kDiaMaxDict distinct values or a

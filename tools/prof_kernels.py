@@ -1,4 +1,5 @@
-"""Kernel-profiling driver (run under ncu on one GPU): config 3 pi(A)v, CGS2 and V*Q.
+"""Kernel-profiling driver (run under ncu on one GPU): config 3 pi(A)v, CGS2 and V*Q
+(PPA_PROF_CONFIG=N picks another BASELINE config).
 
     python tools/prof_kernels.py [all|spmv|cgs] [auto|sell32|sell32_packed|dia_coded|csr]
 """
@@ -15,7 +16,7 @@ what = sys.argv[1] if len(sys.argv) > 1 else "all"
 layout = sys.argv[2] if len(sys.argv) > 2 else "auto"
 torch.cuda.set_device(0)
 ppa.set_stream(torch.cuda.current_stream())
-csr = ppa.CsrMatrix.config(3)
+csr = ppa.CsrMatrix.config(int(os.environ.get("PPA_PROF_CONFIG", "3")))
 n = csr.n
 A = ppa.make_csr_operator(csr, layout)
 # 8 real roots spread over the config-3 spectrum (the timing does not depend on them)
