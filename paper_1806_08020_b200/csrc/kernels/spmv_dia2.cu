@@ -74,15 +74,30 @@ __device__ __forceinline__ void bulk_load_plain(uint32_t dst, const void* src, u
 // CHECK: an absent term contributes val * (+0.0), which leaves the sum's bits
 // unchanged (the sum starts at +0.0 and round-to-nearest never produces -0.0
 // from it), i.e. exactly the reference's skipped entry, even for inf/nan x.
-template <int ND, bool CHECK>
+// Addresses are split into a per-thread byte offset tb and a warp-uniform
+// one (ub + 8 off_j) so the loads use the [R + UR] form.
+__device__ __forceinline__ double f2_lds(const char* smc, uint32_t tb, int ub) {
+  return *reinterpret_cast<const double*>(smc + (tb + static_cast<uint32_t>(ub)));
+}
+
+// Row sum: diagonals in increasing offset.  xm / xp are the -D / +D terms,
+// xc the centre (diagonal JC, offset 0), the other middle terms at byte
+// tb + ub + 8 off_j.  CHECK: an absent term (bit j of pr clear) contributes
+// val * (+0.0), which leaves the sum's bits unchanged (the sum starts at +0.0
+// and round-to-nearest never produces -0.0 from it), i.e. exactly the
+// reference's skipped entry, even for inf/nan x.
+// UNIT: the diagonals next to the centre are offsets -1 and +1 (every 2-D
+// and 3-D stencil), read at immediate offsets.
+template <int ND, bool UNIT, bool CHECK>
 __device__ __forceinline__ double f2_row(const F2Params& P, unsigned pr, double xm, double xc,
-                                         double xp, const double* __restrict__ sm, int c) {
+                                         double xp, const char* smc, uint32_t tb, int ub) {
   constexpr int JC = (ND - 1) / 2;
   double s = 0.0;
   s = __dadd_rn(s, __dmul_rn(P.val[0], CHECK && !(pr & 1u) ? 0.0 : xm));
 #pragma unroll
   for (int j = 1; j < ND - 1; ++j) {
-    double v = j == JC ? xc : sm[c + P.off[j]];
+    const int o = UNIT && j == JC - 1 ? -1 : UNIT && j == JC + 1 ? 1 : P.off[j];
+    double v = j == JC ? xc : f2_lds(smc, tb, ub + 8 * o);
     if (CHECK && !(pr & (1u << j))) v = 0.0;
     s = __dadd_rn(s, __dmul_rn(P.val[j], v));
   }
@@ -96,6 +111,8 @@ __device__ __forceinline__ double f2_row(const F2Params& P, unsigned pr, double 
 template <int KC>
 struct F2Thread {
   int ee[KC];     // owned column (0 for lanes past E1)
+  uint32_t eb[KC];  // 8 ee
+  uint32_t cb[KC];  // 8 x (core ? ee : Dm): level-2 column (halo lanes read a valid one)
   bool own[KC];   // column inside the extended tile
   bool core[KC];  // column inside the tile (level 2 stores it)
   bool wcore[KC]; // some lane of the warp has a core column k
@@ -109,14 +126,13 @@ struct F2Thread {
 // level 2 at plane q - 1.  The register triples rotate with period 3 and the
 // slots with period 6, so the six unrolled steps use fixed registers and
 // fixed slot indices.
-template <int ND, int KC, bool PAIR, bool COMPL, int V>
+template <int ND, bool UNIT, int KC, bool PAIR, bool COMPL, int V>
 __device__ __forceinline__ bool f2_step(const F2Params& P, const F2Thread<KC>& T, int u,
                                         double* __restrict__ sm, uint64_t* bar,
                                         const double* __restrict__ x, double* y,
                                         const double* __restrict__ base, const unsigned char* pres,
                                         double (&xm)[KC], double (&x0)[KC], double (&xp)[KC],
                                         double (&l1m)[KC], double (&l1c)[KC], double (&l1n)[KC]) {
-  constexpr unsigned kAll = (1u << ND) - 1u;
   const int t = 6 * u + V;
   if (t >= T.nsteps) return false;
   const int q = T.qa - 1 + t;
@@ -128,28 +144,30 @@ __device__ __forceinline__ bool f2_step(const F2Params& P, const F2Thread<KC>& T
   // presence slots hold rows from a 16-byte aligned start: plane p's row of
   // column e at byte ps + s pw + e + ((p D + rbase) & 15)
   const unsigned char* pb = reinterpret_cast<const unsigned char*>(sm);
+  const char* smc = reinterpret_cast<const char*>(sm);
   const int pq = T.ps + SQ * T.pw + ((q * D + T.rbase) & 15);
   const int pm = T.ps + SM1 * T.pw + (((q - 1) * D + T.rbase) & 15);
+  constexpr unsigned kAll = (1u << ND) - 1u;
   unsigned prc[KC], prp[KC];
   bool full = true;
 #pragma unroll
   for (int k = 0; k < KC; ++k) {
-    xp[k] = sm[xn + T.ee[k]];
-    prc[k] = T.own[k] ? pb[pq + T.ee[k]] : kAll;
-    prp[k] = T.core[k] ? pb[pm + T.ee[k]] : kAll;
+    xp[k] = f2_lds(smc, T.eb[k], 8 * xn);
+    prc[k] = T.own[k] ? pb[static_cast<uint32_t>(T.ee[k]) + static_cast<uint32_t>(pq)] : kAll;
+    prp[k] = T.core[k] ? pb[static_cast<uint32_t>(T.ee[k]) + static_cast<uint32_t>(pm)] : kAll;
     full = full && prc[k] == kAll;
   }
-  // ---- level 1 at plane q
+  // ---- level 1 at plane q (warp-uniform: interior warps skip the presence tests)
   if (__all_sync(0xffffffffu, full)) {
 #pragma unroll
     for (int k = 0; k < KC; ++k) {
-      const double s = f2_row<ND, false>(P, kAll, xm[k], x0[k], xp[k], sm, xq + T.ee[k]);
+      const double s = f2_row<ND, UNIT, false>(P, kAll, xm[k], x0[k], xp[k], smc, T.eb[k], 8 * xq);
       l1n[k] = PAIR ? s : __dadd_rn(x0[k], __dmul_rn(P.a0, s));
     }
   } else {
 #pragma unroll
     for (int k = 0; k < KC; ++k) {
-      const double s = f2_row<ND, true>(P, prc[k], xm[k], x0[k], xp[k], sm, xq + T.ee[k]);
+      const double s = f2_row<ND, UNIT, true>(P, prc[k], xm[k], x0[k], xp[k], smc, T.eb[k], 8 * xq);
       l1n[k] = PAIR ? s : __dadd_rn(x0[k], __dmul_rn(P.a0, s));
     }
   }
@@ -157,7 +175,10 @@ __device__ __forceinline__ bool f2_step(const F2Params& P, const F2Thread<KC>& T
   const int lr = T.ls + ((V + 2) % F2_LSLOT) * E1;
 #pragma unroll
   for (int k = 0; k < KC; ++k) {
-    if (T.own[k]) sm[lw + T.ee[k]] = l1n[k];
+    if (T.own[k]) {
+      *reinterpret_cast<double*>(reinterpret_cast<char*>(sm) +
+                                 (T.eb[k] + static_cast<uint32_t>(8 * lw))) = l1n[k];
+    }
   }
   __syncthreads();  // level-1 plane q visible; slot SM1 (plane q - 1) free for reuse
   // ---- level 2 at plane q - 1
@@ -170,9 +191,9 @@ __device__ __forceinline__ bool f2_step(const F2Params& P, const F2Thread<KC>& T
 #pragma unroll
     for (int k = 0; k < KC; ++k) {
       if (!T.wcore[k]) continue;  // warp-uniform: the whole warp is in the halo
-      const int c = T.core[k] ? T.ee[k] : Dm;
-      const double s = f2all ? f2_row<ND, false>(P, kAll, l1m[k], l1c[k], l1n[k], sm, lr + c)
-                             : f2_row<ND, true>(P, prp[k], l1m[k], l1c[k], l1n[k], sm, lr + c);
+      const double s =
+          f2all ? f2_row<ND, UNIT, false>(P, kAll, l1m[k], l1c[k], l1n[k], smc, T.cb[k], 8 * lr)
+                : f2_row<ND, UNIT, true>(P, prp[k], l1m[k], l1c[k], l1n[k], smc, T.cb[k], 8 * lr);
       double z = PAIR ? __dadd_rn(__dadd_rn(xm[k], __dmul_rn(P.a1, l1c[k])), __dmul_rn(P.a0, s))
                       : __dadd_rn(l1c[k], __dmul_rn(P.b0, s));
       const int r2 = r2q + T.ee[k];
@@ -185,7 +206,7 @@ __device__ __forceinline__ bool f2_step(const F2Params& P, const F2Thread<KC>& T
   return true;
 }
 
-template <int ND, int KC, bool PAIR, bool COMPL>
+template <int ND, bool UNIT, int KC, bool PAIR, bool COMPL>
 __global__ void __launch_bounds__(f2_max_nt(KC), 1) k_spmv_dia2(
     const unsigned char* __restrict__ pres, const double* __restrict__ x, double* y,
     const double* __restrict__ base, const F2Params P) {
@@ -213,6 +234,8 @@ __global__ void __launch_bounds__(f2_max_nt(KC), 1) k_spmv_dia2(
     T.own[k] = e < E1;
     T.ee[k] = T.own[k] ? e : 0;
     T.core[k] = T.own[k] && e >= Dm && e < Dm + twe;
+    T.eb[k] = 8u * static_cast<uint32_t>(T.ee[k]);
+    T.cb[k] = 8u * static_cast<uint32_t>(T.core[k] ? T.ee[k] : Dm);
     T.wcore[k] = __any_sync(0xffffffffu, T.core[k]);
   }
 
@@ -266,7 +289,7 @@ __global__ void __launch_bounds__(f2_max_nt(KC), 1) k_spmv_dia2(
   // folded into the step by splitting the step at the barrier
   for (int u = 0;; ++u) {
 #define F2_STEP(V, XM, X0, XP, LM, LC, LN)                                                       \
-  if (!f2_step<ND, KC, PAIR, COMPL, V>(P, T, u, f2_sm, bar, x, y, base, pres, XM, X0, XP, LM,   \
+  if (!f2_step<ND, UNIT, KC, PAIR, COMPL, V>(P, T, u, f2_sm, bar, x, y, base, pres, XM, X0, XP, LM,   \
                                        LC, LN)) {                                               \
     break;                                                                                      \
   }                                                                                             \
@@ -299,7 +322,7 @@ int f2_sms() {
 }
 
 int f2_smem_limit() {
-  static const int lim = max_dynamic_smem(k_spmv_dia2<7, 2, true, true>);
+  static const int lim = max_dynamic_smem(k_spmv_dia2<7, true, 2, true, true>);
   return lim;
 }
 
@@ -373,10 +396,10 @@ F2Plan f2_plan(int n, int D, int Dm) {
   return best;
 }
 
-template <int ND, int KC, bool PAIR, bool COMPL>
+template <int ND, bool UNIT, int KC, bool PAIR, bool COMPL>
 void launch_f2(const CsrDevice& a, const F2Params& P, const F2Plan& pl, const double* x,
                double* y, const double* base, cudaStream_t st) {
-  auto kernel = k_spmv_dia2<ND, KC, PAIR, COMPL>;
+  auto kernel = k_spmv_dia2<ND, UNIT, KC, PAIR, COMPL>;
   static const bool attr = [kernel] {
     PPA_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   max_dynamic_smem(kernel)));
@@ -387,26 +410,38 @@ void launch_f2(const CsrDevice& a, const F2Params& P, const F2Plan& pl, const do
              base, P);
 }
 
-template <int ND, int KC>
+template <int ND, bool UNIT, int KC>
 void launch_f2_k(const CsrDevice& a, const F2Params& P, const F2Plan& pl, bool pair,
                  const double* x, double* y, const double* base, cudaStream_t st) {
   if (pair) {
-    base ? launch_f2<ND, KC, true, true>(a, P, pl, x, y, base, st)
-         : launch_f2<ND, KC, true, false>(a, P, pl, x, y, base, st);
+    base ? launch_f2<ND, UNIT, KC, true, true>(a, P, pl, x, y, base, st)
+         : launch_f2<ND, UNIT, KC, true, false>(a, P, pl, x, y, base, st);
   } else {
-    base ? launch_f2<ND, KC, false, true>(a, P, pl, x, y, base, st)
-         : launch_f2<ND, KC, false, false>(a, P, pl, x, y, base, st);
+    base ? launch_f2<ND, UNIT, KC, false, true>(a, P, pl, x, y, base, st)
+         : launch_f2<ND, UNIT, KC, false, false>(a, P, pl, x, y, base, st);
+  }
+}
+
+template <int ND, bool UNIT>
+void launch_f2_u(const CsrDevice& a, const F2Params& P, const F2Plan& pl, bool pair,
+                 const double* x, double* y, const double* base, cudaStream_t st) {
+  switch (pl.kc) {
+    case 2: return launch_f2_k<ND, UNIT, 2>(a, P, pl, pair, x, y, base, st);
+    case 3: return launch_f2_k<ND, UNIT, 3>(a, P, pl, pair, x, y, base, st);
+    default: return launch_f2_k<ND, UNIT, 4>(a, P, pl, pair, x, y, base, st);
   }
 }
 
 template <int ND>
 void launch_f2_nd(const CsrDevice& a, const F2Params& P, const F2Plan& pl, bool pair,
                   const double* x, double* y, const double* base, cudaStream_t st) {
-  switch (pl.kc) {
-    case 2: return launch_f2_k<ND, 2>(a, P, pl, pair, x, y, base, st);
-    case 3: return launch_f2_k<ND, 3>(a, P, pl, pair, x, y, base, st);
-    default: return launch_f2_k<ND, 4>(a, P, pl, pair, x, y, base, st);
+  if constexpr (ND >= 5) {
+    constexpr int JC = (ND - 1) / 2;
+    if (P.off[JC - 1] == -1 && P.off[JC + 1] == 1) {
+      return launch_f2_u<ND, true>(a, P, pl, pair, x, y, base, st);
+    }
   }
+  launch_f2_u<ND, false>(a, P, pl, pair, x, y, base, st);
 }
 
 int f2_dm(const CsrDevice& a) {
