@@ -130,13 +130,20 @@ def load_golden_poly():
     return np.array(g["roots"]["re"]) + 1j * np.array(g["roots"]["im"])
 
 
-def count_launches(roots):
+def count_launches(roots, two_factor=False):
+    """Kernel launches of one pi(A)v (gmres_poly.cpp apply_poly_csr): a real
+    root is one launch, a pair two; with the two-factor pass (spmv_dia2.cu)
+    two consecutive real roots or one pair share a launch."""
     launches = 0
     i = 0
     r = list(roots)
     while i < len(r):
-        if abs(r[i].imag) > 1e-13 * abs(r[i]):
-            launches += 2
+        pair = abs(r[i].imag) > 1e-13 * abs(r[i])
+        if pair:
+            launches += 1 if two_factor else 2
+            i += 2
+        elif two_factor and i + 1 < len(r) and abs(r[i + 1].imag) <= 1e-13 * abs(r[i + 1]):
+            launches += 1
             i += 2
         else:
             launches += 1
@@ -299,20 +306,36 @@ def run_b200(args):
     ms_auto, _ = time_pi(A_auto)
     auto_match = bool(torch.equal(out, ref_out))
     e2e_auto_ms, e2e_auto_match = time_e2e(A_auto)
-    kbytes = lay["stream_bytes"] + 16.0 * n  # + x gather (8n) + y store (8n)
-    auto_launch_s = ms_auto * 1e-3 / launches
+    two = bool(lay.get("two_factor_pass"))
+    auto_launches = count_launches(roots, two)
+    auto_launch_s = ms_auto * 1e-3 / auto_launches
+    if two:
+        # two factors per launch: x read once (8n), the second factor's y
+        # written once (8n), one presence byte per row (n)
+        kbytes = 17.0 * n
+        kname = ("k_spmv_dia2 (two factors per pass: temporally blocked diagonal form, "
+                 "x planes by cp.async.bulk into a shared-memory ring)")
+        note = ("8n x + 8n y + n presence per two-factor launch; the kernel is issue-bound "
+                "(~67% issue slots busy, ncu), not HBM-bound")
+    else:
+        kbytes = lay["stream_bytes"] + 16.0 * n  # + x gather (8n) + y store (8n)
+        kname = ("k_spmv_diam (regular-row diagonal form, marching over the +-plane "
+                 "diagonals, fused real-root factor)")
+        note = "matrix stream of this layout + 8n x + 8n y"
     default_layout = {
         "layout": lay["layout"], "ms_per_step": round(ms_auto, 4),
         "value": round(whole_job_gbs(step_bytes, ms_auto, ws), 3), "unit": "GB/s (north-star model)",
         "speedup_vs_sell32": round(ms_step / ms_auto, 3),
+        "two_factor_pass": two, "launches_per_step": auto_launches,
+        "us_per_factor": round(ms_auto * 1e3 / len(roots), 3),
         "e2e": {"value": round(whole_job_gbs(step_bytes, e2e_auto_ms, ws), 3),
                 "ms_per_step": round(e2e_auto_ms, 4), "matches_device_result": e2e_auto_match},
         "roofline": {"bound": "hbm", "achieved": round(kbytes / auto_launch_s / 1e9, 2),
                      "peak": peak, "unit": "GB/s",
                      "frac": round(kbytes / auto_launch_s / 1e9 / peak, 4),
-                     "kernel": "k_spmv_diam (regular-row diagonal form, marching over the +-plane diagonals, fused real-root factor)",
+                     "kernel": kname,
                      "algorithmic_bytes_per_launch": kbytes,
-                     "bytes_note": "matrix stream of this layout + 8n x + 8n y"},
+                     "bytes_note": note},
         "bit_identical_to_sell32": auto_match,
     }
 
