@@ -56,7 +56,7 @@ constexpr int f2_max_nt(int kc) { return kc <= 2 ? 1024 : kc == 3 ? 768 : 512; }
 struct F2Params {
   int off[8];
   double val[8];
-  int n, D, Dm, E1, E2, TW, ntiles, nq, nchunks;
+  int n, D, Dm, E1, E2, TW, SH, ntiles, nq, nchunks;
   double a0, a1, b0;
 };
 
@@ -119,7 +119,7 @@ struct F2Thread {
   int ls;         // first double of the level-1 slots
   int ps;         // first byte of the presence slots
   int pw;         // bytes per presence slot
-  int qa, nsteps, c0, rbase;  // rbase = c0 - Dm
+  int qa, nsteps, c0, rbase;  // rbase = c0 - Dm - SH: the row of column e is q D + rbase + e
 };
 
 // One step of the march (t = 6 u + V): level 1 at plane q = qa - 1 + t,
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(f2_max_nt(KC), 1) k_spmv_dia2(
   const int n = P.n, D = P.D, Dm = P.Dm, E1 = P.E1, E2 = P.E2;
   F2Thread<KC> T;
   T.c0 = tile * P.TW;
-  T.rbase = T.c0 - Dm;
+  T.rbase = T.c0 - Dm - P.SH;
   T.qa = static_cast<int>(static_cast<long long>(chunk) * P.nq / P.nchunks);
   const int qb = static_cast<int>(static_cast<long long>(chunk + 1) * P.nq / P.nchunks);
   T.nsteps = qb - T.qa + 2;  // q = qa-1 .. qb
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(f2_max_nt(KC), 1) k_spmv_dia2(
     const int e = tid + k * NT;
     T.own[k] = e < E1;
     T.ee[k] = T.own[k] ? e : 0;
-    T.core[k] = T.own[k] && e >= Dm && e < Dm + twe;
+    T.core[k] = T.own[k] && e >= Dm + P.SH && e < Dm + P.SH + twe;
     T.eb[k] = 8u * static_cast<uint32_t>(T.ee[k]);
     T.cb[k] = 8u * static_cast<uint32_t>(T.core[k] ? T.ee[k] : Dm);
     T.wcore[k] = __any_sync(0xffffffffu, T.core[k]);
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(f2_max_nt(KC), 1) k_spmv_dia2(
   auto issue = [&](int i) {
     const int p = pfirst + i;
     if (p > plast) return;
-    const int lo = p * D + T.c0 - 2 * Dm;
+    const int lo = p * D + T.rbase - Dm;
     const int a = max(lo, 0), b = min(lo + E2, n);
     const uint32_t bytes = b > a ? static_cast<uint32_t>(b - a) * 8u : 0u;
     const int r1 = p * D + T.rbase;
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(f2_max_nt(KC), 1) k_spmv_dia2(
 }
 
 struct F2Plan {
-  int nt = 0, kc = 0, tw = 0, ntiles = 0, nchunks = 0;
+  int nt = 0, kc = 0, tw = 0, sh = 0, ntiles = 0, nchunks = 0;
   size_t smem = 0;
 };
 
@@ -349,6 +349,12 @@ int f2_env(const char* name, int dflt) {
 
 F2Plan f2_plan(int n, int D, int Dm) {
   const int sms = f2_sms();
+  // 3-D stencils: the boundary rows of a grid line (ix = N - 1 and the next
+  // line's ix = 0) are neighbours.  With lines of a multiple of 32 rows,
+  // tiles of a multiple of 32 columns and the extended tile starting 16
+  // columns early, each such pair falls inside one warp, so one warp in
+  // Dm / 32 takes the presence-tested path instead of two.
+  const int sh = (Dm >= 64 && Dm % 32 == 0 && D % 32 == 0 && f2_env("PPA_DIA2_SHIFT", 1)) ? 16 : 0;
   const int nq = (n + D - 1) / D;
   const int force_cps = f2_env("PPA_DIA2_CPS", 0);
   const int ntmax = f2_env("PPA_DIA2_NTMAX", 1024);
@@ -371,7 +377,8 @@ F2Plan f2_plan(int n, int D, int Dm) {
           const int ntiles = (D + cap - 1) / cap;
           int tw = (D + ntiles - 1) / ntiles;
           tw += tw & 1;
-          const int e1 = tw + 2 * Dm;
+          if (sh) tw = (tw + 31) & ~31;
+          const int e1 = tw + 2 * Dm + sh;
           if (e1 > nt * kc) continue;
           size_t smem = f2_smem_bytes(e1, Dm);
           if ((smem + 1024) * cps > static_cast<size_t>(kSmTotal) ||
@@ -387,7 +394,7 @@ F2Plan f2_plan(int n, int D, int Dm) {
                               (static_cast<double>(nt) * kc);
           if (cost < best_cost * 0.999) {
             best_cost = cost;
-            best = F2Plan{nt, kc, tw, ntiles, nchunks, smem};
+            best = F2Plan{nt, kc, tw, sh, ntiles, nchunks, smem};
           }
         }
       }
@@ -481,7 +488,8 @@ void spmv_dia2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y,
   P.D = D;
   P.Dm = dm;
   P.TW = pl.tw;
-  P.E1 = pl.tw + 2 * dm;
+  P.SH = pl.sh;
+  P.E1 = pl.tw + 2 * dm + pl.sh;
   P.E2 = P.E1 + 2 * dm;
   P.ntiles = pl.ntiles;
   P.nq = (a.n + D - 1) / D;

@@ -65,6 +65,7 @@ GEOMETRIES = [
     (2048 * 300 + 512, (-2048, -1, 0, 1, 2048)),           # many planes, partial last plane
     (25600 * 8, (-25600, -160, -1, 0, 1, 160, 25600)),     # config-3 plane, few planes
     (100 * 50, (-100, -10, -3, 0, 2, 5, 100)),             # 7 diagonals, irregular spacing
+    (4096 * 10 + 64, (-4096, -64, -1, 0, 1, 64, 4096)),    # lines of 64: warp-shifted tiles
 ]
 
 
@@ -84,6 +85,7 @@ def test_dia2_geometries_bit_exact(cuda, n, offsets, kind, complement):
 STENCILS = [
     ("laplace3d_24", lambda M: M.laplacian_3d(24)),
     ("laplace3d_40", lambda M: M.laplacian_3d(40)),
+    ("laplace3d_64", lambda M: M.laplacian_3d(64)),       # lines of 64: warp-shifted tiles
     ("convdiff_300", lambda M: M.convection_diffusion_const(300, 0.5)),
 ]
 
