@@ -35,6 +35,8 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "pdl.cuh"
@@ -347,7 +349,7 @@ int f2_env(const char* name, int dflt) {
   return v ? std::atoi(v) : dflt;
 }
 
-F2Plan f2_plan(int n, int D, int Dm) {
+F2Plan f2_plan_search(int n, int D, int Dm) {
   const int sms = f2_sms();
   // 3-D stencils: the boundary rows of a grid line (ix = N - 1 and the next
   // line's ix = 0) are neighbours.  With lines of a multiple of 32 rows,
@@ -401,6 +403,26 @@ F2Plan f2_plan(int n, int D, int Dm) {
     }
   }
   return best;
+}
+
+// Plans are searched once per geometry (the search visits a few hundred
+// candidates; a solve launches thousands of passes).  The A/B overrides
+// (PPA_DIA2_*) apply to geometries planned after they are set.
+F2Plan f2_plan(int n, int D, int Dm) {
+  struct Entry {
+    int n, D, Dm;
+    F2Plan plan;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  for (const Entry& e : cache) {
+    if (e.n == n && e.D == D && e.Dm == Dm) return e.plan;
+  }
+  const F2Plan plan = f2_plan_search(n, D, Dm);
+  if (cache.size() >= 64) cache.erase(cache.begin());
+  cache.push_back({n, D, Dm, plan});
+  return plan;
 }
 
 template <int ND, bool UNIT, int KC, bool PAIR, bool COMPL>

@@ -150,3 +150,20 @@ def test_config_table():
         cfg = ppa.config_solve_config(k)
         assert cfg.m > cfg.k > 0
     assert ppa.CONFIGS[3]["n"] == 160 ** 3
+
+
+def test_bench_launch_count_model():
+    # bench.py's launches-per-step mirrors gmres_poly.cpp apply_poly_csr: a
+    # real root is one launch and a pair two; with the two-factor pass two
+    # consecutive real roots, or one pair, share a launch
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+
+    roots = [5.0, 4.0, 3 + 1j, 3 - 1j, 2.0, 1 + 2j, 1 - 2j, 0.5, 0.25, 0.125]
+    assert bench.count_launches(roots) == 10
+    # passes: (5,4) (3+-1j) (2) (1+-2j) (0.5,0.25) (0.125)
+    assert bench.count_launches(roots, True) == 6
+    assert bench.count_launches([], True) == 0
+    assert bench.count_launches([1.0] * 51, True) == 26
