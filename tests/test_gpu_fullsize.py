@@ -161,3 +161,32 @@ def test_config_solve_vs_fixture(cuda, k):
     got = np.sort_complex(r["eigenvalues"])
     ref = np.sort_complex(_c(g["eigenvalues"]))
     assert np.max(np.abs(got - ref) / np.abs(ref)) < 1e-8
+
+
+@pytest.mark.parametrize("k", [2, 5])
+def test_two_factor_pass_full_size_bit_exact(cuda, k):
+    # BASELINE configs 2 and 5 at full size run the two-factor pass with two
+    # CTAs per SM (spmv_dia2.cu): a mixed real/pair chain, its complement and
+    # the nested phi(tau(A)) of solve_double, bit-identical to the oracle
+    P = ppa.CsrMatrix.config(k)
+    A = ppa.make_csr_operator(P)
+    assert A.layout()["two_factor_pass"]
+    Q = O.csr_operator(O.Csr.config(k))
+    O.set_threads(os.cpu_count() or 1)
+    lam_max = 8.0 * (P.n ** 0.5 + 1) ** 2
+    r1 = O.leja_order([0.9 * lam_max, 0.5 * lam_max + 0.05j * lam_max,
+                       0.5 * lam_max - 0.05j * lam_max, 0.2 * lam_max, 0.05 * lam_max])
+    r2 = O.leja_order([0.9, 0.4 + 0.1j, 0.4 - 0.1j])
+    v = ppa.normal_vector(P.n, 3, ppa.STREAM_ARNOLDI)
+    x = cuda.tensor(v, device="cuda")
+    y = cuda.empty(P.n, dtype=cuda.float64, device="cuda")
+    for op, ref in (
+        (ppa.make_poly_operator(A, r1), O.poly_operator(Q, r1)),
+        (ppa.make_poly_complement_operator(A, r1), O.poly_operator(Q, r1, True)),
+        (ppa.make_poly_operator(ppa.make_poly_complement_operator(A, r1), r2),
+         O.poly_operator(O.poly_operator(Q, r1, True), r2)),
+    ):
+        op.apply(x, y)
+        want = ref.apply(v)
+        got = y.cpu().numpy()
+        assert np.array_equal(got, want), np.linalg.norm(got - want) / np.linalg.norm(want)
