@@ -492,12 +492,13 @@ bool build_dia_device(const int* row_ptr, const int* col_idx, const double* valu
   out.regular = true;
   out.pres.release();
   if (nd <= 8 && n > 0) {
-    // zero padding of 4 D + 64 rows (a multiple of 16) on both sides (D = the
+    // zero padding of 5 D + 64 rows (a multiple of 16) on both sides (D = the
     // widest offset): the two-factor pass copies presence bytes of rows just
-    // outside the matrix, from 16-byte aligned starts
+    // outside the matrix, from 16-byte aligned starts (its last chunk reaches
+    // row n + 4 D + Dm + 15 at most, Dm <= D / 4)
     const long long D = std::max(std::abs(static_cast<long long>(out.offsets.front())),
                                  std::abs(static_cast<long long>(out.offsets.back())));
-    out.pres_pad = (4 * D + 64 + 15) & ~15LL;
+    out.pres_pad = (5 * D + 64 + 15) & ~15LL;
     const size_t total = static_cast<size_t>(n + 2 * out.pres_pad + 16);
     out.pres.resize(total);
     PPA_CUDA(cudaMemsetAsync(out.pres.get(), 0, total, st));

@@ -59,6 +59,7 @@ struct F2Params {
   int off[8];
   double val[8];
   int n, D, Dm, E1, E2, TW, SH, ntiles, nq, nchunks;
+  int ppad;  // zero rows of dia_pres on each side (a multiple of 16)
   double a0, a1, b0;
 };
 
@@ -251,8 +252,8 @@ __global__ void __launch_bounds__(f2_max_nt(KC), 1) k_spmv_dia2(
 
   // Plane p = qa - 2 + i lives in slot i % NSLOT: x rows p D + c0 - 2 Dm +
   // [0, E2) clipped to the matrix (32-bit rows: the host guarantees
-  // n + 4 D < 2^31) and the presence bytes of rows p D + rbase + [0, E1)
-  // from the 16-byte boundary below (pres is zero-padded by >= 4 D rows).
+  // n + 6 D < 2^31) and the presence bytes of rows p D + rbase + [0, E1)
+  // from the 16-byte boundary below (pres is zero-padded by >= 5 D rows).
   const int pfirst = T.qa - 2;
   const int plast = qb + 1;
   auto issue = [&](int i) {
@@ -262,7 +263,10 @@ __global__ void __launch_bounds__(f2_max_nt(KC), 1) k_spmv_dia2(
     const int a = max(lo, 0), b = min(lo + E2, n);
     const uint32_t bytes = b > a ? static_cast<uint32_t>(b - a) * 8u : 0u;
     const int r1 = p * D + T.rbase;
-    const int pa = r1 & ~15, pe = (r1 + E1 + 15) & ~15;
+    // clamped to the padded presence array (never binding for the planner's
+    // geometries: rows stay within n + 4 D + Dm + 15 of a 5 D + 64 padding)
+    const int pa = max(r1 & ~15, -P.ppad);
+    const int pe = max(pa, min((r1 + E1 + 15) & ~15, (n + P.ppad + 15) & ~15));
     const uint32_t pbytes = static_cast<uint32_t>(pe - pa);
     const int sl = i % F2_NSLOT;
     mbar_expect_tx(bar + sl, bytes + pbytes);
@@ -270,8 +274,10 @@ __global__ void __launch_bounds__(f2_max_nt(KC), 1) k_spmv_dia2(
       bulk_load_plain(sm_base + 8u * static_cast<uint32_t>(F2_XS + sl * E2 + (a - lo)), x + a,
                       bytes, smem_u32(bar + sl));
     }
-    bulk_load_plain(sm_base + static_cast<uint32_t>(T.ps + sl * T.pw), pres + pa, pbytes,
-                    smem_u32(bar + sl));
+    if (pbytes) {
+      bulk_load_plain(sm_base + static_cast<uint32_t>(T.ps + sl * T.pw + (pa - (r1 & ~15))),
+                      pres + pa, pbytes, smem_u32(bar + sl));
+    }
   };
   if (tid == 0) {
     for (int i = 0; i < F2_NSLOT; ++i) issue(i);
@@ -491,7 +497,8 @@ bool dia2_supported(const CsrDevice& a) {
   if (a.dia_off[0] != -D || D < 64 || (D & 1) || (a.n & 1)) return false;
   const int dm = f2_dm(a);
   if (4 * dm > D || a.n / D < 4) return false;
-  if (static_cast<long long>(a.n) + 4LL * D >= (1LL << 31)) return false;
+  // 32-bit rows: the kernel forms rows up to n + 4 D + Dm + 15
+  if (static_cast<long long>(a.n) + 6LL * D >= (1LL << 31)) return false;
   return f2_plan(a.n, D, dm).nt > 0;
 }
 
@@ -511,6 +518,7 @@ void spmv_dia2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y,
   P.Dm = dm;
   P.TW = pl.tw;
   P.SH = pl.sh;
+  P.ppad = static_cast<int>(a.dia_pres_pad);
   P.E1 = pl.tw + 2 * dm + pl.sh;
   P.E2 = P.E1 + 2 * dm;
   P.ntiles = pl.ntiles;

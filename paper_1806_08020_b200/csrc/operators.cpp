@@ -183,7 +183,10 @@ bool CsrOperator::upload_dia(cudaStream_t st) {
     dev_.dia_irr_codes = dia_.irr_codes.get();
     dev_.dia_nirr = dia_.nirr;
     for (int j = 0; j < dia_.ndiag; ++j) dev_.dia_dflt[j] = dia_.defaults[j];
-    if (dia_.pres.get()) dev_.dia_pres = dia_.pres.get() + dia_.pres_pad;
+    if (dia_.pres.get()) {
+      dev_.dia_pres = dia_.pres.get() + dia_.pres_pad;
+      dev_.dia_pres_pad = dia_.pres_pad;
+    }
   }
   return true;
 }

@@ -67,9 +67,10 @@ struct CsrDevice {
   // Presence form (spmv_dia2.cu): bit j of dia_pres[r] set when row r has an
   // entry on diagonal j; only built when at most 8 diagonals and every
   // present entry carries its diagonal's default value.  nullptr otherwise.
-  // Rows [-4D - 64, n + 4D + 64) are readable (zero outside the matrix);
+  // Rows [-5D - 64, n + 5D + 64) are readable (zero outside the matrix);
   // dia_pres is 16-byte aligned.
   const unsigned char* dia_pres = nullptr;
+  long long dia_pres_pad = 0;
 };
 
 constexpr int kDiaMaxDiag = 32;

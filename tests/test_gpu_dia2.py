@@ -66,6 +66,8 @@ GEOMETRIES = [
     (25600 * 8, (-25600, -160, -1, 0, 1, 160, 25600)),     # config-3 plane, few planes
     (100 * 50, (-100, -10, -3, 0, 2, 5, 100)),             # 7 diagonals, irregular spacing
     (4096 * 10 + 64, (-4096, -64, -1, 0, 1, 64, 4096)),    # lines of 64: warp-shifted tiles
+    (25600 * 6 + 2, (-25600, -160, -1, 0, 1, 160, 25600)), # last plane of 2 rows: the
+                                                           # presence copies reach n + 4D + Dm
 ]
 
 
