@@ -218,7 +218,7 @@ typedef struct ppa_solve_config {
   int stagnation_stop, stagnation_window;
   double stagnation_rtol;
   int want_eigenvectors;     /* keep unit eigenvectors for evec_re/evec_im */
-  int orthogonalization;     /* 0 CGS2 (default), 1 delayed CGS2 */
+  int orthogonalization;     /* 0 CGS2, 1 delayed CGS2 (the C++ and Python SolveConfig default) */
 } ppa_solve_config;
 
 /* EigResult (inc/solver.hpp:71-89); arrays supplied by the caller */

@@ -560,7 +560,8 @@ class ArnoldiState:
         return h.reshape((m, m + 1)).T.copy()
 
     def set_orthogonalization(self, mode: str) -> None:
-        """cgs2 (default) or dcgs2 for later extends (ppa_arnoldi_set_orthogonalization)."""
+        """cgs2 (the Arnoldi state's default) or dcgs2 for later extends
+        (ppa_arnoldi_set_orthogonalization); solve() defaults to dcgs2."""
         _check(lib().ppa_arnoldi_set_orthogonalization(self._h, {"cgs2": 0, "dcgs2": 1}[mode]))
 
     def extend(self, op: LinearOperator, to_dim: int, rec: Optional[CostRecord] = None):
@@ -636,7 +637,7 @@ class SolveConfig:
     stagnation_window: int = 5
     stagnation_rtol: float = 0.01
     want_eigenvectors: bool = False
-    orthogonalization: str = "cgs2"  # cgs2 | dcgs2 (delayed CGS2)
+    orthogonalization: str = "dcgs2"  # dcgs2 (delayed CGS2, default) | cgs2
     reference: Sequence[complex] = field(default_factory=list)
 
     def _c(self, use_double: bool) -> _SolveConfigC:

@@ -56,7 +56,7 @@ struct SolveConfig {
   EigenList reference;
   bool want_eigenvectors = false;  // materialise EigResult::eigenvectors
   // cycle orthogonalisation (ours; the polynomial build always uses CGS2)
-  Orthogonalization orthogonalization = Orthogonalization::cgs2;
+  Orthogonalization orthogonalization = Orthogonalization::dcgs2;
   bool allow_nev_above_k = false;
 
   void validate() const;
