@@ -109,6 +109,9 @@ PolyPrecond build_gmres_poly(const LinearOperator& a, const double* b, int degre
   }
   const int d = std::min(degree, a.dim());
   ArnoldiState st = arnoldi_init(b, a.dim(), d, rec);
+  // delayed CGS2 (two sweeps over the basis per step instead of three; the
+  // reference's MGS2 counters are charged either way, arnoldi.cpp)
+  st.ortho = Orthogonalization::dcgs2;
   arnoldi_extend(st, a, d, rec);
 
   PolyPrecond p;
