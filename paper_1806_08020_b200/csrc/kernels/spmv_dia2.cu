@@ -10,10 +10,11 @@
 // order) and skips absent entries, with __dmul_rn/__dadd_rn: bit-identical to
 // the two single-factor launches and to the CPU loop.
 //
-// Applies to the regular-row diagonal layout when every present entry carries
+// Applies to 3-, 5- and 7-point stencils in the regular-row diagonal layout
+// (centre offset 0 in the middle, outer diagonals +-D: the plane offset of a
+// 3-D stencil, the row offset of a 2-D one) when every present entry carries
 // its diagonal's default value (stencils truncated at the boundary; presence
-// is one byte per row, dia_pres) and the outer diagonals are +-D (the plane
-// offset of a 3-D stencil, the row offset of a 2-D one).
+// is one byte per row, dia_pres).
 //
 // Geometry.  Row r = q D + c is column c of plane q.  A CTA owns a column tile
 // [c0, c0 + TW) of a chunk of planes [qa, qb) and marches through the planes:
@@ -24,13 +25,16 @@
 // planes q-2, q-1, q.  Each thread owns columns e = tid + k*NT of the extended
 // tile and keeps its own column's x and level-1 values of three consecutive
 // planes in registers (the +-D and centre terms); the in-plane neighbours come
-// from shared memory: x planes arrive by cp.async.bulk into a ring of NSLOT
-// slots (prefetched NSLOT-2 planes ahead), level-1 planes are stored into a
-// ring of three.  One __syncthreads per step.
+// from shared memory: x planes and their presence bytes arrive by
+// cp.async.bulk into a ring of NSLOT slots (prefetched NSLOT-2 planes ahead),
+// level-1 planes are stored into a ring of three.  One __syncthreads per
+// step; the step loop is unrolled six times so the register triples and the
+// slot indices are fixed per unrolled step.
 //
 // The halo rows (level 1 outside the tile, planes qa-1 and qb) are computed
-// twice, by neighbouring CTAs; the host picks the tile width and chunk count
-// (one CTA per SM) that minimise the per-CTA work.
+// twice, by neighbouring CTAs; the host picks the tile width, chunk count
+// and CTAs per SM that minimise the per-SM work (f2_plan).  Issue-bound on
+// B200, not HBM-bound.
 
 #include <algorithm>
 #include <cstdint>
