@@ -187,3 +187,42 @@ def test_dia2_repeated_applies_and_graphs(cuda, monkeypatch):
         for _ in range(3):
             op.apply(x, y)
             assert np.array_equal(host(y), ref)
+
+
+def _fuzz_case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    nd = int(rng.choice([3, 5, 7]))
+    D = int(rng.choice([64, 96, 130, 256, 400, 1000, 2048]))
+    side = (nd - 3) // 2  # in-plane offsets on each side of the centre
+    dm_cap = max(2, D // 4)
+
+    def draw():
+        vals = set()
+        if side and rng.integers(0, 2):
+            vals.add(1)  # the +-1 neighbours of 2-D/3-D stencils (immediate offsets)
+        while len(vals) < side:
+            vals.add(int(rng.integers(1, dm_cap + 1)))
+        return sorted(vals)
+
+    neg, pos = draw(), draw()
+    offsets = [-D] + [-v for v in reversed(neg)] + [0] + pos + [D]
+    planes = int(rng.integers(4, 40))
+    n = D * planes + int(rng.integers(0, D))
+    n += n & 1
+    vals = [float(v) for v in rng.choice([-1.0, 2.5, -0.75, 4.0, 0.5, -3.0], size=nd)]
+    kind = str(rng.choice(["real_even", "real_odd", "mixed", "pairs_only"]))
+    return n, tuple(offsets), vals, kind, bool(rng.integers(0, 2))
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_dia2_fuzz_bit_exact(cuda, seed):
+    # seeded stencil geometries (plane widths, in-plane offsets up to D/4,
+    # 3/5/7 points, ragged last planes, values per diagonal) and root mixes:
+    # the two-factor pass must reproduce the oracle bit for bit
+    n, offsets, vals, kind, complement = _fuzz_case(seed)
+    rp, ci, vv = _banded(n, offsets, vals)
+    P = ppa.CsrMatrix.from_arrays(n, rp, ci, vv)
+    Q = O.Csr.from_arrays(n, rp, ci, vv)
+    lay = ppa.make_csr_operator(P).layout()
+    assert lay["layout"] == "dia_coded" and lay["two_factor_pass"], (n, offsets, lay)
+    _check(cuda, P, Q, ROOTS[kind], complement, seed=seed)
