@@ -139,12 +139,13 @@ __device__ __forceinline__ bool f2_step(const F2Params& P, const F2Thread<KC>& T
                                         const double* __restrict__ x, double* y,
                                         const double* __restrict__ base, const unsigned char* pres,
                                         double (&xm)[KC], double (&x0)[KC], double (&xp)[KC],
-                                        double (&l1m)[KC], double (&l1c)[KC], double (&l1n)[KC]) {
+                                        double (&l1m)[KC], double (&l1c)[KC], double (&l1n)[KC],
+                                        const unsigned (&pr_prev)[KC], unsigned (&prc)[KC]) {
   const int t = 6 * u + V;
   if (t >= T.nsteps) return false;
   const int q = T.qa - 1 + t;
   const int D = P.D, Dm = P.Dm, E1 = P.E1, E2 = P.E2;
-  constexpr int SQ = (V + 1) % F2_NSLOT, SP = (V + 2) % F2_NSLOT, SM1 = V % F2_NSLOT;
+  constexpr int SQ = (V + 1) % F2_NSLOT, SP = (V + 2) % F2_NSLOT;
   mbar_wait(bar + SP, (u + (V >= 4 ? 1 : 0)) & 1);  // plane q + 1 (plane q: one step earlier)
   const int xq = F2_XS + SQ * E2 + Dm;  // column e of plane q at xq + e
   const int xn = F2_XS + SP * E2 + Dm;  // plane q + 1
@@ -153,15 +154,15 @@ __device__ __forceinline__ bool f2_step(const F2Params& P, const F2Thread<KC>& T
   const unsigned char* pb = reinterpret_cast<const unsigned char*>(sm);
   const char* smc = reinterpret_cast<const char*>(sm);
   const int pq = T.ps + SQ * T.pw + ((q * D + T.rbase) & 15);
-  const int pm = T.ps + SM1 * T.pw + (((q - 1) * D + T.rbase) & 15);
   constexpr unsigned kAll = (1u << ND) - 1u;
-  unsigned prc[KC], prp[KC];
+  // presence of plane q - 1 (level 2) is the previous step's plane-q presence
+  unsigned prp[KC];
   bool full = true;
 #pragma unroll
   for (int k = 0; k < KC; ++k) {
     xp[k] = f2_lds(smc, T.eb[k], 8 * xn);
     prc[k] = T.own[k] ? pb[static_cast<uint32_t>(T.ee[k]) + static_cast<uint32_t>(pq)] : kAll;
-    prp[k] = T.core[k] ? pb[static_cast<uint32_t>(T.ee[k]) + static_cast<uint32_t>(pm)] : kAll;
+    prp[k] = T.core[k] ? pr_prev[k] : kAll;
     full = full && prc[k] == kAll;
   }
   // ---- level 1 at plane q (warp-uniform: interior warps skip the presence tests)
@@ -187,7 +188,9 @@ __device__ __forceinline__ bool f2_step(const F2Params& P, const F2Thread<KC>& T
                                  (T.eb[k] + static_cast<uint32_t>(8 * lw))) = l1n[k];
     }
   }
-  __syncthreads();  // level-1 plane q visible; slot SM1 (plane q - 1) free for reuse
+  // level-1 plane q visible to the next step, whose refill of this step's
+  // plane q - 1 slot relies on every thread having passed here
+  __syncthreads();
   // ---- level 2 at plane q - 1
   if (t >= 2) {
     const int r2q = q * D + T.rbase - D;
@@ -297,21 +300,26 @@ __global__ void __launch_bounds__(f2_max_nt(KC), 1) k_spmv_dia2(
     xb[k] = f2_sm[F2_XS + E2 + Dm + T.ee[k]];  // plane qa - 1
     xc[k] = la[k] = lb[k] = lc[k] = 0.0;
   }
-  // the issue of plane t + NSLOT goes right after step t's barrier; it is
-  // folded into the step by splitting the step at the barrier
+  // presence of the previous step's plane, alternating between two arrays
+  unsigned pr_a[KC], pr_b[KC];
+#pragma unroll
+  for (int k = 0; k < KC; ++k) pr_a[k] = pr_b[k] = (1u << ND) - 1u;
+  __syncthreads();  // every thread has read slots 0 and 1 before they are refilled
+  // Step t refills the slot of plane q - 1 (last read in step t - 1, whose
+  // closing barrier every thread has passed) before it computes.
   for (int u = 0;; ++u) {
-#define F2_STEP(V, XM, X0, XP, LM, LC, LN)                                                       \
-  if (!f2_step<ND, UNIT, KC, PAIR, COMPL, V>(P, T, u, f2_sm, bar, x, y, base, pres, XM, X0, XP, LM,   \
-                                       LC, LN)) {                                               \
+#define F2_STEP(V, XM, X0, XP, LM, LC, LN, PP, PC)                                              \
+  if (tid == 0) issue(6 * u + V + F2_NSLOT);                                                    \
+  if (!f2_step<ND, UNIT, KC, PAIR, COMPL, V>(P, T, u, f2_sm, bar, x, y, base, pres, XM, X0, XP, \
+                                             LM, LC, LN, PP, PC)) {                             \
     break;                                                                                      \
-  }                                                                                             \
-  if (tid == 0) issue(6 * u + V + F2_NSLOT);
-    F2_STEP(0, xa, xb, xc, la, lb, lc)
-    F2_STEP(1, xb, xc, xa, lb, lc, la)
-    F2_STEP(2, xc, xa, xb, lc, la, lb)
-    F2_STEP(3, xa, xb, xc, la, lb, lc)
-    F2_STEP(4, xb, xc, xa, lb, lc, la)
-    F2_STEP(5, xc, xa, xb, lc, la, lb)
+  }
+    F2_STEP(0, xa, xb, xc, la, lb, lc, pr_a, pr_b)
+    F2_STEP(1, xb, xc, xa, lb, lc, la, pr_b, pr_a)
+    F2_STEP(2, xc, xa, xb, lc, la, lb, pr_a, pr_b)
+    F2_STEP(3, xa, xb, xc, la, lb, lc, pr_b, pr_a)
+    F2_STEP(4, xb, xc, xa, lb, lc, la, pr_a, pr_b)
+    F2_STEP(5, xc, xa, xb, lc, la, lb, pr_b, pr_a)
 #undef F2_STEP
   }
 }
@@ -352,7 +360,8 @@ size_t f2_smem_bytes(int e1, int dm) {
 // fewest lane-steps per SM wins: waves x cps x (planes + 2) x NT x KC (both
 // levels sweep KC columns of NT threads per plane; halo columns and the two
 // warm-up planes are the overhead).  Measured on B200 (tools/spmv_ab.py):
-// config 3 one 960-thread CTA per SM, configs 2 and 5 two 512-544-thread CTAs.
+// config 3 one 896-thread CTA per SM (18 tiles), config 5 one 768-thread CTA
+// (the whole 2048-column plane), config 2 two 512-thread CTAs.
 // PPA_DIA2_CPS / PPA_DIA2_NTMIN / PPA_DIA2_NTMAX override (A/B only).
 int f2_env(const char* name, int dflt) {
   const char* v = std::getenv(name);
@@ -402,7 +411,11 @@ F2Plan f2_plan_search(int n, int D, int Dm) {
           const int tq = (nq + nchunks - 1) / nchunks;
           const long long ctas = static_cast<long long>(ntiles) * nchunks;
           const long long waves = (ctas + slots - 1) / slots;
-          const double cost = static_cast<double>(waves) * cps * (tq + 2) *
+          // measured, not modelled: two CTAs per SM on a plane split into
+          // several tiles ran 1.4x slower than the model says (config 5:
+          // 13.0 us per factor vs 9.4 with one 768-thread CTA per SM)
+          const double penalty = (cps > 1 && ntiles > 1) ? 1.25 : 1.0;
+          const double cost = penalty * static_cast<double>(waves) * cps * (tq + 2) *
                               (static_cast<double>(nt) * kc);
           if (cost < best_cost * 0.999) {
             best_cost = cost;
