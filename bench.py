@@ -44,7 +44,8 @@ def hbm_peak():
 
 
 class ClockSampler:
-    """nvidia-smi sampling during the timed region."""
+    """nvidia-smi sampling (every 50 ms) over the whole run; summary() keeps
+    the samples that fall inside the timed regions marked with region()."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -54,8 +55,9 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines = []
+        self.regions = []
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
@@ -69,27 +71,42 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
-    def __exit__(self, *a):
+    def stop(self):
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+            self.proc = None
+
+    class _Region:
+        def __init__(self, owner):
+            self.owner = owner
+
+        def __enter__(self):
+            self.t0 = time.time()
+
+        def __exit__(self, *a):
+            # a sample reports the state of the preceding ~50 ms window
+            self.owner.regions.append((self.t0, time.time() + 0.06))
+
+    def region(self):
+        return ClockSampler._Region(self)
 
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for t, ln in self.lines:
+            if not any(a <= t <= b for a, b in self.regions):
+                continue
             p = [x.strip() for x in ln.split(",")]
             if len(p) < 7:
                 continue
             try:
-                util = float(p[6])
-                if util > 0:
-                    sm.append(float(p[0]))
+                sm.append(float(p[0]))
                 mx = float(p[1])
             except ValueError:
                 continue
@@ -97,7 +114,22 @@ class ClockSampler:
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "timed_regions": len(self.regions),
+                "timed_seconds": round(sum(b - a - 0.06 for a, b in self.regions), 3)}
+
+
+def cpu_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
 
 
 def dist_setup(gpus):
@@ -125,9 +157,23 @@ def whole_job_gbs(bytes_per_step: float, ms_per_step: float, ws: int) -> float:
 
 
 def load_golden_poly():
+    """Config 3's degree-50 GMRES polynomial + pof copies as the oracle built
+    it (tests/golden/c3_poly.json): the root set BOTH arms apply."""
     with open(os.path.join(ROOT, "tests", "golden", "c3_poly.json")) as f:
         g = json.load(f)
-    return np.array(g["roots"]["re"]) + 1j * np.array(g["roots"]["im"])
+    roots = np.array(g["roots"]["re"]) + 1j * np.array(g["roots"]["im"])
+    base = np.array(g["base_roots"]["re"]) + 1j * np.array(g["base_roots"]["im"])
+    return roots, base
+
+
+def workload_config(n, nnz, roots, base, ws):
+    """The `config` dict, identical in both arms."""
+    return {"workload": "config3-laplace3d-160^3-pi(A)v", "n": n, "nnz": nnz,
+            "eff_degree": len(roots), "base_degree": len(base),
+            "roots": "tests/golden/c3_poly.json (oracle-built degree-50 GMRES polynomial, "
+                     "Leja order, no pof copies needed)",
+            "spmv_launches_per_step": count_launches(roots), "parallelism": f"replicas{ws}",
+            "l2": "inputs larger than L2 (424 MB matrix stream per SpMV vs 126 MB L2)"}
 
 
 def count_launches(roots, two_factor=False):
@@ -151,6 +197,10 @@ def count_launches(roots, two_factor=False):
     return launches
 
 
+# BASELINE config 3 solve settings (configs.py / tests/golden/c3_solve.json)
+SOLVE_C3 = {"m": 40, "k": 20, "nev": 15, "degree": 50, "stability": "pof_auto", "seed": 2}
+
+
 # --------------------------------------------------------------- reference --
 def run_reference(args):
     ws, rank, _ = dist_setup(args.gpus)
@@ -163,7 +213,7 @@ def run_reference(args):
     csr = O.Csr.config(3)
     n, nnz, _ = csr.info()
     A = O.csr_operator(csr)
-    roots = load_golden_poly()
+    roots, base = load_golden_poly()
     bspmv = 12.0 * nnz + 4.0 * (n + 1) + 16.0 * n
     # size the per-step sample: ~3 s of CPU work (after one warm call)
     O.time_poly_factors(A, roots, 1, 1)
@@ -174,18 +224,33 @@ def run_reference(args):
     times = [O.time_poly_factors(A, roots, nf, 1) for _ in range(args.steps)]
     t = float(np.mean(times))
     gbs = nf * bspmv / t / 1e9
+    # time to nev: the oracle's config-3 solve (solve, inc/solver.hpp:91-94),
+    # all host threads, same settings as the GPU arm's time_to_nev
+    solve_info = None
+    if not args.no_solve:
+        p = SOLVE_C3
+        r = O.solve(A, p["m"], p["k"], p["nev"], degree=p["degree"], stability=True,
+                    seed=p["seed"])
+        lam = np.sort(r["eigenvalues"].real)
+        solve_info = {"seconds": round(r["wall"], 4), "converged": r["converged"],
+                      "cycles": r["cycles"], "mvps": r["cost"]["mvps"], "dots": r["cost"]["dots"],
+                      "eff_degree": r["composite_degree"], "smallest": round(float(lam[0]), 6),
+                      "timing": {"total": round(r["wall"], 4)}, "threads": threads,
+                      "params": p}
+    cpu = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+           "sample": f"{nf} of {len(roots)} polynomial factors (SpMV+axpy) per step, "
+                     "oracle restatement of src/gmres_poly.cpp:117-147, OpenMP rows",
+           "sample_factors": nf, **cpu_info()}
     line = {
         "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded generator, BASELINE config 3)", "impl": "reference",
-        "config": {"workload": "config3-laplace3d-160^3-pi(A)v", "n": n, "nnz": nnz,
-                   "eff_degree": len(roots), "sample_factors": nf},
-        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": f"{nf} of {len(roots)} polynomial factors (SpMV+axpy) per step, "
-                                   "oracle restatement of src/gmres_poly.cpp:117-147, OpenMP rows"},
+        "data": "synthetic (seeded generator; BASELINE config 3)", "impl": "reference",
+        "config": workload_config(n, nnz, roots, base, ws),
+        "cpu_baseline": cpu,
         "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "time_to_nev": solve_info,
     }
     print(json.dumps(line), flush=True)
 
@@ -206,7 +271,7 @@ def cpu_baseline_port(roots):
     t = O.time_poly_factors(A, roots, nf, 1)
     return {"value": round(nf * bspmv / t / 1e9, 3), "unit": "GB/s", "cores": 1, "kind": "port",
             "sample": f"{nf} of {len(roots)} factors of pi(A)v on config 3 "
-                      f"({t:.1f} s, single thread, oracle -O3)"}
+                      f"({t:.1f} s, single thread, oracle -O3)", **cpu_info()}
 
 
 def run_b200(args):
@@ -222,6 +287,7 @@ def run_b200(args):
 
     stream = torch.cuda.current_stream()
     ppa.set_stream(stream)
+    clk = ClockSampler(local).start()
     t0 = time.time()
     csr = ppa.CsrMatrix.config(3)
     n, nnz, _ = csr.info()
@@ -232,16 +298,22 @@ def run_b200(args):
     A_auto = ppa.make_csr_operator(csr)
     bspmv = A.model_bytes()
     b = torch.tensor(ppa.normal_vector(n, 2, ppa.STREAM_POLY), device="cuda")
-    base, _ = ppa.build_gmres_poly(A, b, 50)
-    roots = ppa.add_stability_roots(base, len(base))
+    dev_base, _ = ppa.build_gmres_poly(A, b, 50)
+    dev_roots = ppa.add_stability_roots(dev_base, len(dev_base))
     setup_s = time.time() - t0
+    # both arms apply the oracle-built root set (the device-built one agrees
+    # to roundoff, reported as poly_check)
+    roots, base = load_golden_poly()
+    poly_check = {"same_count": len(dev_roots) == len(roots),
+                  "max_rel_diff": (float(np.max(np.abs(dev_roots - roots) / np.abs(roots)))
+                                   if len(dev_roots) == len(roots) else None)}
     launches = count_launches(roots)
     step_bytes = len(roots) * bspmv
 
     v = torch.tensor(ppa.normal_vector(n, 2, ppa.STREAM_ARNOLDI), device="cuda")
     out = torch.empty(n, dtype=torch.float64, device="cuda")
 
-    def time_pi(op, clk_index=None):
+    def time_pi(op):
         def step():
             ppa.apply_poly(roots, op, v, out)
 
@@ -250,23 +322,19 @@ def run_b200(args):
         torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
-        clk = ClockSampler(local) if clk_index is not None else None
-        if clk:
-            clk.__enter__()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
-        e0.record(stream)
-        for _ in range(args.steps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        if clk:
-            clk.__exit__(None, None, None)
+        with clk.region():
+            e0.record(stream)
+            for _ in range(args.steps):
+                step()
+            e1.record(stream)
+            torch.cuda.synchronize()
         ms = reduce_max(e0.elapsed_time(e1), ws, "cuda")
         if ws > 1:
             dist.barrier()
-        return ms / args.steps, clk
+        return ms / args.steps
 
     # e2e: pinned host buffers through the C-ABI batch call: every step does the
     # H2D of its input vector, pi(A)v and the D2H of its result; the copies of
@@ -284,15 +352,16 @@ def run_b200(args):
         torch.cuda.synchronize()
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
-        f0.record(stream)
-        op.apply_host_batch(xh, yh)
-        f1.record(stream)
-        torch.cuda.synchronize()
+        with clk.region():
+            f0.record(stream)
+            op.apply_host_batch(xh, yh)
+            f1.record(stream)
+            torch.cuda.synchronize()
         e_ms = reduce_max(f0.elapsed_time(f1) / ke, ws, "cuda")
         match = bool(np.array_equal(yh[ke - 1].numpy(), out.cpu().numpy()))
         return e_ms, match
 
-    ms_step, clk = time_pi(A, clk_index=local)
+    ms_step = time_pi(A)
     value = whole_job_gbs(step_bytes, ms_step, ws)
     avg_launch_ms = ms_step / launches
     achieved = bspmv / (avg_launch_ms * 1e-3) / 1e9
@@ -303,7 +372,7 @@ def run_b200(args):
 
     # the default layout on the same workload (bit-identical output)
     lay = A_auto.layout()
-    ms_auto, _ = time_pi(A_auto)
+    ms_auto = time_pi(A_auto)
     auto_match = bool(torch.equal(out, ref_out))
     e2e_auto_ms, e2e_auto_match = time_e2e(A_auto)
     two = bool(lay.get("two_factor_pass"))
@@ -379,7 +448,8 @@ def run_b200(args):
             # one-cycle warm-up solve first: loads every kernel the solve uses
             # (lazy module loading) so the timed solve measures the solver
             ppa.solve(op, warm)
-            r = ppa.solve(op, cfg)
+            with clk.region():
+                r = ppa.solve(op, cfg)
             lam = np.sort(r["eigenvalues"].real)
             return {"seconds": round(r["timing"]["total"], 4), "converged": r["converged"],
                     "cycles": r["cycles"], "mvps": r["cost"]["mvps"], "dots": r["cost"]["dots"],
@@ -396,6 +466,7 @@ def run_b200(args):
         warm.orthogonalization = "cgs2"
         solve_info["cgs2"] = solve_on(A_auto)
 
+    clk.stop()
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_port(roots)
@@ -412,10 +483,7 @@ def run_b200(args):
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms_step, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator; BASELINE config 3)",
-            "config": {"workload": "config3-laplace3d-160^3-pi(A)v", "n": n, "nnz": nnz,
-                       "eff_degree": len(roots), "base_degree": len(base),
-                       "spmv_launches_per_step": launches, "parallelism": f"replicas{ws}",
-                       "l2": "inputs larger than L2 (424 MB matrix stream per SpMV vs 126 MB L2)"},
+            "config": workload_config(n, nnz, roots, base, ws),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "kernel": "k_spmv_sell32 (fused real-root factor)",
@@ -426,9 +494,18 @@ def run_b200(args):
                                          if traffic else None),
                          "traffic_frac": (round(traffic / (avg_launch_ms * 1e-3) / 1e9 / peak, 4)
                                           if traffic else None)},
-            "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
-                    "d2h_bytes_per_step": 8 * n, "ms_per_step": round(e2e_ms, 4),
-                    "steps": ke, "matches_device_result": e2e_match},
+            # e2e: the call a user makes - make_csr_operator(A) (automatic
+            # layout), make_poly_operator, apply with host vectors through the
+            # C-ABI (ppa_op_apply_host_batch); H2D of v and D2H of pi(A)v in the
+            # timed region.  Same metric and unit as `value` (north-star bytes
+            # per pi(A)v); the SELL-32 layout's e2e is e2e_sell32.
+            "e2e": {"value": round(whole_job_gbs(step_bytes, e2e_auto_ms, ws), 3), "unit": "GB/s",
+                    "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+                    "ms_per_step": round(e2e_auto_ms, 4), "steps": ke,
+                    "layout": lay["layout"] + " (automatic, make_csr_operator default)",
+                    "matches_device_result": e2e_auto_match},
+            "e2e_sell32": {"value": round(e2e_val, 3), "unit": "GB/s", "ms_per_step": round(e2e_ms, 4),
+                           "matches_device_result": e2e_match},
             "default_layout": default_layout,
             "gpu_launches": launches * args.steps,
             "layout": "sell32 (fp64 values, int32 columns)",
@@ -440,6 +517,7 @@ def run_b200(args):
                      "breakdown_flag": cgs_flag},
             "time_to_nev": solve_info,
             "setup_seconds": round(setup_s, 3),
+            "poly_check": poly_check,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -469,7 +547,7 @@ def run_sharded(args):
     csr = ppa.CsrMatrix.config(3)
     n, nnz, _ = csr.info()
     bspmv = 12.0 * nnz + 4.0 * (n + 1) + 16.0 * n
-    roots = load_golden_poly()
+    roots, _ = load_golden_poly()
     plan = HaloPlan.build(*csr.arrays(), n, dist)
     sp = ShardedPoly(plan, CudaBackend(plan), dist)
     r0, r1 = plan.ranges[rank]

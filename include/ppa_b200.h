@@ -42,6 +42,11 @@ enum {
 /* OperatorKind (inc/operators.hpp:43) */
 enum { PPA_KIND_CSR = 0, PPA_KIND_DIAGONAL = 1, PPA_KIND_SHIFTED = 2, PPA_KIND_BLOCK2 = 3,
        PPA_KIND_POLY = 4, PPA_KIND_COMPOSITE = 5 };
+/* Orthogonalization of the device Arnoldi (ours).  The C++
+   and Python SolveConfig default is PPA_ORTHO_DCGS2; a zero-filled
+   ppa_solve_config is not a default configuration (m = 0 is invalid), use
+   ppa_solve_config_default. */
+enum { PPA_ORTHO_CGS2 = 0, PPA_ORTHO_DCGS2 = 1 };
 /* RitzOrdering (inc/arnoldi.hpp:40) */
 enum { PPA_SMALLEST_MAGNITUDE = 0, PPA_LARGEST_MAGNITUDE = 1, PPA_TARGET_ONE = 2 };
 
@@ -131,9 +136,15 @@ int ppa_csr_two_factor_pass(const ppa_op* op, int* supported);
 /* apply_poly (src/gmres_poly.cpp:117-147): out_dev = pi(A) v_dev */
 int ppa_apply_poly(const double* re, const double* im, int nroots, const ppa_op* a,
                    const double* v_dev, double* out_dev, ppa_cost* cost);
-/* build_gmres_poly (src/gmres_poly.cpp:95-115); re/im capacity >= degree */
+/* build_gmres_poly (src/gmres_poly.cpp:95-115); re/im capacity >= degree.
+   Delayed CGS2 (PPA_ORTHO_DCGS2), the solver's default. */
 int ppa_build_gmres_poly(const ppa_op* a, const double* b_dev, int degree, double* re,
                          double* im, int* nroots, int* truncated, ppa_cost* cost);
+/* Same with the orthogonalisation chosen (PPA_ORTHO_CGS2 / PPA_ORTHO_DCGS2);
+   ppa_solve passes its config's orthogonalization to every polynomial build */
+int ppa_build_gmres_poly_ortho(const ppa_op* a, const double* b_dev, int degree, int ortho,
+                               double* re, double* im, int* nroots, int* truncated,
+                               ppa_cost* cost);
 /* leja_order (src/gmres_poly.cpp:38-93) */
 int ppa_leja_order(const double* re, const double* im, int n, double* out_re, double* out_im);
 /* compute_pof (src/gmres_poly.cpp:155-179); arrays sized >= n */
@@ -218,7 +229,9 @@ typedef struct ppa_solve_config {
   int stagnation_stop, stagnation_window;
   double stagnation_rtol;
   int want_eigenvectors;     /* keep unit eigenvectors for evec_re/evec_im */
-  int orthogonalization;     /* 0 CGS2, 1 delayed CGS2 (the C++ and Python SolveConfig default) */
+  int orthogonalization;     /* PPA_ORTHO_CGS2 or PPA_ORTHO_DCGS2 (the default of
+                                ppa_solve_config_default, C++ and Python); also used by
+                                every polynomial build of the solve */
 } ppa_solve_config;
 
 /* EigResult (inc/solver.hpp:71-89); arrays supplied by the caller */
@@ -251,6 +264,8 @@ typedef struct ppa_solve_result {
   long long evec_ld;
 } ppa_solve_result;
 
+/* Fill *cfg with the defaults of SolveConfig (inc/solver.hpp:21-58) */
+int ppa_solve_config_default(ppa_solve_config* cfg);
 /* solve (inc/solver.hpp:94) or solve_double (inc/solver.hpp:111) */
 int ppa_solve(const ppa_op* a, const ppa_solve_config* cfg, ppa_solve_result* res);
 /* check_ideal_order (inc/solver.hpp:99): 1 if the condition holds */

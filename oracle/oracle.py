@@ -42,6 +42,8 @@ def lib():
         L.orc_last_error.restype = C.c_char_p
         L.orc_set_threads.argtypes = [C.c_int]
         L.orc_set_threads.restype = None
+        L.orc_set_variant.argtypes = [C.c_int]
+        L.orc_set_variant.restype = None
         L.orc_max_threads.restype = C.c_int
         sig = {
             "orc_gen_config": [C.c_int, C.POINTER(vp)],
@@ -123,6 +125,17 @@ def _ri(roots):
 
 def set_threads(t: int) -> None:
     lib().orc_set_threads(int(t))
+
+
+def set_variant(v: int) -> None:
+    """Roundoff-floor probes (not the reference): 0 = reference MGS2 with
+    sequential dots (default), 1 = classical CGS2 + blocked dots, 2 = MGS2 +
+    blocked dots (ppa_oracle.cpp g_variant)."""
+    lib().orc_set_variant(int(v))
+
+
+def get_variant() -> int:
+    return int(lib().orc_get_variant())
 
 
 def max_threads() -> int:

@@ -26,6 +26,9 @@
 // twice, as the reference's un-flagged build (CMakeLists.txt:1-6) does.
 // Threading (OpenMP) is used only where it cannot change results: the
 // row loop of the SpMV and elementwise axpy/scale.  Dots are sequential.
+// orc_set_variant(1|2) switches to the roundoff-floor probes (classical
+// CGS2 / blocked dots, see g_variant); variant 0, the default, is the
+// reference restatement every parity test uses.
 // ===========================================================================
 
 #include <omp.h>
@@ -71,10 +74,38 @@ struct Cost {
   double nnzr = 0.0, wall_seconds = 0.0;
 };
 
+// Roundoff-floor probe (NOT the reference; test infrastructure for
+// tests/golden/roundoff_floor.json).  Variant 0 is the reference: MGS2 with
+// sequential dot products (src/arnoldi.cpp:129-140, inc/cost.hpp:51-76).
+// Variants 1 and 2 change only the floating-point summation order, which the
+// reference leaves to Eigen (unpinned): 1 = classical CGS2 (all coefficients
+// of a pass from the same w) with blocked dots, 2 = MGS2 with blocked dots.
+// A blocked dot sums 4096-element chunks in order, then the chunk sums in
+// order, so it is deterministic for any thread count.  The spread of the
+// three variants' results is the oracle's own roundoff floor on a problem.
+int g_variant = 0;
+constexpr long kDotChunk = 4096;
+
+double blocked_sum(const double* x, const double* y, long n) {
+  const long nc = (n + kDotChunk - 1) / kDotChunk;
+  std::vector<double> part(static_cast<size_t>(nc));
+#pragma omp parallel for schedule(static)
+  for (long b = 0; b < nc; ++b) {
+    double s = 0.0;
+    const long e = std::min(n, (b + 1) * kDotChunk);
+    for (long i = b * kDotChunk; i < e; ++i) s += x[i] * y[i];
+    part[static_cast<size_t>(b)] = s;
+  }
+  double s = 0.0;
+  for (long b = 0; b < nc; ++b) s += part[static_cast<size_t>(b)];
+  return s;
+}
+
 // inc/cost.hpp:51-76 - counted length-n kernels.
 double dot(const double* x, const double* y, long n, Cost& c) {
   ++c.dots;
   ++c.vops;
+  if (g_variant != 0) return blocked_sum(x, y, n);
   double s = 0.0;
   for (long i = 0; i < n; ++i) s += x[i] * y[i];
   return s;
@@ -82,6 +113,7 @@ double dot(const double* x, const double* y, long n, Cost& c) {
 double norm(const double* x, long n, Cost& c) {
   ++c.dots;
   ++c.vops;
+  if (g_variant != 0) return std::sqrt(blocked_sum(x, x, n));
   double s = 0.0;
   for (long i = 0; i < n; ++i) s += x[i] * x[i];
   return std::sqrt(s);
@@ -686,15 +718,27 @@ void arnoldi_extend(State& st, const Op& op, int to_dim, Cost& c) {
   Vec w(n);
   for (int j = st.cur_dim; j < to_dim; ++j) {
     op.apply(st.col(j), w.data(), c);
-    for (int i = 0; i <= j; ++i) {
-      const double h = dot(st.col(i), w.data(), n, c);
-      st.H(i, j) = h;
-      axpy(-h, st.col(i), w.data(), n, c);
-    }
-    for (int i = 0; i <= j; ++i) {
-      const double h = dot(st.col(i), w.data(), n, c);
-      st.H(i, j) += h;
-      axpy(-h, st.col(i), w.data(), n, c);
+    if (g_variant == 1) {
+      // roundoff-floor variant 1: classical Gram-Schmidt, two passes
+      std::vector<double> h(static_cast<size_t>(j) + 1);
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int i = 0; i <= j; ++i) h[i] = dot(st.col(i), w.data(), n, c);
+        for (int i = 0; i <= j; ++i) {
+          st.H(i, j) = pass == 0 ? h[i] : st.H(i, j) + h[i];
+          axpy(-h[i], st.col(i), w.data(), n, c);
+        }
+      }
+    } else {
+      for (int i = 0; i <= j; ++i) {
+        const double h = dot(st.col(i), w.data(), n, c);
+        st.H(i, j) = h;
+        axpy(-h, st.col(i), w.data(), n, c);
+      }
+      for (int i = 0; i <= j; ++i) {
+        const double h = dot(st.col(i), w.data(), n, c);
+        st.H(i, j) += h;
+        axpy(-h, st.col(i), w.data(), n, c);
+      }
     }
     const double hsub = norm(w.data(), n, c);
     st.H(j + 1, j) = hsub;
@@ -1572,6 +1616,8 @@ extern "C" {
 
 const char* orc_last_error() { return g_err.c_str(); }
 void orc_set_threads(int t) { omp_set_num_threads(t < 1 ? 1 : t); }
+void orc_set_variant(int v) { orc::g_variant = (v >= 0 && v <= 2) ? v : 0; }
+int orc_get_variant(void) { return orc::g_variant; }
 int orc_max_threads() { return omp_get_max_threads(); }
 
 int orc_gen_config(int c, orc_csr** out) {

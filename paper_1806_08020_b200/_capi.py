@@ -123,6 +123,9 @@ def lib():
             "ppa_arnoldi_set_orthogonalization": [vp, C.c_int],
             "ppa_apply_poly": [vp, vp, C.c_int, vp, vp, vp, C.POINTER(CostRecord)],
             "ppa_build_gmres_poly": [vp, vp, C.c_int, vp, vp, _ip, _ip, C.POINTER(CostRecord)],
+            "ppa_build_gmres_poly_ortho": [vp, vp, C.c_int, C.c_int, vp, vp, _ip, _ip,
+                                           C.POINTER(CostRecord)],
+            "ppa_solve_config_default": [vp],
             "ppa_leja_order": [vp, vp, C.c_int, vp, vp],
             "ppa_compute_pof": [vp, vp, C.c_int, vp, vp, _ip, _dp, _ip],
             "ppa_add_stability_roots": [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, _ip],
@@ -461,14 +464,17 @@ def apply_poly(roots, a: LinearOperator, v, out, rec: Optional[CostRecord] = Non
     return rec
 
 
-def build_gmres_poly(a: LinearOperator, b, degree: int, rec: Optional[CostRecord] = None):
+def build_gmres_poly(a: LinearOperator, b, degree: int, rec: Optional[CostRecord] = None,
+                     orthogonalization: str = "dcgs2"):
     """Returns (roots complex128 in Leja order, truncated)."""
     re = np.zeros(max(degree, 1))
     im = np.zeros(max(degree, 1))
     nr, tr = C.c_int(), C.c_int()
     rec = rec if rec is not None else CostRecord()
-    _check(lib().ppa_build_gmres_poly(a._h, _ptr(b), degree, _np_ptr(re), _np_ptr(im),
-                                      C.byref(nr), C.byref(tr), C.byref(rec)))
+    _check(lib().ppa_build_gmres_poly_ortho(a._h, _ptr(b), degree,
+                                            {"cgs2": 0, "dcgs2": 1}[orthogonalization],
+                                            _np_ptr(re), _np_ptr(im),
+                                            C.byref(nr), C.byref(tr), C.byref(rec)))
     return re[:nr.value] + 1j * im[:nr.value], bool(tr.value)
 
 

@@ -296,10 +296,13 @@ void extend_dcgs2(ArnoldiState& st, const LinearOperator& op, int to_dim, CostRe
       return;
     }
     ++rec.vops;  // the scaling of v_j (src/arnoldi.cpp:149-150)
-    // g = H(0:j, 0:j-1) s (upper Hessenberg)
+    // g = H(0:j, 0:j-1) s over every row: after thick_restart the leading
+    // restart_k columns are full (rows 0..restart_k), so H is not upper
+    // Hessenberg there (src/arnoldi.cpp:326-333).
     g.assign(static_cast<size_t>(j) + 1, 0.0);
     for (int k = 0; k < j; ++k) {
-      for (int i = 0; i <= k + 1; ++i) g[i] += st.h(i, k) * sv[k];
+      const int last = std::min(j, std::max(k + 1, st.restart_k));
+      for (int i = 0; i <= last; ++i) g[i] += st.h(i, k) * sv[k];
     }
     hcol.assign(static_cast<size_t>(j) + 1, 0.0);
     for (int k = 0; k < j; ++k) hcol[k] = (t[k] - g[k]) / rho;
@@ -330,11 +333,10 @@ void extend_dcgs2(ArnoldiState& st, const LinearOperator& op, int to_dim, CostRe
   ++rec.vops;
 }
 
-// DCGS2 is opt-in (ArnoldiState::ortho, SolveConfig::orthogonalization):
-// it is as stable as CGS2 but its roundoff differs enough that borderline
-// convergence tests can flip by a cycle (config 3 converges in 4 cycles
-// instead of the oracle's 5), which breaks the matvec-count parity the
-// reference comparison asks for.  A single-step extend keeps CGS2 (the
+// Delayed CGS2 is the solver's default (SolveConfig::orthogonalization,
+// DESIGN.md 3.2); a bare ArnoldiState starts in CGS2.  Its roundoff differs
+// from CGS2's, so matvec-count parity with the oracle is a property of the
+// current kernels, not a guarantee.  A single-step extend keeps CGS2 (the
 // delayed form would need a flush pass as well).
 bool use_dcgs2(const ArnoldiState& st, int steps) {
   return st.ortho == Orthogonalization::dcgs2 && steps >= 2;

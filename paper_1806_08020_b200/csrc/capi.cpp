@@ -144,7 +144,7 @@ void roots_out(const ppa::PolyPrecond& p, double* re, double* im, int cap, int* 
 extern "C" {
 
 const char* ppa_last_error(void) { return t_err.c_str(); }
-int ppa_abi_version(void) { return 2; }
+int ppa_abi_version(void) { return 3; }
 
 int ppa_device_info(int* sm_count, double* l2_bytes) {
   return guard([&] {
@@ -460,14 +460,19 @@ int ppa_apply_poly(const double* re, const double* im, int nroots, const ppa_op*
   });
 }
 
-int ppa_build_gmres_poly(const ppa_op* a, const double* b, int degree, double* re, double* im,
-                         int* nroots, int* truncated, ppa_cost* cost) {
+int ppa_build_gmres_poly_ortho(const ppa_op* a, const double* b, int degree, int ortho,
+                               double* re, double* im, int* nroots, int* truncated,
+                               ppa_cost* cost) {
   return guard([&] {
     need(a, "ppa_build_gmres_poly");
     need(re, "ppa_build_gmres_poly");
     need(im, "ppa_build_gmres_poly");
+    if (ortho != PPA_ORTHO_CGS2 && ortho != PPA_ORTHO_DCGS2) {
+      throw std::invalid_argument("build_gmres_poly: orthogonalization must be 0 or 1");
+    }
     ppa::CostRecord r;
-    const ppa::PolyPrecond p = ppa::build_gmres_poly(*a->p, b, degree, r);
+    const ppa::PolyPrecond p =
+        ppa::build_gmres_poly(*a->p, b, degree, r, static_cast<ppa::Orthogonalization>(ortho));
     for (size_t i = 0; i < p.roots.size(); ++i) {
       re[i] = p.roots[i].real();
       im[i] = p.roots[i].imag();
@@ -476,6 +481,12 @@ int ppa_build_gmres_poly(const ppa_op* a, const double* b, int degree, double* r
     if (truncated) *truncated = p.truncated ? 1 : 0;
     add_cost(cost, r);
   });
+}
+
+int ppa_build_gmres_poly(const ppa_op* a, const double* b, int degree, double* re, double* im,
+                         int* nroots, int* truncated, ppa_cost* cost) {
+  return ppa_build_gmres_poly_ortho(a, b, degree, PPA_ORTHO_DCGS2, re, im, nroots, truncated,
+                                    cost);
 }
 
 int ppa_leja_order(const double* re, const double* im, int n, double* out_re, double* out_im) {
@@ -708,6 +719,33 @@ int ppa_ts_combine(const double* V, long long ldv, int n, int d, const double* G
                    double* Out, long long ldo) {
   return guard([&] {
     ppa::kern::ts_combine(V, ldv, n, d, G, p, Out, ldo, ppa::current_context().stream());
+  });
+}
+
+int ppa_solve_config_default(ppa_solve_config* c) {
+  return guard([&] {
+    need(c, "ppa_solve_config_default");
+    const ppa::SolveConfig d;
+    *c = ppa_solve_config{};
+    c->m = d.m;
+    c->k = d.k;
+    c->nev = d.nev;
+    c->degree = d.degree;
+    c->rtol_multiplier = d.rtol_multiplier;
+    c->rtol_absolute = 0.0;
+    c->variant = 0;
+    c->stability = 0;
+    c->max_cycles = d.max_cycles;
+    c->seed = d.seed;
+    c->damping_alpha = d.damping_alpha;
+    c->damping_power = d.damping_power;
+    c->check_mid_cycle = d.check_mid_cycle ? 1 : 0;
+    c->mid_cycle_stride = d.mid_cycle_stride;
+    c->stagnation_stop = d.stagnation_stop ? 1 : 0;
+    c->stagnation_window = d.stagnation_window;
+    c->stagnation_rtol = d.stagnation_rtol;
+    c->want_eigenvectors = d.want_eigenvectors ? 1 : 0;
+    c->orthogonalization = static_cast<int>(d.orthogonalization);
   });
 }
 

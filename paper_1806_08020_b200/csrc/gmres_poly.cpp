@@ -100,7 +100,7 @@ std::vector<cplx> leja_order(const std::vector<cplx>& roots) {
 }
 
 PolyPrecond build_gmres_poly(const LinearOperator& a, const double* b, int degree,
-                             CostRecord& rec) {
+                             CostRecord& rec, Orthogonalization ortho) {
   if (degree < 1) throw std::invalid_argument("build_gmres_poly: degree < 1");
   if (b == nullptr) throw std::invalid_argument("build_gmres_poly: dimension mismatch");
   // Uncounted, like the reference's b.norm() guard (src/gmres_poly.cpp:101).
@@ -109,9 +109,9 @@ PolyPrecond build_gmres_poly(const LinearOperator& a, const double* b, int degre
   }
   const int d = std::min(degree, a.dim());
   ArnoldiState st = arnoldi_init(b, a.dim(), d, rec);
-  // delayed CGS2 (two sweeps over the basis per step instead of three; the
-  // reference's MGS2 counters are charged either way, arnoldi.cpp)
-  st.ortho = Orthogonalization::dcgs2;
+  // delayed CGS2 by default (two sweeps over the basis per step instead of
+  // three; the reference's MGS2 counters are charged either way, arnoldi.cpp)
+  st.ortho = ortho;
   arnoldi_extend(st, a, d, rec);
 
   PolyPrecond p;

@@ -51,9 +51,12 @@ struct PofReport {
 // ---- construction --------------------------------------------------------
 // GMRES(d) from the device start vector b: d = min(degree, n) Arnoldi steps
 // (device CGS2), harmonic Ritz values on the host, then Leja order
-// (reference src/gmres_poly.cpp:95-115).
+// (reference src/gmres_poly.cpp:95-115).  `ortho` selects the device
+// orthogonalisation of that Arnoldi run (the reference's MGS2 counters are
+// charged either way); the solver passes SolveConfig::orthogonalization.
 PolyPrecond build_gmres_poly(const LinearOperator& a, const double* b, int degree,
-                             CostRecord& rec);
+                             CostRecord& rec,
+                             Orthogonalization ortho = Orthogonalization::dcgs2);
 // Two start vectors: GMRES on diag(A, A) from [b1; b2] with each half scaled
 // to norm 1/sqrt(2) (src/gmres_poly.cpp:228-264).
 PolyPrecond build_two_vector_poly(const OperatorPtr& a, const double* b1, const double* b2,

@@ -55,7 +55,7 @@ struct SolveConfig {
   double stagnation_rtol = 0.01;  // run until max-residual stalls
   EigenList reference;
   bool want_eigenvectors = false;  // materialise EigResult::eigenvectors
-  // cycle orthogonalisation (ours; the polynomial build always uses CGS2)
+  // orthogonalisation of the cycles and of the polynomial builds (ours)
   Orthogonalization orthogonalization = Orthogonalization::dcgs2;
   bool allow_nev_above_k = false;
 

@@ -458,7 +458,7 @@ PolyPrecond damping_search(const OperatorPtr& a, const SolveConfig& cfg, CostRec
   bool damped = false;
   for (;;) {
     const double* start = damped ? ab.get() : b.get();
-    PolyPrecond p = stabilise(build_gmres_poly(*a, start, d, rec), cfg);
+    PolyPrecond p = stabilise(build_gmres_poly(*a, start, d, rec, cfg.orthogonalization), cfg);
     if (damped) {
       p.provenance = PolyProvenance::damped;
       p.damping_power = 1;
@@ -636,12 +636,12 @@ EigResult solve(const OperatorPtr& a, const SolveConfig& cfg) {
         // damped start A^power b + alpha b (section 6)
         DBuffer<double> bd(static_cast<size_t>(a->dim()));
         damped_start(*a, b.get(), cfg.damping_alpha, cfg.damping_power, bd.get(), rec);
-        p = build_gmres_poly(*a, bd.get(), cfg.degree, rec);
+        p = build_gmres_poly(*a, bd.get(), cfg.degree, rec, cfg.orthogonalization);
         p.provenance = PolyProvenance::damped;
         p.damping_alpha = cfg.damping_alpha;
         p.damping_power = cfg.damping_power;
       } else {
-        p = build_gmres_poly(*a, b.get(), cfg.degree, rec);
+        p = build_gmres_poly(*a, b.get(), cfg.degree, rec, cfg.orthogonalization);
       }
       p = stabilise(p, cfg);
     }
@@ -677,11 +677,11 @@ EigResult solve_double(const OperatorPtr& a, const SolveConfig& cfg) {
   auto t0 = Clock::now();
   StartVectors sv(a->dim(), cfg.seed, solve_streams(*a, {rng::kPolyStart, rng::kPoly2Start}));
   PoolBuffer b1 = sv.take(rng::kPolyStart);
-  PolyPrecond p1 = build_gmres_poly(*a, b1.get(), cfg.double_d1, rec);
+  PolyPrecond p1 = build_gmres_poly(*a, b1.get(), cfg.double_d1, rec, cfg.orthogonalization);
   p1.provenance = PolyProvenance::composite_stage;
   OperatorPtr tau = make_poly_complement_operator(a, p1);
   PoolBuffer b2 = sv.take(rng::kPoly2Start);
-  PolyPrecond p2 = build_gmres_poly(*tau, b2.get(), cfg.double_d2, rec);
+  PolyPrecond p2 = build_gmres_poly(*tau, b2.get(), cfg.double_d2, rec, cfg.orthogonalization);
   if (cfg.stability == StabilityMode::pof_auto && p2.roots.size() >= 2) {
     p2 = add_stability_roots(p2);
   }

@@ -22,7 +22,7 @@
 
 int main(int argc, char** argv) {
   const int config = argc > 1 ? atoi(argv[1]) : 1;
-  if (ppa_abi_version() < 2) return 2;
+  if (ppa_abi_version() < 3) return 2;
   ppa_host_csr* h = NULL;
   CHECK(ppa_gen_config(config, &h));
   int n = 0;
@@ -33,7 +33,7 @@ int main(int argc, char** argv) {
   CHECK(ppa_csr_operator(h, &a));
 
   ppa_solve_config cfg;
-  memset(&cfg, 0, sizeof cfg); /* zero = defaults for the optional members */
+  CHECK(ppa_solve_config_default(&cfg)); /* SolveConfig's defaults (delayed CGS2) */
   cfg.m = 30;
   cfg.k = 15;
   cfg.nev = 10;

@@ -74,7 +74,33 @@ def _solve_fixture(cfg_id, **kw):
             "oracle_seconds": time.time() - t}
 
 
+def _variant_solve(cfg_id, variant, **kw):
+    O.set_variant(variant)
+    try:
+        return _solve_fixture(cfg_id, **kw)
+    finally:
+        O.set_variant(0)
+
+
+SOLVE_PARAMS = {
+    2: dict(m=50, k=20, nev=20, degree=25, seed=1),
+    5: dict(m=30, k=15, nev=20, double=(15, 20), seed=3, allow_nev_above_k=True),
+}
+
+
+def roundoff_floor():
+    """The oracle's own roundoff floor on the non-normal configs 2 and 5: the
+    same solve under two more summation orders the reference leaves to Eigen
+    (oracle variants 1 = classical CGS2 + blocked dots, 2 = MGS2 + blocked
+    dots; ppa_oracle.cpp g_variant).  Variant 0 is c{2,5}_solve.json."""
+    out = {}
+    for cfg_id, kw in SOLVE_PARAMS.items():
+        out[f"config{cfg_id}"] = {str(v): _variant_solve(cfg_id, v, **kw) for v in (1, 2)}
+    return out
+
+
 FIXTURES = {
+    "roundoff_floor": roundoff_floor,
     "fingerprints": fingerprints,
     "c3_poly": c3_poly,
     "c1_solve": lambda: _solve_fixture(1, m=30, k=15, nev=10, degree=10, seed=1),

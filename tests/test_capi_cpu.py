@@ -39,7 +39,18 @@ def test_library_is_sm100a():
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", so],
                          capture_output=True, text=True).stdout
     assert "sm_100a" in out
-    assert ppa.lib().ppa_abi_version() == 2
+    assert ppa.lib().ppa_abi_version() == 3
+
+
+def test_solve_config_default_matches_cpp():
+    # ppa_solve_config_default fills SolveConfig's defaults (inc/solver.hpp:21-58),
+    # including the delayed-CGS2 orthogonalisation the C++/Python layers use
+    from paper_1806_08020_b200 import _capi
+    c = _capi._SolveConfigC()
+    assert ppa.lib().ppa_solve_config_default(ctypes.byref(c)) == 0
+    assert (c.m, c.k, c.nev, c.degree, c.max_cycles) == (50, 20, 15, 0, 100)
+    assert c.rtol_multiplier == 1e-8 and c.rtol_absolute == 0.0
+    assert c.orthogonalization == 1 and ppa.SolveConfig().orthogonalization == "dcgs2"
 
 
 @pytest.mark.parametrize("name,gen", [

@@ -467,14 +467,16 @@ def test_build_gmres_poly_vs_oracle(cuda, gen, deg):
     P, Q = gen(ppa.CsrMatrix), gen(O.Csr)
     n = P.n
     b = O.normal_vector(n, 1, 2)
-    rec = ppa.CostRecord()
-    roots, trunc = ppa.build_gmres_poly(ppa.make_csr_operator(P), dev(cuda, b), deg, rec)
     cost = np.zeros(3)
     oroots, otrunc = O.build_gmres_poly(O.csr_operator(Q), b, deg, cost)
-    assert trunc == otrunc and len(roots) == len(oroots)
-    # same Leja permutation, roots equal to roundoff (CGS2 vs MGS2)
-    assert np.max(np.abs(roots - oroots) / np.abs(oroots)) < 1e-8
-    assert (rec.mvps, rec.dots, rec.vops) == tuple(int(c) for c in cost)
+    for ortho in ("cgs2", "dcgs2"):
+        rec = ppa.CostRecord()
+        roots, trunc = ppa.build_gmres_poly(ppa.make_csr_operator(P), dev(cuda, b), deg, rec,
+                                            orthogonalization=ortho)
+        assert trunc == otrunc and len(roots) == len(oroots)
+        # same Leja permutation, roots equal to roundoff (CGS2 / DCGS2 vs MGS2)
+        assert np.max(np.abs(roots - oroots) / np.abs(oroots)) < 1e-8, ortho
+        assert (rec.mvps, rec.dots, rec.vops) == tuple(int(c) for c in cost)
     # minimum-residual property: ||pi(A) b|| equals the GMRES(d) residual
     A = ppa.make_csr_operator(P)
     out = cuda.empty(n, dtype=cuda.float64, device="cuda")
@@ -603,6 +605,30 @@ def test_thick_restart_preserves_pairs(cuda, ortho):
     Vh = _read_V(cuda, st, 100, 21)
     R = np.diag(d) @ Vh[:, :20] - Vh @ st.H
     assert np.linalg.norm(R) <= 1e-9 * max(1.0, np.linalg.norm(st.H))
+
+
+def test_extend_after_restart_nonsymmetric(cuda, ortho):
+    # after thick_restart H's leading block is full, not Hessenberg
+    # (src/arnoldi.cpp:326-333); the next extend must keep the Arnoldi
+    # relation A V_m = V_{m+1} H to roundoff under either orthogonalisation
+    P = ppa.CsrMatrix.convection_diffusion(30)
+    n = P.n
+    A = ppa.make_csr_operator(P)
+    m, k = 30, 12
+    st = ppa.arnoldi_init(dev(cuda, O.normal_vector(n, 6, 3)), n, m)
+    st.set_orthogonalization(ortho)
+    Ad = _dense(P)
+    for cycle in range(3):
+        st.extend(A, m)
+        assert st.cur_dim == m and not st.breakdown
+        Vh = _read_V(cuda, st, n, m + 1)
+        H = st.H
+        assert np.linalg.norm(Vh.T @ Vh - np.eye(m + 1)) <= 1e-10
+        R = Ad @ Vh[:, :m] - Vh @ H
+        assert np.linalg.norm(R) <= 1e-9 * max(1.0, np.linalg.norm(H)), (cycle, np.linalg.norm(R))
+        kk = st.thick_restart(k, ppa.SMALLEST_MAGNITUDE)
+        # the restarted block is genuinely non-Hessenberg for this matrix
+        assert np.abs(np.tril(st.H[:kk + 1, :kk], -2)).max() > 1e-6 * np.abs(st.H).max()
 
 
 def test_breakdown_late_invariant_subspace(cuda, ortho):
