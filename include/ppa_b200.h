@@ -131,6 +131,10 @@ int ppa_csr_layout(const ppa_op* op, int* layout, double* stream_bytes, int* sig
    diagonal layout (stencils).  No reference
    counterpart: an introspection hook next to ppa_csr_layout. */
 int ppa_csr_two_factor_pass(const ppa_op* op, int* supported);
+/* CSR operators: the box-grid form of the two-factor pass (spmv_grid2.cu):
+   nx, ny, nz of the 7-point (3-D) or 5-point (2-D, ny = 1) stencil the matrix
+   is, or nx = 0; *supported = 1 when that form runs.  Introspection only. */
+int ppa_csr_grid_form(const ppa_op* op, int* nx, int* ny, int* nz, int* supported);
 
 /* ---- polynomial -------------------------------------------------------- */
 /* apply_poly (src/gmres_poly.cpp:117-147): out_dev = pi(A) v_dev */

@@ -120,6 +120,7 @@ def lib():
             "ppa_host_csr_multiply": [vp, vp, vp],
             "ppa_csr_operator_layout": [vp, C.c_int, C.POINTER(vp)],
             "ppa_csr_two_factor_pass": [vp, _ip],
+            "ppa_csr_grid_form": [vp, _ip, _ip, _ip, _ip],
             "ppa_arnoldi_set_orthogonalization": [vp, C.c_int],
             "ppa_apply_poly": [vp, vp, C.c_int, vp, vp, vp, C.POINTER(CostRecord)],
             "ppa_build_gmres_poly": [vp, vp, C.c_int, vp, vp, _ip, _ip, C.POINTER(CostRecord)],
@@ -383,9 +384,14 @@ class LinearOperator:
                                     C.byref(nd)))
         two = C.c_int()
         _check(lib().ppa_csr_two_factor_pass(self._h, C.byref(two)))
+        gx, gy, gz, g2 = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        _check(lib().ppa_csr_grid_form(self._h, C.byref(gx), C.byref(gy), C.byref(gz),
+                                       C.byref(g2)))
         return {"layout": ("csr", "sell32", "sell32_packed", "dia_coded")[lay.value],
                 "stream_bytes": sb.value, "sigma": sig.value, "dict_size": nd.value,
-                "two_factor_pass": bool(two.value)}
+                "two_factor_pass": bool(two.value),
+                "grid": (gx.value, gy.value, gz.value) if gx.value else None,
+                "grid_pass": bool(g2.value)}
 
 
 LAYOUTS = {"auto": 0, "csr": 1, "sell32": 2, "sell32_packed": 3, "dia_coded": 4}

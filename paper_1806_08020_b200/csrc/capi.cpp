@@ -449,6 +449,19 @@ int ppa_csr_two_factor_pass(const ppa_op* op, int* supported) {
   });
 }
 
+int ppa_csr_grid_form(const ppa_op* op, int* nx, int* ny, int* nz, int* supported) {
+  return guard([&] {
+    need(op, "ppa_csr_grid_form");
+    const auto* c = dynamic_cast<const ppa::CsrOperator*>(op->p.get());
+    if (!c) throw std::invalid_argument("ppa_csr_grid_form: not a CSR operator");
+    const ppa::kern::CsrDevice& d = c->device();
+    if (nx) *nx = d.grid_nx;
+    if (ny) *ny = d.grid_ny;
+    if (nz) *nz = d.grid_nz;
+    if (supported) *supported = ppa::kern::grid2_supported(d) ? 1 : 0;
+  });
+}
+
 int ppa_apply_poly(const double* re, const double* im, int nroots, const ppa_op* a,
                    const double* v, double* out, ppa_cost* cost) {
   return guard([&] {

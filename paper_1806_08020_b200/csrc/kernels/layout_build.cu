@@ -282,6 +282,30 @@ __global__ void k_dia_presence(const unsigned char* __restrict__ codes, int n, i
   if (!ok) atomicOr(bad, 1);
 }
 
+// Counts the rows whose presence byte differs from the geometric presence of
+// a box-grid stencil: nd = 7: offsets (-nx ny, -nx, -1, 0, 1, nx, nx ny) on an
+// nx x ny x nz grid; nd = 5: (-nx, -1, 0, 1, nx) on nx x nz.  Diagonal j is
+// present exactly when its neighbour lies inside the box (Dirichlet cut).
+__global__ void k_grid_check(const unsigned char* __restrict__ pres, int n, int nd, int nx,
+                             int ny, int nz, int* __restrict__ bad) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int x = static_cast<int>(i % nx);
+  const long long rest = i / nx;
+  unsigned want;
+  if (nd == 7) {
+    const int y = static_cast<int>(rest % ny);
+    const int z = static_cast<int>(rest / ny);
+    want = (z > 0 ? 1u : 0u) | (y > 0 ? 2u : 0u) | (x > 0 ? 4u : 0u) | 8u |
+           (x < nx - 1 ? 16u : 0u) | (y < ny - 1 ? 32u : 0u) | (z < nz - 1 ? 64u : 0u);
+  } else {
+    const int z = static_cast<int>(rest);
+    want = (z > 0 ? 1u : 0u) | (x > 0 ? 2u : 0u) | 4u | (x < nx - 1 ? 8u : 0u) |
+           (z < nz - 1 ? 16u : 0u);
+  }
+  if (pres[i] != want) atomicAdd(bad, 1);
+}
+
 __global__ void k_gather_codes(const unsigned char* __restrict__ codes, const int* __restrict__ rows,
                                long long nrows, int stride, unsigned char* __restrict__ out) {
   const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -512,6 +536,37 @@ bool build_dia_device(const int* row_ptr, const int* col_idx, const double* valu
     PPA_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof hbad, cudaMemcpyDeviceToHost, st));
     PPA_CUDA(cudaStreamSynchronize(st));
     if (hbad) out.pres.release();
+    // Box-grid geometry (spmv_grid2.cu): a 7-point stencil with offsets
+    // (-nx ny, -nx, -1, 0, 1, nx, nx ny) or a 5-point one with (-nx, -1, 0, 1,
+    // nx) whose entries are cut exactly at the box faces.
+    const std::vector<int>& o = out.offsets;
+    int gx = 0, gy = 0, gz = 0;
+    if (!hbad && nd == 7 && o[2] == -1 && o[3] == 0 && o[4] == 1 && o[1] == -o[5] &&
+        o[0] == -o[6] && o[5] > 1 && o[6] % o[5] == 0 && n % o[6] == 0) {
+      gx = o[5];
+      gy = o[6] / o[5];
+      gz = n / o[6];
+    } else if (!hbad && nd == 5 && o[1] == -1 && o[2] == 0 && o[3] == 1 && o[0] == -o[4] &&
+               o[4] > 1 && n % o[4] == 0) {
+      gx = o[4];
+      gy = 1;
+      gz = n / o[4];
+    }
+    if (gx > 0) {
+      PPA_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+      k_grid_check<<<blocks_for(n, 256), 256, 0, st>>>(out.pres.get() + out.pres_pad, n, nd, gx,
+                                                       gy, gz, bad.as<int>());
+      PPA_CUDA(cudaGetLastError());
+      int gbad = 0;
+      PPA_CUDA(cudaMemcpyAsync(&gbad, bad.p, sizeof gbad, cudaMemcpyDeviceToHost, st));
+      PPA_CUDA(cudaStreamSynchronize(st));
+      if (gbad == 0) {
+        grid2_zeros();
+        out.grid[0] = gx;
+        out.grid[1] = gy;
+        out.grid[2] = gz;
+      }
+    }
   }
   PPA_CUDA(cudaStreamSynchronize(st));
   return true;

@@ -507,6 +507,7 @@ int f2_dm(const CsrDevice& a) {
 bool dia2_supported(const CsrDevice& a) {
   const char* off = std::getenv("PPA_DISABLE_DIA2");
   if (off && off[0] == '1') return false;
+  if (grid2_supported(a)) return true;
   const int nd = a.dia_ndiag;
   // odd stencils with the centre (offset 0) in the middle: 3, 5 or 7 points
   if (!a.dia_pres || (nd != 3 && nd != 5 && nd != 7) || a.dia_off[(nd - 1) / 2] != 0) return false;
@@ -521,6 +522,8 @@ bool dia2_supported(const CsrDevice& a) {
 
 void spmv_dia2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y,
                const double* base, cudaStream_t st) {
+  // box-grid stencils take the boundary-free form (spmv_grid2.cu)
+  if (grid2_supported(a)) return spmv_grid2(a, p, x, y, base, st);
   const int ND = a.dia_ndiag;
   const int D = a.dia_off[ND - 1];
   const int dm = f2_dm(a);

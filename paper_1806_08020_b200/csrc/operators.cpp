@@ -186,6 +186,9 @@ bool CsrOperator::upload_dia(cudaStream_t st) {
     if (dia_.pres.get()) {
       dev_.dia_pres = dia_.pres.get() + dia_.pres_pad;
       dev_.dia_pres_pad = dia_.pres_pad;
+      dev_.grid_nx = dia_.grid[0];
+      dev_.grid_ny = dia_.grid[1];
+      dev_.grid_nz = dia_.grid[2];
     }
   }
   return true;

@@ -71,6 +71,11 @@ struct CsrDevice {
   // dia_pres is 16-byte aligned.
   const unsigned char* dia_pres = nullptr;
   long long dia_pres_pad = 0;
+  // Box-grid stencil (spmv_grid2.cu): the presence form is exactly a 7-point
+  // stencil on a grid_nx x grid_ny x grid_nz box (offsets -nx ny, -nx, -1, 0,
+  // 1, nx, nx ny) or a 5-point one on grid_nx x grid_nz (grid_ny = 1), cut at
+  // the box faces.  grid_nx = 0 otherwise.
+  int grid_nx = 0, grid_ny = 0, grid_nz = 0;
 };
 
 constexpr int kDiaMaxDiag = 32;
@@ -116,6 +121,16 @@ void spmv_mp2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y1,
 /// diagonal layout (spmv_dia2.cu): presence form, outer diagonals +-D, even n
 /// and D, in-plane offsets small against D.  PPA_DISABLE_DIA2=1 turns it off.
 bool dia2_supported(const CsrDevice& a);
+/// True when the box-grid form of the two-factor pass applies (spmv_grid2.cu:
+/// grid_nx > 0 and a launch plan exists).  PPA_DISABLE_GRID2=1 turns it off.
+bool grid2_supported(const CsrDevice& a);
+/// The per-device zero page the box-grid pass copies for planes outside the
+/// box (allocated on first use; layout_build.cu touches it so that a capture
+/// never allocates).
+const double* grid2_zeros();
+/// The box-grid two-factor pass (same contract as spmv_dia2).
+void spmv_grid2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y,
+                const double* base, cudaStream_t st);
 /// One two-factor pass (Mp2Pass semantics, y2 only; t / y1 never stored).
 /// x and y distinct and 16-byte aligned; `base` folds the complement.
 void spmv_dia2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y,
@@ -157,6 +172,7 @@ struct DevDia {
   long long nirr = 0;
   DBuffer<unsigned char> pres;  // presence form, pres_pad zero rows each side; may be empty
   long long pres_pad = 0;
+  int grid[3] = {0, 0, 0};  // box-grid stencil nx, ny, nz (0: not one; spmv_grid2.cu)
 };
 /// Diagonal-coded layout from the device CSR; false when the matrix has more
 /// than kDiaMaxDiag diagonals, more than kDiaMaxDict distinct values or a

@@ -226,3 +226,82 @@ def test_dia2_fuzz_bit_exact(cuda, seed):
     lay = ppa.make_csr_operator(P).layout()
     assert lay["layout"] == "dia_coded" and lay["two_factor_pass"], (n, offsets, lay)
     _check(cuda, P, Q, ROOTS[kind], complement, seed=seed)
+
+
+# ---- box-grid form (kernels/spmv_grid2.cu) --------------------------------
+def _box(nx, ny, nz, vals):
+    """7-point (ny > 1) or 5-point (ny == 1) stencil on an nx x ny x nz box,
+    cut at the faces, one value per diagonal (columns in increasing order)."""
+    if ny > 1:
+        offs = [(-1, 0, 0, 2), (0, -1, 0, 1), (0, 0, -1, 0), (0, 0, 0, None), (0, 0, 1, 0),
+                (0, 1, 0, 1), (1, 0, 0, 2)]
+    else:
+        offs = [(-1, 0, 0, 2), (0, 0, -1, 0), (0, 0, 0, None), (0, 0, 1, 0), (1, 0, 0, 2)]
+    z, y, x = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    z, y, x = z.ravel(), y.ravel(), x.ravel()
+    n = nx * ny * nz
+    cols, keeps = [], []
+    for dz, dy, dx, _ in offs:
+        zz, yy, xx = z + dz, y + dy, x + dx
+        keeps.append((zz >= 0) & (zz < nz) & (yy >= 0) & (yy < ny) & (xx >= 0) & (xx < nx))
+        cols.append((zz * ny + yy) * nx + xx)
+    C = np.stack(cols, axis=1)
+    K = np.stack(keeps, axis=1)
+    V = np.broadcast_to(np.asarray(vals, dtype=np.float64), C.shape)
+    rp = np.concatenate([[0], np.cumsum(K.sum(axis=1))]).astype(np.int32)
+    return n, rp, C[K].astype(np.int32), V[K].copy()
+
+
+BOXES = [
+    (160, 160, 6),     # config-3 planes, fewer planes than chunks
+    (30, 50, 20),      # lines shorter than a warp, odd tile splits
+    (200, 7, 30),      # few lines per plane
+    (8, 100, 50),      # one partial warp per line
+    (96, 96, 96),
+    (252, 40, 12),     # widest line the 3-D form takes
+    (1000, 1, 40),     # 2-D: several x tiles
+    (2048, 1, 64),
+    (64, 1, 700),      # 2-D, narrow lines, many chunks
+    (130, 1, 9),
+]
+
+
+@pytest.mark.parametrize("box", BOXES)
+@pytest.mark.parametrize("kind", ["real_even", "real_odd", "mixed", "pairs_only"])
+@pytest.mark.parametrize("complement", [False, True])
+def test_grid2_boxes_bit_exact(cuda, box, kind, complement):
+    nx, ny, nz = box
+    nd = 7 if ny > 1 else 5
+    vals = [float(v) for v in np.random.default_rng(nx * ny + nz).choice(
+        [-1.0, 2.5, -0.75, 4.0, 0.5, -3.0, 6.0], size=nd)]
+    n, rp, ci, vv = _box(nx, ny, nz, vals)
+    P = ppa.CsrMatrix.from_arrays(n, rp, ci, vv)
+    Q = O.Csr.from_arrays(n, rp, ci, vv)
+    lay = ppa.make_csr_operator(P).layout()
+    assert lay["grid"] == (nx, ny, nz) and lay["grid_pass"] and lay["two_factor_pass"], lay
+    _check(cuda, P, Q, ROOTS[kind], complement, seed=nx + nz)
+
+
+def test_grid2_configs_detected(cuda):
+    # configs 2, 3 and 5 are box grids; the reference's jump-coefficient
+    # convection-diffusion is not (two values on one diagonal)
+    for k, g in ((2, (1000, 1, 1000)), (3, (160, 160, 160)), (5, (2048, 1, 2048))):
+        lay = ppa.make_csr_operator(ppa.CsrMatrix.config(k)).layout()
+        assert lay["grid"] == g and lay["grid_pass"], (k, lay)
+    assert ppa.make_csr_operator(ppa.CsrMatrix.convection_diffusion(64)).layout()["grid"] is None
+
+
+def test_grid2_matches_presence_form(cuda, monkeypatch):
+    # the box-grid form and the presence-byte form of the pass agree bit for bit
+    P = ppa.CsrMatrix.laplacian_3d(48)
+    roots = ROOTS["mixed"]
+    x = dev(cuda, O.normal_vector(P.n, 5, 5))
+    outs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PPA_DISABLE_GRID2", flag)
+        A = ppa.make_csr_operator(P)
+        assert A.layout()["grid_pass"] == (flag == "0") and A.layout()["two_factor_pass"]
+        y = cuda.empty(P.n, dtype=cuda.float64, device="cuda")
+        ppa.apply_poly(roots, A, x, y)
+        outs.append(host(y))
+    assert np.array_equal(outs[0], outs[1])

@@ -64,4 +64,5 @@ for var in variants:
     r = subprocess.run([sys.executable, "-c", CHILD, cfg] + extra, env=env, capture_output=True,
                        text=True)
     line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-400:]
-    print(json.dumps({"variant": var or "default", "result": line}))
+    plans = [ln for ln in r.stderr.splitlines() if "plan" in ln]
+    print(json.dumps({"variant": var or "default", "result": line, "plans": plans}))
