@@ -48,9 +48,14 @@ def c3(cuda):
     return P, ppa.make_csr_operator(P)
 
 
-def test_c3_uses_sell_and_model_bytes(c3):
+def test_c3_model_bytes_and_default_layout(c3):
+    # the north-star byte model of one SpMV, and the layout make_csr_operator
+    # picks for config 3 (diagonal-coded, box-grid two-factor pass)
     P, A = c3
     assert A.model_bytes() == 12 * 28518400 + 4 * (4096000 + 1) + 16 * 4096000
+    lay = A.layout()
+    assert lay["layout"] == "dia_coded" and lay["grid"] == (160, 160, 160) and lay["grid_pass"]
+    assert ppa.make_csr_operator(P, "sell32").layout()["layout"] == "sell32"
 
 
 def test_c3_pi_av_bit_exact_full_size(cuda, c3):
@@ -146,17 +151,18 @@ def test_config_solve_vs_fixture(cuda, k):
         assert 0.1 < np.min(hist) / np.min(ghist) < 10.0
         return
     assert np.all(r["residuals"] <= r["rtol"])
-    assert abs(r["cost"]["mvps"] - g["cost"]["mvps"]) <= 0.05 * g["cost"]["mvps"]
+    if k != 5:
+        # config 5's matvec count moves with the summation order even between
+        # oracle variants (2 or 3 cycles); checked in test_nonnormal_vs_oracle_floor
+        assert abs(r["cost"]["mvps"] - g["cost"]["mvps"]) <= 0.05 * g["cost"]["mvps"]
     if k in (1, 2):
         # simple spectra: the GPU and oracle trajectories agree to roundoff
         # through the early cycles (~1e-13 observed in cycles 1-2)
         hist, ghist = r["cycle_max_residual"], np.array(g["cycle_max_residual"])
         assert np.allclose(hist[:3], ghist[:3], rtol=1e-8, atol=0)
     if k in (2, 5):
-        # Constant-Peclet convection-diffusion: the certified Ritz values lie in
-        # the pseudospectrum, where CPU and
-        # GPU roundoff select different, equally valid pairs (the polynomial
-        # was compared above).
+        # Constant-Peclet convection-diffusion: eigenvalues are compared against
+        # the oracle's own roundoff floor in test_nonnormal_vs_oracle_floor
         return
     got = np.sort_complex(r["eigenvalues"])
     ref = np.sort_complex(_c(g["eigenvalues"]))
@@ -190,3 +196,79 @@ def test_two_factor_pass_full_size_bit_exact(cuda, k):
         want = ref.apply(v)
         got = y.cpu().numpy()
         assert np.array_equal(got, want), np.linalg.norm(got - want) / np.linalg.norm(want)
+
+
+# ---- non-normal configs 2 and 5: parity against the oracle's roundoff floor
+def _convdiff_spectrum(N, pe=0.5, k=400):
+    """Closed form of the constant-Peclet operator."""
+    h = 1.0 / (N + 1)
+    j = np.arange(1, 60)
+    ax = (2 / h ** 2) * (1 - np.sqrt(1 - pe ** 2) * np.cos(j * np.pi * h))
+    ay = (2 / h ** 2) * (1 - np.cos(j * np.pi * h))
+    return np.sort((ax[:, None] + ay[None, :]).ravel())[:k]
+
+
+def _oracle_variants(k):
+    """Oracle solves of config k under three summation orders: the reference
+    (MGS2, sequential dots; c{k}_solve.json) and the two roundoff-floor probes
+    of roundoff_floor.json (classical CGS2 / MGS2 with blocked dots)."""
+    out = [_golden(f"c{k}_solve.json")]
+    fl = _golden("roundoff_floor.json")[f"config{k}"]
+    out += [fl["1"], fl["2"]]
+    return out
+
+
+def _nearest_rel(a, b):
+    b = np.asarray(b)
+    return np.array([np.min(np.abs(z - b)) / abs(z) for z in a])
+
+
+@pytest.mark.parametrize("k", [2, 5])
+def test_nonnormal_vs_oracle_floor(cuda, k):
+    """The certified Ritz values of configs 2 and 5 sit in the pseudospectrum
+    (cond of the symmetrising scaling ~3^((N-1)/2)), where the
+    summation order alone moves them.  The bar: the GPU's values lie within
+    the spread the oracle itself shows under equally valid summation orders
+    (its roundoff floor, measured and committed), every returned pair is
+    residual-certified by an independent host check, and the cycle count and
+    matvecs fall inside the oracle variants' range."""
+    vs = _oracle_variants(k)
+    evs = [_c(v["eigenvalues"]) for v in vs]
+    # the oracle's floor: worst nearest-value distance between any two variants
+    floor = max(np.max(_nearest_rel(evs[i], evs[j])) for i in range(3) for j in range(3)
+                if i != j)
+    A = ppa.make_csr_operator(ppa.CsrMatrix.config(k))
+    cfg = ppa.config_solve_config(k, want_eigenvectors=True)
+    r = ppa.solve_double(A, cfg) if k == 5 else ppa.solve(A, cfg)
+    assert r["converged"] and all(v["converged"] for v in vs)
+    cyc = [v["cycles"] for v in vs]
+    mv = [v["cost"]["mvps"] for v in vs]
+    assert min(cyc) <= r["cycles"] <= max(cyc), (r["cycles"], cyc)
+    assert 0.95 * min(mv) <= r["cost"]["mvps"] <= 1.05 * max(mv), (r["cost"]["mvps"], mv)
+    got = r["eigenvalues"]
+    union = np.concatenate(evs)
+    d = _nearest_rel(got, union)
+    print(f"config {k}: oracle floor {floor:.3e}, GPU-to-oracle max {d.max():.3e}")
+    assert d.max() <= floor, (d.max(), floor)
+    if k == 2:
+        # the floor is ~1e-5 here; the GPU sits inside it against every variant
+        for e in evs:
+            assert np.max(_nearest_rel(got, e)) <= floor
+    # independent residual certificate: ||A y - mu y|| on the host (oracle SpMV)
+    O.set_threads(os.cpu_count() or 1)
+    Q = O.csr_operator(O.Csr.config(k))
+    Y = r["eigenvectors"]
+    for j, mu in enumerate(got):
+        y = Y[:, j]
+        ay = Q.apply(y.real) + 1j * Q.apply(y.imag)
+        res = np.linalg.norm(ay - mu * y) / np.linalg.norm(y)
+        assert res <= r["rtol"] * (1 + 1e-6), (j, mu, res, r["rtol"])
+    # these are pseudo-eigenvalues: every certified value (GPU and oracle alike)
+    # lies far from the true spectrum, whose smallest member is ~10x larger
+    N = 1000 if k == 2 else 2048
+    lam = _convdiff_spectrum(N)
+    dg = _nearest_rel(got, lam)
+    do = _nearest_rel(evs[0], lam)
+    print(f"config {k}: distance to the closed-form spectrum GPU min {dg.min():.3f} "
+          f"oracle min {do.min():.3f} (lambda_min {lam[0]:.3f})")
+    assert dg.min() > 1.0 and do.min() > 1.0
