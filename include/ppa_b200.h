@@ -41,7 +41,8 @@ enum {
 
 /* OperatorKind (inc/operators.hpp:43) */
 enum { PPA_KIND_CSR = 0, PPA_KIND_DIAGONAL = 1, PPA_KIND_SHIFTED = 2, PPA_KIND_BLOCK2 = 3,
-       PPA_KIND_POLY = 4, PPA_KIND_COMPOSITE = 5 };
+       PPA_KIND_POLY = 4, PPA_KIND_COMPOSITE = 5,
+       PPA_KIND_EXTERNAL = 6 /* ours: ppa_op_create_callback */ };
 /* Orthogonalization of the device Arnoldi (ours).  The C++
    and Python SolveConfig default is PPA_ORTHO_DCGS2; a zero-filled
    ppa_solve_config is not a default configuration (m = 0 is invalid), use
@@ -107,6 +108,18 @@ int ppa_diagonal_operator(int n, const double* diag, ppa_op** out);
 /* make_poly_operator / make_poly_complement_operator (inc/gmres_poly.hpp:91,95) */
 int ppa_poly_operator(const ppa_op* base, const double* re, const double* im, int nroots,
                       int base_degree, int complement, ppa_op** out);
+/* A caller-defined operator: the reference's plugin mechanism, an abstract
+   LinearOperator (inc/operators.hpp:49-76) that arnoldi_extend, build_gmres_poly,
+   apply_poly and solve accept whatever its implementation.  apply(ctx, x_dev,
+   y_dev, stream) must enqueue y = Op x (device vectors of length dim) on
+   `stream` (a cudaStream_t: the library's current stream) and return 0; any
+   other value fails the calling entry point with PPA_RUNTIME_ERROR.  Every
+   apply charges mvps_per_apply matrix-vector products (mvps_per_apply(),
+   inc/operators.hpp:53); nnzr is reported by ppa_op_info.  ctx must outlive
+   the operator. */
+typedef int (*ppa_apply_fn)(void* ctx, const double* x_dev, double* y_dev, void* cuda_stream);
+int ppa_op_create_callback(int dim, int mvps_per_apply, double nnzr, ppa_apply_fn apply,
+                           void* ctx, ppa_op** out);
 void ppa_op_free(ppa_op* op);
 /* dim(), mvps_per_apply(), nnzr(), kind() (inc/operators.hpp:53-68) */
 int ppa_op_info(const ppa_op* op, int* dim, int* mvps_per_apply, double* nnzr, int* kind);
@@ -183,6 +196,21 @@ int ppa_arnoldi_ritz_vector(const ppa_arnoldi* st, int ordering, int j, double* 
                             double* y_im_dev, int* is_complex, ppa_cost* cost);
 /* thick_restart with ritz_pairs(ordering) as keep set (src/arnoldi.cpp:267-334) */
 int ppa_arnoldi_restart(ppa_arnoldi* st, int ordering, int k, ppa_cost* cost, int* kk);
+/* ritz_pairs (src/arnoldi.cpp:154-176) with the eigenvectors of H: pair i's
+   vector g_i (cur_dim entries) at vec_re/vec_im[i * cur_dim + r]; NULL skips */
+int ppa_arnoldi_ritz_vectors(const ppa_arnoldi* st, int ordering, double* re, double* im,
+                             double* resid, double* vec_re, double* vec_im);
+/* harmonic_restart_selection (inc/arnoldi.hpp:68-69; src/arnoldi.cpp:208-246),
+   same layout as ppa_arnoldi_ritz_vectors */
+int ppa_arnoldi_harmonic_selection(const ppa_arnoldi* st, int ordering, double* re, double* im,
+                                   double* resid, double* vec_re, double* vec_im);
+/* thick_restart(state, keep, k) (inc/arnoldi.hpp:79-80) with a caller-built
+   keep set: `count` values (re, im) and vectors g_i of H (vec layout as
+   above; im / vec_im may be NULL for real sets), taken in the given order,
+   conjugate pairs adjacent (+imag first) as ritz_pairs returns them */
+int ppa_arnoldi_restart_keep(ppa_arnoldi* st, int count, const double* re, const double* im,
+                             const double* vec_re, const double* vec_im, int k, ppa_cost* cost,
+                             int* kk);
 void ppa_arnoldi_free(ppa_arnoldi* st);
 
 /* ---- raw device kernels -------------------------------------------------- */

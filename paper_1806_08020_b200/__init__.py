@@ -44,6 +44,7 @@ from ._capi import (  # noqa: F401
     damping_heuristic,
     make_block2,
     make_shifted,
+    make_callback_operator,
     build_two_vector_poly,
     damped_start,
     read_matrix_market,

@@ -20,7 +20,10 @@ _LIB_PATH = os.path.join(_HERE, "libppa_b200.so")
 
 STREAM_NORM, STREAM_POLY, STREAM_ARNOLDI, STREAM_POLY2, STREAM_MATRIX = 1, 2, 3, 4, 5
 SMALLEST_MAGNITUDE, LARGEST_MAGNITUDE, TARGET_ONE = 0, 1, 2
-KINDS = ["csr", "diagonal", "shifted", "block2", "poly", "composite"]
+# int (*)(void* ctx, const double* x_dev, double* y_dev, void* cuda_stream)
+_APPLY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
+
+KINDS = ["csr", "diagonal", "shifted", "block2", "poly", "composite", "external"]
 
 
 class PPAError(RuntimeError):
@@ -127,6 +130,12 @@ def lib():
             "ppa_build_gmres_poly_ortho": [vp, vp, C.c_int, C.c_int, vp, vp, _ip, _ip,
                                            C.POINTER(CostRecord)],
             "ppa_solve_config_default": [vp],
+            "ppa_op_create_callback": [C.c_int, C.c_int, C.c_double, _APPLY_FN, vp,
+                                       C.POINTER(vp)],
+            "ppa_arnoldi_ritz_vectors": [vp, C.c_int, vp, vp, vp, vp, vp],
+            "ppa_arnoldi_harmonic_selection": [vp, C.c_int, vp, vp, vp, vp, vp],
+            "ppa_arnoldi_restart_keep": [vp, C.c_int, vp, vp, vp, vp, C.c_int,
+                                         C.POINTER(CostRecord), _ip],
             "ppa_leja_order": [vp, vp, C.c_int, vp, vp],
             "ppa_compute_pof": [vp, vp, C.c_int, vp, vp, _ip, _dp, _ip],
             "ppa_add_stability_roots": [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, _ip],
@@ -587,6 +596,41 @@ class ArnoldiState:
         _check(lib().ppa_arnoldi_ritz(self._h, ordering, _np_ptr(re), _np_ptr(im), _np_ptr(rs)))
         return re + 1j * im, rs
 
+    def ritz_pairs_vectors(self, ordering=SMALLEST_MAGNITUDE):
+        """ritz_pairs with the eigenvectors of H: (values, residuals, G) with
+        G[:, i] the vector of pair i (ppa_arnoldi_ritz_vectors)."""
+        d = self.cur_dim
+        re, im, rs = np.zeros(d), np.zeros(d), np.zeros(d)
+        vr, vi = np.zeros((d, d)), np.zeros((d, d))
+        _check(lib().ppa_arnoldi_ritz_vectors(self._h, ordering, _np_ptr(re), _np_ptr(im),
+                                              _np_ptr(rs), _np_ptr(vr), _np_ptr(vi)))
+        return re + 1j * im, rs, (vr + 1j * vi).T.copy()
+
+    def harmonic_restart_selection(self, ordering=SMALLEST_MAGNITUDE):
+        """harmonic_restart_selection (inc/arnoldi.hpp:68-69): (values,
+        residuals, G) as ritz_pairs_vectors."""
+        d = self.cur_dim
+        re, im, rs = np.zeros(d), np.zeros(d), np.zeros(d)
+        vr, vi = np.zeros((d, d)), np.zeros((d, d))
+        _check(lib().ppa_arnoldi_harmonic_selection(self._h, ordering, _np_ptr(re), _np_ptr(im),
+                                                    _np_ptr(rs), _np_ptr(vr), _np_ptr(vi)))
+        return re + 1j * im, rs, (vr + 1j * vi).T.copy()
+
+    def thick_restart_keep(self, values, G, k: int, rec=None) -> int:
+        """thick_restart(state, keep, k) (inc/arnoldi.hpp:79-80) with a
+        caller-built keep set: values[i] and H-eigenvector G[:, i]."""
+        rec = rec if rec is not None else CostRecord()
+        vals = np.asarray(values, dtype=np.complex128)
+        G = np.asarray(G, dtype=np.complex128)
+        re, im = np.ascontiguousarray(vals.real), np.ascontiguousarray(vals.imag)
+        vr = np.ascontiguousarray(G.real.T)
+        vi = np.ascontiguousarray(G.imag.T)
+        kk = C.c_int()
+        _check(lib().ppa_arnoldi_restart_keep(self._h, len(vals), _np_ptr(re), _np_ptr(im),
+                                              _np_ptr(vr), _np_ptr(vi), k, C.byref(rec),
+                                              C.byref(kk)))
+        return kk.value
+
     def harmonic_ritz_values(self):
         d = self.cur_dim
         re, im = np.zeros(d), np.zeros(d)
@@ -736,6 +780,31 @@ def damping_heuristic(a: LinearOperator, cfg: SolveConfig, rec: Optional[CostRec
     _check(lib().ppa_damping_heuristic(a._h, C.byref(c), _np_ptr(re), _np_ptr(im), cap,
                                        C.byref(nr), C.byref(rec)))
     return re[:nr.value] + 1j * im[:nr.value]
+
+
+def make_callback_operator(dim: int, apply, mvps_per_apply: int = 1,
+                           nnzr: float = 0.0) -> LinearOperator:
+    """A caller-defined device operator (ppa_op_create_callback): the
+    reference's LinearOperator plugin point (inc/operators.hpp:49-76).
+    ``apply(x_ptr, y_ptr, stream_ptr)`` must enqueue y = Op x on the CUDA
+    stream ``stream_ptr`` for device vectors of length ``dim`` and return 0
+    (or None); an exception or nonzero return fails the calling entry point."""
+
+    def tramp(ctx, x, y, stream):
+        try:
+            rc = apply(x or 0, y or 0, stream or 0)
+            return 0 if rc is None else int(rc)
+        except Exception:  # noqa: BLE001  (reported as PPA_RUNTIME_ERROR)
+            import traceback
+
+            traceback.print_exc()
+            return -1
+
+    fn = _APPLY_FN(tramp)
+    h = C.c_void_p()
+    _check(lib().ppa_op_create_callback(dim, mvps_per_apply, C.c_double(nnzr), fn, None,
+                                        C.byref(h)))
+    return LinearOperator(h, keep=(fn, apply))
 
 
 def make_block2(a: LinearOperator) -> LinearOperator:

@@ -316,6 +316,19 @@ int ppa_poly_operator(const ppa_op* base, const double* re, const double* im, in
   });
 }
 
+int ppa_op_create_callback(int dim, int mvps_per_apply, double nnzr, ppa_apply_fn apply,
+                           void* ctx, ppa_op** out) {
+  return guard([&] {
+    need(out, "ppa_op_create_callback");
+    if (!apply) throw std::invalid_argument("make_callback_operator: null apply");
+    *out = wrap_op(ppa::make_callback_operator(
+        dim, mvps_per_apply, nnzr,
+        [apply, ctx](const double* x, double* y, cudaStream_t s) {
+          return apply(ctx, x, y, static_cast<void*>(s));
+        }));
+  });
+}
+
 void ppa_op_free(ppa_op* op) { delete op; }
 
 int ppa_op_info(const ppa_op* op, int* dim, int* mvps, double* nnzr, int* kind) {
@@ -653,6 +666,67 @@ int ppa_arnoldi_ritz_vector(const ppa_arnoldi* st, int ordering, int j, double* 
     if (y.complex && yi) ppa::kern::copy(y.im.get(), yi, st->s.n, str);
     ppa::current_context().sync();
     if (is_complex) *is_complex = y.complex ? 1 : 0;
+    add_cost(cost, r);
+  });
+}
+
+namespace {
+void ritz_out(const ppa::RitzSet& s, double* re, double* im, double* resid, double* vre,
+              double* vim) {
+  const int d = s.vectors_h.rows;
+  for (int i = 0; i < s.count(); ++i) {
+    if (re) re[i] = s.values[i].real();
+    if (im) im[i] = s.values[i].imag();
+    if (resid) resid[i] = s.residuals[i];
+    for (int r = 0; r < d; ++r) {
+      if (vre) vre[static_cast<size_t>(i) * d + r] = s.vectors_h(r, i).real();
+      if (vim) vim[static_cast<size_t>(i) * d + r] = s.vectors_h(r, i).imag();
+    }
+  }
+}
+}  // namespace
+
+int ppa_arnoldi_ritz_vectors(const ppa_arnoldi* st, int ordering, double* re, double* im,
+                             double* resid, double* vec_re, double* vec_im) {
+  return guard([&] {
+    need(st, "ppa_arnoldi_ritz_vectors");
+    ritz_out(ppa::ritz_pairs(st->s, static_cast<ppa::RitzOrdering>(ordering)), re, im, resid,
+             vec_re, vec_im);
+  });
+}
+
+int ppa_arnoldi_harmonic_selection(const ppa_arnoldi* st, int ordering, double* re, double* im,
+                                   double* resid, double* vec_re, double* vec_im) {
+  return guard([&] {
+    need(st, "ppa_arnoldi_harmonic_selection");
+    ritz_out(ppa::harmonic_restart_selection(st->s, static_cast<ppa::RitzOrdering>(ordering)),
+             re, im, resid, vec_re, vec_im);
+  });
+}
+
+int ppa_arnoldi_restart_keep(ppa_arnoldi* st, int count, const double* re, const double* im,
+                             const double* vec_re, const double* vec_im, int k, ppa_cost* cost,
+                             int* kk) {
+  return guard([&] {
+    need(st, "ppa_arnoldi_restart_keep");
+    need(re, "ppa_arnoldi_restart_keep");
+    need(vec_re, "ppa_arnoldi_restart_keep");
+    if (count < 0) throw std::invalid_argument("thick_restart: selection smaller than k");
+    const int d = st->s.cur_dim;
+    ppa::RitzSet s;
+    s.values.resize(count);
+    s.residuals.assign(count, 0.0);
+    s.vectors_h = ppa::dense::CMat(d, count);
+    for (int i = 0; i < count; ++i) {
+      s.values[i] = {re[i], im ? im[i] : 0.0};
+      for (int r = 0; r < d; ++r) {
+        const size_t at = static_cast<size_t>(i) * d + r;
+        s.vectors_h(r, i) = {vec_re[at], vec_im ? vec_im[at] : 0.0};
+      }
+    }
+    ppa::CostRecord r;
+    const int got = ppa::thick_restart(st->s, s, k, r);
+    if (kk) *kk = got;
     add_cost(cost, r);
   });
 }

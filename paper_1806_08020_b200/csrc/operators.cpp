@@ -327,6 +327,33 @@ class ShiftedOperator final : public LinearOperator {
   double mu_;
 };
 
+class CallbackOperator final : public LinearOperator {
+ public:
+  CallbackOperator(int n, int mvps, double nnzr, DeviceApplyFn fn)
+      : n_(n), mvps_(mvps), nnzr_(nnzr), fn_(std::move(fn)) {
+    if (n_ < 1) throw std::invalid_argument("make_callback_operator: dim < 1");
+    if (mvps_ < 0) throw std::invalid_argument("make_callback_operator: mvps_per_apply < 0");
+    if (!fn_) throw std::invalid_argument("make_callback_operator: null apply");
+  }
+  int dim() const override { return n_; }
+  OperatorKind kind() const override { return OperatorKind::external; }
+  int mvps_per_apply() const override { return mvps_; }
+  double nnzr() const override { return nnzr_; }
+  void apply(const double* x, double* y, CostRecord& rec) const override {
+    if (x == nullptr || y == nullptr) throw std::invalid_argument("apply: dimension mismatch");
+    const int rc = fn_(x, y, current_context().stream());
+    if (rc != 0) {
+      throw std::runtime_error("callback operator: apply returned " + std::to_string(rc));
+    }
+    rec.mvps += mvps_;
+  }
+
+ private:
+  int n_, mvps_;
+  double nnzr_;
+  DeviceApplyFn fn_;
+};
+
 std::string lower(std::string s) {
   std::transform(s.begin(), s.end(), s.begin(), [](unsigned char c) { return std::tolower(c); });
   return s;
@@ -338,6 +365,10 @@ OperatorPtr make_block2(OperatorPtr a) { return std::make_shared<Block2Operator>
 
 OperatorPtr make_shifted(OperatorPtr a, double mu) {
   return std::make_shared<ShiftedOperator>(std::move(a), mu);
+}
+
+OperatorPtr make_callback_operator(int dim, int mvps_per_apply, double nnzr, DeviceApplyFn apply) {
+  return std::make_shared<CallbackOperator>(dim, mvps_per_apply, nnzr, std::move(apply));
 }
 
 CsrMatrix read_matrix_market(const std::string& path) {

@@ -6,6 +6,7 @@
 // §8b "Constraint": host vectors would force a 32 MB H2D/D2H per apply).
 
 #include <complex>
+#include <functional>
 #include <memory>
 #include <string>
 #include <tuple>
@@ -53,7 +54,7 @@ struct SpectrumSpec {
   bool real_only(double tol = 0.0) const;
 };
 
-enum class OperatorKind { csr, diagonal, shifted, block2, poly, composite };
+enum class OperatorKind { csr, diagonal, shifted, block2, poly, composite, external };
 
 /// A counted action v -> Op v on device vectors (inc/operators.hpp:49-76).
 /// Kernels run on the calling thread's current context stream.
@@ -138,6 +139,16 @@ OperatorPtr make_diagonal(std::vector<double> diag_values);
 OperatorPtr make_block2(OperatorPtr a);
 /// v -> Av - mu v (src/operators.cpp:152-170).
 OperatorPtr make_shifted(OperatorPtr a, double mu);
+
+/// A caller-defined device operator: the reference's plugin mechanism (any
+/// LinearOperator subclass is accepted by arnoldi_extend, build_gmres_poly
+/// and solve; inc/operators.hpp:49-76) for code outside this library, e.g. a
+/// matrix-free stencil.  `apply(x, y, stream)` must write y = Op x for device
+/// vectors of length dim on `stream` (the calling thread's context stream)
+/// and return 0; a nonzero return becomes std::runtime_error.  Each apply
+/// charges mvps_per_apply base applications (kind() = external, ours).
+using DeviceApplyFn = std::function<int(const double* x, double* y, cudaStream_t stream)>;
+OperatorPtr make_callback_operator(int dim, int mvps_per_apply, double nnzr, DeviceApplyFn apply);
 
 /// Strict Matrix Market coordinate reader, real general/symmetric
 /// (src/operators.cpp:246-305); symmetric storage is expanded.
