@@ -201,9 +201,8 @@ namespace {
 // Fused chain for a CSR base operator.  The factors are grouped into passes:
 //   single real root : one SpMV launch, y = x + c0 (A x)
 //   conjugate pair   : t1 = A x, then y = (x + c1 t1) + c0 (A t1)
-//   two real roots   : when the matrix qualifies (banded SELL-32), one
-//                      matrix-powers launch applies both (kernels/mpk.cu)
-// A pair also runs as one matrix-powers launch when the matrix qualifies.
+//   two real roots   : on stencils, one temporally blocked pass applies both
+//                      (kernels/spmv_grid2.cu, spmv_dia2.cu); a pair too
 // Every pass maps the current vector to a new buffer; buffers are assigned
 // backwards from the end so the last pass writes `dst` directly, and
 // `complement_base`, when set, is folded into that last pass (tau = I - pi,
@@ -233,18 +232,13 @@ void apply_poly_csr(const std::vector<PolyFactor>& plan, const CsrOperator& a, c
     }
     return;
   }
-  // Matrix-powers fusion is opt-in: it is bit-exact and halves HBM traffic
-  // (L2 reuse), but its cross-CTA waits make it slower than two plain
-  // launches on B200.
-  const char* mpk_env = std::getenv("PPA_ENABLE_MPK");
-  const bool mp = mpk_env && mpk_env[0] == '1' && kern::mp2_supported(a.device()) && !outer_fold;
   std::optional<Scratch> s_other, s_t1;
   double* other = cb ? cb->other : (s_other.emplace(static_cast<size_t>(n)), s_other->get());
   // Temporal blocking over stencils (kernels/spmv_dia2.cu): two real roots or
   // one pair per pass, x read once.  Its bulk copies need 16-byte aligned
   // sources (the chain's inputs: v and the ping-pong pair).
   auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
-  const bool d2 = !mp && kern::dia2_supported(a.device()) && aligned(v) && aligned(dst) &&
+  const bool d2 = kern::dia2_supported(a.device()) && aligned(v) && aligned(dst) &&
                   aligned(other);
   struct Pass {
     int first;
@@ -257,7 +251,7 @@ void apply_poly_csr(const std::vector<PolyFactor>& plan, const CsrOperator& a, c
       passes.push_back({k, 1});
       any_two = true;
       k += 1;
-    } else if ((mp || d2) && k + 1 < K && !plan[k + 1].pair) {
+    } else if (d2 && k + 1 < K && !plan[k + 1].pair) {
       passes.push_back({k, 2});
       any_two = true;
       k += 2;
@@ -293,17 +287,6 @@ void apply_poly_csr(const std::vector<PolyFactor>& plan, const CsrOperator& a, c
         m.b0 = plan[ps.first + 1].c0;
       }
       kern::spmv_dia2(a.device(), m, cur, out, base, st);
-    } else if (ps.count == 2 || (f.pair && mp)) {
-      kern::Mp2Pass m;
-      m.pair = f.pair;
-      if (f.pair) {
-        m.a0 = f.c0;
-        m.a1 = f.c1;
-      } else {
-        m.a0 = f.c0;
-        m.b0 = plan[ps.first + 1].c0;
-      }
-      kern::spmv_mp2(a.device(), m, cur, t1p, out, base, ctx.mp_work(), ctx.sm_count(), st);
     } else {
       kern::EpiArgs ep;
       ep.base = base;
@@ -572,9 +555,7 @@ class PolyOperator final : public LinearOperator {
     if (complement_) return nullptr;
     const auto* tau = dynamic_cast<const PolyOperator*>(a_.get());
     const auto* base_csr = tau ? dynamic_cast<const CsrOperator*>(tau->a_.get()) : nullptr;
-    const char* mpk_env = std::getenv("PPA_ENABLE_MPK");
-    if (tau && tau->complement_ && base_csr && !tau->plan_.empty() &&
-        !(mpk_env && mpk_env[0] == '1')) {
+    if (tau && tau->complement_ && base_csr && !tau->plan_.empty()) {
       return tau;
     }
     return nullptr;

@@ -329,22 +329,17 @@ struct F2Plan {
   size_t smem = 0;
 };
 
+// Per-device queries (a process may drive several GPUs): not cached.
 int f2_sms() {
-  static const int sms = [] {
-    int dev = 0, v = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
-      v = 148;
-    }
-    return v;
-  }();
-  return sms;
+  int dev = 0, v = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    v = 148;
+  }
+  return v;
 }
 
-int f2_smem_limit() {
-  static const int lim = max_dynamic_smem(k_spmv_dia2<7, true, 2, true, true>);
-  return lim;
-}
+int f2_smem_limit() { return max_dynamic_smem(k_spmv_dia2<7, true, 2, true, true>); }
 
 size_t f2_smem_bytes(int e1, int dm) {
   return sizeof(double) * (static_cast<size_t>(F2_XS) +
@@ -391,6 +386,10 @@ F2Plan f2_plan_search(int n, int D, int Dm) {
       const int slots = sms * cps;
       const int ntmin = ntmin_env ? ntmin_env : relax ? 128 : (768 + cps - 1) / cps;
       for (int kc = 2; kc <= 4; ++kc) {
+        // two CTAs per SM only where the register budget of
+        // __launch_bounds__(f2_max_nt(KC), 1) leaves room for both (KC = 2:
+        // 64 registers at up to 1024 threads; KC = 3 / 4 allow ~85 / 128)
+        if (cps > 1 && kc > 2) continue;
         for (int nt = 128; nt <= std::min(ntmax, f2_max_nt(kc)); nt += 32) {
           if (nt < ntmin || nt * cps > 2048) continue;
           const int cap = nt * kc - 2 * Dm;
@@ -433,18 +432,20 @@ F2Plan f2_plan_search(int n, int D, int Dm) {
 // (PPA_DIA2_*) apply to geometries planned after they are set.
 F2Plan f2_plan(int n, int D, int Dm) {
   struct Entry {
-    int n, D, Dm;
+    int dev, n, D, Dm;
     F2Plan plan;
   };
   static std::mutex mu;
   static std::vector<Entry> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(mu);
   for (const Entry& e : cache) {
-    if (e.n == n && e.D == D && e.Dm == Dm) return e.plan;
+    if (e.dev == dev && e.n == n && e.D == D && e.Dm == Dm) return e.plan;
   }
   const F2Plan plan = f2_plan_search(n, D, Dm);
   if (cache.size() >= 64) cache.erase(cache.begin());
-  cache.push_back({n, D, Dm, plan});
+  cache.push_back({dev, n, D, Dm, plan});
   return plan;
 }
 
@@ -452,12 +453,10 @@ template <int ND, bool UNIT, int KC, bool PAIR, bool COMPL>
 void launch_f2(const CsrDevice& a, const F2Params& P, const F2Plan& pl, const double* x,
                double* y, const double* base, cudaStream_t st) {
   auto kernel = k_spmv_dia2<ND, UNIT, KC, PAIR, COMPL>;
-  static const bool attr = [kernel] {
-    PPA_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  max_dynamic_smem(kernel)));
-    return true;
-  }();
-  (void)attr;
+  // the attribute is per device: set on every launch (a cheap host call)
+  // rather than once per process
+  PPA_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(pl.smem)));
   launch_pdl(kernel, dim3(pl.ntiles * pl.nchunks), dim3(pl.nt), pl.smem, st, a.dia_pres, x, y,
              base, P);
 }

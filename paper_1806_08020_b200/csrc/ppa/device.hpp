@@ -71,15 +71,6 @@ struct ReduceWorkspace {
   int max_width = 0;
 };
 
-/// Per-chunk release flags and the work ticket of the matrix-powers kernel
-/// (kernels/mpk.cu); epochs make the flags reusable without resets.
-struct MpWork {
-  DBuffer<int> flags;
-  DBuffer<unsigned int> counter;
-  int capacity = 0;
-  int epoch = 0;
-};
-
 /// Execution context: the stream every kernel of one solver run is
 /// launched on plus its reduction workspace.  One solve is single-threaded
 /// (SPEC.md concurrency model), so a context is owned by one thread.
@@ -136,10 +127,8 @@ class Context {
   double* pinned_aux_ = nullptr;
   size_t pinned_aux_count_ = 0;
   DBuffer<double> results_;
-  MpWork mp_;
 
  public:
-  MpWork& mp_work() { return mp_; }
 };
 
 /// The calling thread's current context (created on first use, default

@@ -102,20 +102,15 @@ bool build_sell32_packed(const int* row_ptr, const int* col_idx, const double* v
 /// Bytes the packed stream occupies (cols + codes/values) per entry.
 inline double packed_entry_bytes(int ndict) { return 2.0 + (ndict > 0 ? 1.0 : 8.0); }
 
-/// Two polynomial factors fused into one matrix-powers pass (mpk.cu):
+/// Two polynomial factors applied in one temporally blocked pass
+/// (spmv_dia2.cu, spmv_grid2.cu):
 ///   pair = false: y1 = x + a0 (A x),  y2 = y1 + b0 (A y1)   (two real roots)
-///   pair = true : t = A x (into y1),  y2 = (x + a1 t) + a0 (A t)  (conjugate pair)
+///   pair = true : t = A x,            y2 = (x + a1 t) + a0 (A t)  (conjugate pair)
+/// Only y2 is stored.
 struct Mp2Pass {
   bool pair = false;
   double a0 = 0.0, a1 = 0.0, b0 = 0.0;
 };
-
-/// True when the fused two-level kernel applies: SELL-32 without row
-/// permutation and a bandwidth small against n.
-bool mp2_supported(const CsrDevice& a);
-/// One fused pass; x, y1, y2 distinct; `base` folds the complement into y2.
-void spmv_mp2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y1, double* y2,
-              const double* base, MpWork& w, int sm_count, cudaStream_t st);
 
 /// True when two factors can run as one temporally blocked pass over the
 /// diagonal layout (spmv_dia2.cu): presence form, outer diagonals +-D, even n

@@ -346,12 +346,10 @@ def test_apply_poly_bit_exact(cuda, kind):
 
 @pytest.mark.parametrize("kind", ["real_even", "real_odd", "mixed", "pairs_only"])
 @pytest.mark.parametrize("complement", [False, True])
-@pytest.mark.parametrize("mpk", ["1", "0"])
-def test_matrix_powers_fused_bit_exact(cuda, monkeypatch, kind, complement, mpk):
-    # n >= 65536 and small bandwidth: with PPA_ENABLE_MPK=1 consecutive factors
-    # run as fused two-level matrix-powers passes (kernels/mpk.cu); fused and
-    # plain chains must both equal the oracle bit for bit
-    monkeypatch.setenv("PPA_ENABLE_MPK", mpk)
+def test_large_chains_bit_exact(cuda, kind, complement):
+    # n >= 65536 chains (two-factor passes on the stencils, the generic
+    # pair path on the reference's jump-coefficient matrix) equal the oracle
+    # bit for bit, and repeated applies stay exact
     gens = {"real_even": lambda M: M.laplacian_3d(48), "real_odd": lambda M: M.laplacian_3d(48),
             "mixed": lambda M: M.convection_diffusion(300),
             "pairs_only": lambda M: M.convection_diffusion_const(260, 0.5)}
@@ -371,7 +369,6 @@ def test_matrix_powers_fused_bit_exact(cuda, monkeypatch, kind, complement, mpk)
     ref = opo.apply(x, cost)
     assert np.array_equal(host(y), ref), rel(host(y), ref)
     assert (rec.mvps, rec.vops) == (int(cost[0]), int(cost[2]))
-    # repeated applies reuse the per-context flags (epochs): still exact
     op.apply(dev(cuda, x), y)
     assert np.array_equal(host(y), ref)
 
