@@ -378,7 +378,15 @@ def run_b200(args):
     two = bool(lay.get("two_factor_pass"))
     auto_launches = count_launches(roots, two)
     auto_launch_s = ms_auto * 1e-3 / auto_launches
-    if two:
+    if two and lay.get("grid_pass"):
+        # box-grid two-factor pass: x read once (8n), the second factor's y
+        # written once (8n); no matrix bytes at all
+        kbytes = 16.0 * n
+        kname = ("k_spmv_grid2 (two factors per pass over the box-grid stencil: x planes by "
+                 "cp.async.bulk into a shared-memory ring, per-warp mbarrier split barriers)")
+        note = ("8n x + 8n y per two-factor launch; bound by the FP64 pipe and issue "
+                "(16 DP ops per row per factor, bit-exact mul-then-add order), not by HBM")
+    elif two:
         # two factors per launch: x read once (8n), the second factor's y
         # written once (8n), one presence byte per row (n)
         kbytes = 17.0 * n
