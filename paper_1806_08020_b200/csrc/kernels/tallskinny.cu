@@ -183,15 +183,16 @@ __global__ void k_fill(double* x, double v, long long n) {
 
 inline int ew_grid(long long n) { return std::max(1, std::min(ceil_div(n, 256), 148 * 16)); }
 
-// Out[:,0:p] = V[:,0:d] * G.  One row per thread with its p accumulators in
-// registers: the row's d values are streamed once (8 columns of loads in
-// flight) and G comes from shared memory, row-major with an even row
-// length, two columns per broadcast 16-byte read.  A row's outputs are
+// Out[:,0:p] = V[:,0:d] * G.  RB rows per thread (rows r and r + CB of the
+// CTA's 2 CB-row block when RB = 2) with their p accumulators in registers:
+// each row's d values are streamed once (JU columns of loads in flight per
+// row), G comes from shared memory, row-major with an even row length, two
+// columns per broadcast 16-byte read that serves all RB rows (RB = 2 halves
+// the shared-memory wavefronts per FMA, which bounded the one-row kernel:
+// 0.63 ms for d = 40, p = 20 in place on config 3).  A row's outputs are
 // written only after all of its d inputs were read, by the same thread, so
-// Out may alias V (the in-place thick restart, p <= d).  Per output: fma over
-// j = 0..d-1 in order (the same arithmetic as the row-staged kernel it
-// replaces, which was shared-memory-bound: 0.54 ms for d = 40, p = 20 on
-// config 3).
+// Out may alias V (the in-place thick restart, p <= d).  Per output: fma
+// over j = 0..d-1 in order.
 constexpr int CB = 256;  // threads per CTA
 
 template <int PB>
@@ -240,16 +241,98 @@ __global__ void __launch_bounds__(CB) k_ts_combine(const double* V, long long ld
   }
 }
 
+// Two rows per thread (the RB = 2 form described above).
+
+template <int PB, int RB>
+__global__ void __launch_bounds__(CB, RB) k_ts_combine_rb(const double* V, long long ldv, int n, int d,
+                                                   const double* __restrict__ G, int p,
+                                                   double* Out, long long ldo) {
+  static_assert(PB % 2 == 0, "column pairs");
+  extern __shared__ double2 gs2[];  // G row-major: row j = columns 0..PB-1 (zero-padded)
+  double* gs = reinterpret_cast<double*>(gs2);
+  for (int k = threadIdx.x; k < d * PB; k += CB) {
+    const int j = k / PB, c = k - j * PB;
+    gs[k] = c < p ? G[static_cast<long long>(c) * d + j] : 0.0;
+  }
+  __syncthreads();
+  long long row[RB];
+  bool live[RB];
+#pragma unroll
+  for (int r = 0; r < RB; ++r) {
+    const long long i = static_cast<long long>(blockIdx.x) * (CB * RB) + r * CB + threadIdx.x;
+    live[r] = i < n;
+    row[r] = live[r] ? i : n - 1;  // clamped loads, no store
+  }
+  double acc[RB][PB];
+#pragma unroll
+  for (int r = 0; r < RB; ++r)
+#pragma unroll
+    for (int c = 0; c < PB; ++c) acc[r][c] = 0.0;
+  // columns p..PB-1 of G are zero in shared memory: no per-column test
+  auto step = [&](const double (&v)[RB], const double2* g) {
+#pragma unroll
+    for (int c = 0; c < PB / 2; ++c) {
+      const double2 gv = g[c];
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        acc[r][2 * c] = fma(v[r], gv.x, acc[r][2 * c]);
+        acc[r][2 * c + 1] = fma(v[r], gv.y, acc[r][2 * c + 1]);
+      }
+    }
+  };
+  constexpr int JU = RB == 1 ? 8 : 2;
+  int j0 = 0;
+  for (; j0 + JU <= d; j0 += JU) {
+    double v[JU][RB];
+#pragma unroll
+    for (int jj = 0; jj < JU; ++jj)
+#pragma unroll
+      for (int r = 0; r < RB; ++r) v[jj][r] = V[row[r] + static_cast<long long>(j0 + jj) * ldv];
+    const double2* g = gs2 + j0 * (PB / 2);
+#pragma unroll
+    for (int jj = 0; jj < JU; ++jj) step(v[jj], g + jj * (PB / 2));
+  }
+  for (; j0 < d; ++j0) {
+    double v[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) v[r] = V[row[r] + static_cast<long long>(j0) * ldv];
+    step(v, gs2 + j0 * (PB / 2));
+  }
+#pragma unroll
+  for (int r = 0; r < RB; ++r) {
+    if (!live[r]) continue;
+#pragma unroll
+    for (int c = 0; c < PB; ++c) {
+      if (c < p) Out[row[r] + static_cast<long long>(c) * ldo] = acc[r][c];
+    }
+  }
+}
+
 template <int PB>
 void launch_combine(const double* V, long long ldv, int n, int d, const double* G, int p,
                     double* Out, long long ldo, size_t smem, cudaStream_t st) {
-  static const bool capped = [] {  // once per instantiation, thread-safe
-    PPA_CUDA(cudaFuncSetAttribute(k_ts_combine<PB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  max_dynamic_smem(k_ts_combine<PB>)));
-    return true;
-  }();
-  (void)capped;
-  k_ts_combine<PB><<<ceil_div(n, CB), CB, smem, st>>>(V, ldv, n, d, G, p, Out, ldo);
+  // two rows per thread at PB = 20 (the k = 20 restarts of configs 2 and 3):
+  // measured 0.55 ms vs 0.63 ms for d = 40 in place; for other widths the
+  // one-row kernel keeps more warps resident and is faster
+  // (tools/combine_bench.py)
+  if constexpr (PB == 20) {
+    static const bool capped = [] {
+      PPA_CUDA(cudaFuncSetAttribute(k_ts_combine_rb<PB, 2>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    max_dynamic_smem(k_ts_combine_rb<PB, 2>)));
+      return true;
+    }();
+    (void)capped;
+    k_ts_combine_rb<PB, 2><<<ceil_div(n, CB * 2), CB, smem, st>>>(V, ldv, n, d, G, p, Out, ldo);
+  } else {
+    static const bool capped = [] {  // once per instantiation, thread-safe
+      PPA_CUDA(cudaFuncSetAttribute(k_ts_combine<PB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    max_dynamic_smem(k_ts_combine<PB>)));
+      return true;
+    }();
+    (void)capped;
+    k_ts_combine<PB><<<ceil_div(n, CB), CB, smem, st>>>(V, ldv, n, d, G, p, Out, ldo);
+  }
 }
 
 }  // namespace
