@@ -234,6 +234,19 @@ int ppa_spmm(const ppa_op* a, const double* Y_dev, long long ldy, int p, double*
 /* One CGS2 step (replaces MGS2 of src/arnoldi.cpp:129-150); Hcol_dev c+1, flag_dev int */
 int ppa_cgs2_step(double* V_dev, long long ld, int n, int c, double* w_dev, double* Hcol_dev,
                   int* flag_dev);
+/* Row-sharded CGS2 building blocks (the three sweeps of ppa_cgs2_step with
+   rank-local sums, for a c-wide all-reduce between sweeps; dist.py
+   ShardedSolver over NCCL): out = V[:,0:c]^T w (c values);
+   w -= V h then out = [V^T w, ||w||^2] (c + 1 values);
+   V[:,c] = (w - V h2) / *hsub.  All pointers device, results deterministic. */
+int ppa_cgs_dot_local(const double* V_dev, long long ld, int n, int c, const double* w_dev,
+                      double* out_dev);
+int ppa_cgs_update_dot_local(const double* V_dev, long long ld, int n, int c, double* w_dev,
+                             const double* h_dev, double* out_dev);
+int ppa_cgs_store_local(double* V_dev, long long ld, int n, int c, const double* w_dev,
+                        const double* h2_dev, const double* hsub_dev);
+/* out_dev[0] = x . y, deterministic (dot, inc/cost.hpp:51-57) */
+int ppa_dot_local(const double* x_dev, const double* y_dev, long long n, double* out_dev);
 /* Out = V[:,0:d] G (G d x p col-major, device); in place allowed for p <= d
    (src/arnoldi.cpp:258, 309) */
 int ppa_ts_combine(const double* V_dev, long long ldv, int n, int d, const double* G_dev, int p,

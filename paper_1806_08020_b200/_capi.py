@@ -130,6 +130,10 @@ def lib():
             "ppa_build_gmres_poly_ortho": [vp, vp, C.c_int, C.c_int, vp, vp, _ip, _ip,
                                            C.POINTER(CostRecord)],
             "ppa_solve_config_default": [vp],
+            "ppa_cgs_dot_local": [vp, C.c_longlong, C.c_int, C.c_int, vp, vp],
+            "ppa_cgs_update_dot_local": [vp, C.c_longlong, C.c_int, C.c_int, vp, vp, vp],
+            "ppa_cgs_store_local": [vp, C.c_longlong, C.c_int, C.c_int, vp, vp, vp],
+            "ppa_dot_local": [vp, vp, C.c_longlong, vp],
             "ppa_op_create_callback": [C.c_int, C.c_int, C.c_double, _APPLY_FN, vp,
                                        C.POINTER(vp)],
             "ppa_arnoldi_ritz_vectors": [vp, C.c_int, vp, vp, vp, vp, vp],
@@ -664,6 +668,23 @@ def cgs2_step(V, ld, n, c, w, Hcol, flag) -> None:
 
 def ts_combine(V, ldv, n, d, G, p, Out, ldo) -> None:
     _check(lib().ppa_ts_combine(_ptr(V), ldv, n, d, _ptr(G), p, _ptr(Out), ldo))
+
+
+# Row-sharded CGS2 building blocks (rank-local sums; dist.py ShardedSolver).
+def cgs_dot_local(V, ld, n, c, w, out) -> None:
+    _check(lib().ppa_cgs_dot_local(_ptr(V), ld, n, c, _ptr(w), _ptr(out)))
+
+
+def cgs_update_dot_local(V, ld, n, c, w, h, out) -> None:
+    _check(lib().ppa_cgs_update_dot_local(_ptr(V), ld, n, c, _ptr(w), _ptr(h), _ptr(out)))
+
+
+def cgs_store_local(V, ld, n, c, w, h2, hsub) -> None:
+    _check(lib().ppa_cgs_store_local(_ptr(V), ld, n, c, _ptr(w), _ptr(h2), _ptr(hsub)))
+
+
+def dot_local(x, y, n, out) -> None:
+    _check(lib().ppa_dot_local(_ptr(x), _ptr(y), n, _ptr(out)))
 
 
 # ------------------------------------------------------------------ solver --

@@ -802,6 +802,43 @@ int ppa_cgs2_step(double* V, long long ld, int n, int c, double* w, double* Hcol
   });
 }
 
+int ppa_cgs_dot_local(const double* V, long long ld, int n, int c, const double* w,
+                      double* out) {
+  return guard([&] {
+    need(V, "ppa_cgs_dot_local");
+    ppa::Context& ctx = ppa::current_context();
+    ppa::kern::ts_dot(V, ld, n, c, w, out, ctx.ws(), ctx.sm_count(), ctx.stream());
+  });
+}
+
+int ppa_cgs_update_dot_local(const double* V, long long ld, int n, int c, double* w,
+                             const double* h, double* out) {
+  return guard([&] {
+    need(V, "ppa_cgs_update_dot_local");
+    ppa::Context& ctx = ppa::current_context();
+    ppa::kern::cgs_update_dot_local(V, ld, n, c, w, h, out, ctx.ws(), ctx.sm_count(),
+                                    ctx.stream());
+  });
+}
+
+int ppa_cgs_store_local(double* V, long long ld, int n, int c, const double* w, const double* h2,
+                        const double* hsub) {
+  return guard([&] {
+    need(V, "ppa_cgs_store_local");
+    need(hsub, "ppa_cgs_store_local");
+    ppa::Context& ctx = ppa::current_context();
+    ppa::kern::cgs_store_local(V, ld, n, c, w, h2, hsub, ctx.ws(), ctx.sm_count(), ctx.stream());
+  });
+}
+
+int ppa_dot_local(const double* x, const double* y, long long n, double* out) {
+  return guard([&] {
+    need(out, "ppa_dot_local");
+    ppa::Context& ctx = ppa::current_context();
+    ppa::kern::dot(x, y, n, out, ctx.ws(), ctx.sm_count(), ctx.stream());
+  });
+}
+
 int ppa_ts_combine(const double* V, long long ldv, int n, int d, const double* G, int p,
                    double* Out, long long ldo) {
   return guard([&] {

@@ -59,8 +59,9 @@ struct PipeArgs {
   double* partials;
   unsigned int* ticket;
   double* scal;  // upd2 finalisation / store hsub
-  double* Hcol;
-  int* flag;
+  double* Hcol;     // kUpd2: the Hessenberg column; nullptr = raw local sums into out
+  int* flag;        // kStore: skipped when *flag (breakdown); nullptr = never
+  const double* hsub;  // kStore: divisor (nullptr: scal[kScalHsub])
 };
 
 __device__ __forceinline__ bool finish_grid(const double* s_col, int width, double* partials,
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(NT) k_tspipe(const __grid_constant__ CUtensorM
   __shared__ double s_red[NWARP];
   __shared__ double s_wn[MODE == kUpd2 ? TR : 1];
 
-  if (MODE == kStore && *a.flag) return;
+  if (MODE == kStore && a.flag && *a.flag) return;
   const int tid = threadIdx.x, lane = tid & 31, g = tid >> 5;
   const int c = a.c;
   const int ntiles = (a.n + TR - 1) / TR;
@@ -275,7 +276,7 @@ __global__ void __launch_bounds__(NT) k_tspipe(const __grid_constant__ CUtensorM
           nrm = fma(wn, wn, nrm);
           a.w[row0 + tid] = wn;
         } else {  // kStore: V[:,c] = (w - V h2) / hsub
-          dstcol[row0 + tid] = wn / a.scal[kScalHsub];
+          dstcol[row0 + tid] = wn / (a.hsub ? *a.hsub : a.scal[kScalHsub]);
         }
       }
     }
@@ -333,6 +334,12 @@ __global__ void __launch_bounds__(NT) k_tspipe(const __grid_constant__ CUtensorM
   }
   if (MODE == kUpd1) {
     if (tid == 0) *a.out = sqrt(s_final[0]);
+    return;
+  }
+  if (MODE == kUpd2 && a.Hcol == nullptr) {
+    // rank-local sums for the row-sharded solve (dist.py): [V^T w, ||w||^2],
+    // all-reduced by the caller before the store sweep
+    for (int j = tid; j <= c; j += NT) a.out[j] = s_final[j];
     return;
   }
   // kUpd2: s_final[0..c) = h2, s_final[c] = ||w||^2 -> Hessenberg column,
@@ -537,6 +544,35 @@ void dcgs2_update(double* V, long long ld, int n, int c, double* z, const double
   a.w = z;
   a.h = coef;
   dispatch<kUpdD>(a, ws, sm_count, st);
+}
+
+void cgs_update_dot_local(const double* V, long long ld, int n, int c, double* w,
+                          const double* h, double* out, ReduceWorkspace& ws, int sm_count,
+                          cudaStream_t st) {
+  if (n <= 0) return;
+  check_basis(V, ld, n, c, "cgs_update_dot_local");
+  check_aligned(w, "cgs_update_dot_local");
+  PipeArgs a = base_args(V, ld, n, c);
+  a.w = w;
+  a.h = h;
+  a.out = out;
+  a.scal = ws.scalars.get();
+  a.Hcol = nullptr;
+  dispatch<kUpd2>(a, ws, sm_count, st);
+}
+
+void cgs_store_local(double* V, long long ld, int n, int c, const double* w, const double* h2,
+                     const double* hsub, ReduceWorkspace& ws, int sm_count, cudaStream_t st) {
+  if (n <= 0) return;
+  check_basis(V, ld, n, c, "cgs_store_local");
+  check_aligned(w, "cgs_store_local");
+  PipeArgs a = base_args(V, ld, n, c);
+  a.w = const_cast<double*>(w);
+  a.h = h2;
+  a.hsub = hsub;
+  a.scal = ws.scalars.get();
+  a.flag = nullptr;
+  dispatch<kStore>(a, ws, sm_count, st);
 }
 
 void cgs1_pass(const double* V, long long ld, int n, int c, double* v, double* corr,

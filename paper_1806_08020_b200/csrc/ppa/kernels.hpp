@@ -274,6 +274,13 @@ void dcgs2_update(double* V, long long ld, int n, int c, double* z, const double
 
 /// One classical Gram-Schmidt pass: c = V^T v; v -= V c; out_norm = ||v||.
 /// corr (device, c) receives the coefficients.
+/// Row-sharded CGS2 (dist.py): sweep 2 with rank-local sums out = [V^T w',
+/// ||w'||^2] (c + 1) after w' = w - V h, and sweep 3 V[:,c] = (w - V h2) / *hsub.
+void cgs_update_dot_local(const double* V, long long ld, int n, int c, double* w,
+                          const double* h, double* out, ReduceWorkspace& ws, int sm_count,
+                          cudaStream_t st);
+void cgs_store_local(double* V, long long ld, int n, int c, const double* w, const double* h2,
+                     const double* hsub, ReduceWorkspace& ws, int sm_count, cudaStream_t st);
 void cgs1_pass(const double* V, long long ld, int n, int c, double* v, double* corr,
                double* out_norm, ReduceWorkspace& ws, int sm_count, cudaStream_t st);
 

@@ -175,6 +175,36 @@ class CudaBackend:
     def copy_(self, dst, src):
         dst.copy_(src)
 
+    # -- tall-skinny basis kernels with rank-local sums (cgs.cu, tallskinny.cu)
+    def basis(self, cols, n):
+        """Column-major basis: row j of the returned (cols, ld) tensor is
+        column j; ld a multiple of 32 doubles (TMA tiles, aligned columns)."""
+        ld = (n + 31) // 32 * 32
+        return self.torch.zeros((cols, ld), dtype=self.torch.float64, device="cuda"), ld
+
+    def cgs_dot(self, V, ld, n, c, w):
+        out = self.empty(c)
+        self.C.cgs_dot_local(V, ld, n, c, w, out)
+        return out
+
+    def cgs_update_dot(self, V, ld, n, c, w, h):
+        out = self.empty(c + 1)
+        self.C.cgs_update_dot_local(V, ld, n, c, w, h, out)
+        return out
+
+    def cgs_store(self, V, ld, n, c, w, h2, hsub):
+        self.C.cgs_store_local(V, ld, n, c, w, h2, hsub)
+
+    def combine(self, V, ld, n, d, G, p, Out, ldo):
+        g = self.torch.as_tensor(np.asfortranarray(G).ravel(order="F"), dtype=self.torch.float64,
+                                 device="cuda")
+        self.C.ts_combine(V, ld, n, d, g, p, Out, ldo)
+
+    def dot(self, x, y):
+        out = self.empty(1)
+        self.C.dot_local(x, y, x.numel(), out)
+        return out
+
 
 class ShardedPoly:
     """pi(A) v on the owned row block of every rank (collective call)."""
@@ -230,14 +260,14 @@ class ShardedPoly:
 # ------------------------------------------------------------ sharded solve --
 # Thick-restarted Arnoldi with the Krylov basis sharded by rows.  Every
 # reduction (CGS2 coefficients, norms, Rayleigh quotients, residuals) is a
-# local partial sum followed by an all-reduce, so every rank holds the same
+# rank-local sum followed by an all-reduce, so every rank holds the same
 # Hessenberg matrix and the replicated host work (Ritz pairs, restart QR,
-# Leja order) makes identical decisions on every rank.  Vector arithmetic is
-# plain torch on the backend's device (CUDA tensors under NCCL, CPU tensors
-# under gloo); the operator is the sharded pi(A)v above.  Same algorithm and
-# counters as the single-GPU solve (csrc/solver.cpp) except
-# that the summation order of the reductions differs (results agree to
-# roundoff, not bit for bit).
+# Leja order) makes identical decisions on every rank.  The tall-skinny work
+# (CGS2 sweeps, V*Q, Ritz vectors, dots) runs in the backend: the repo's
+# kernels on CUDA, torch CPU ops in the gloo tests; the operator is the
+# sharded pi(A)v above.  Same algorithm as the single-GPU solve
+# (csrc/solver.cpp) with classical CGS2; the summation order
+# of the cross-rank reductions differs, so results agree to roundoff.
 
 _PAIR_TOL = 1e-10  # src/arnoldi.cpp:16
 
@@ -271,7 +301,17 @@ def _arrange(values, vectors, ordering: str):
 
 
 class ShardedSolver:
-    """solve() over row-sharded vectors (collective: every rank calls it)."""
+    """solve() over row-sharded vectors (collective: every rank calls it).
+
+    The Krylov basis is column-major on every rank (the backend's basis()),
+    and each CGS2 step runs the single-GPU kernels' three sweeps with
+    rank-local sums (CudaBackend: ppa_cgs_dot_local, ppa_cgs_update_dot_local,
+    ppa_cgs_store_local, TMA-pipelined like the single-GPU step) and one
+    all-reduce after each of the first two: c doubles, then c + 1 (the
+    second-pass coefficients and ||w||^2; the subdiagonal follows by
+    Pythagoras as in cgs2_step).  Ritz vectors and the thick-restart V*Q are
+    ts_combine on the local rows; norms and Rayleigh quotients are local dots
+    plus an all-reduce."""
 
     def __init__(self, plan: HaloPlan, backend, dist, group=None):
         import torch
@@ -289,11 +329,11 @@ class ShardedSolver:
         self.dist.all_reduce(t, group=self.group)
         return t
 
-    def _dots(self, Vc, w):
-        return self._allreduce(Vc @ w)
+    def _dot(self, x, y) -> float:
+        return float(self._allreduce(self.b.dot(x, y)).item())
 
-    def _norm(self, w):
-        return float(self._allreduce((w @ w).reshape(1)).sqrt().item())
+    def _norm(self, w) -> float:
+        return float(np.sqrt(self._dot(w, w)))
 
     # -- operators -----------------------------------------------------------
     def _spmv(self, x):
@@ -314,28 +354,32 @@ class ShardedSolver:
 
     # -- Arnoldi -------------------------------------------------------------
     def _init(self, v0, m):
-        t = self.torch
-        V = t.zeros((m + 1, self.plan.n_local), dtype=t.float64, device=v0.device)
-        V[0] = v0 / self._norm(v0)
-        return V, np.zeros((m + 1, m))
+        n = self.plan.n_local
+        V, ld = self.b.basis(m + 1, n)
+        V[0, :n] = v0 / self._norm(v0)
+        return (V, ld), np.zeros((m + 1, m))
 
-    def _extend(self, V, H, j0, m, op):
+    def _extend(self, B, H, j0, m, op):
         """CGS2 steps j0..m-1; returns (cur_dim, breakdown)."""
+        V, ld = B
+        n = self.plan.n_local
         for j in range(j0, m):
-            w = op(V[j])
-            Vc = V[:j + 1]
-            h1 = self._dots(Vc, w)
-            w = w - Vc.T @ h1
-            h2 = self._dots(Vc, w)
-            w = w - Vc.T @ h2
-            hsub = self._norm(w)
-            col = (h1 + h2).cpu().numpy()
-            H[:j + 1, j] = col
+            w = op(V[j, :n]).contiguous()
+            c = j + 1
+            h1 = self._allreduce(self.b.cgs_dot(V, ld, n, c, w))
+            s2 = self._allreduce(self.b.cgs_update_dot(V, ld, n, c, w, h1))
+            h1h, s2h = h1.cpu().numpy(), s2.cpu().numpy()
+            h2h, nw = s2h[:c], s2h[c]
+            d2 = nw - float(h2h @ h2h)
+            hsub = float(np.sqrt(d2)) if d2 > 0.0 else 0.0
+            col = h1h + h2h
+            H[:c, j] = col
             if not np.isfinite(hsub) or hsub <= 1e-14 * np.sqrt(col @ col + hsub * hsub):
                 H[j + 1, j] = 0.0
                 return j + 1, True
             H[j + 1, j] = hsub
-            V[j + 1] = w / hsub
+            hs = self.torch.full((1,), hsub, dtype=self.torch.float64, device=w.device)
+            self.b.cgs_store(V, ld, n, c, w, s2[:c], hs)
         return m, False
 
     def _ritz(self, H, d, ordering):
@@ -343,30 +387,31 @@ class ShardedSolver:
         vecs = vecs / np.linalg.norm(vecs, axis=0)
         return _arrange(vals, vecs, ordering)
 
-    def _check(self, V, d, vals, vecs, nev):
+    def _check(self, B, d, vals, vecs, nev):
         """Rayleigh quotients and true residuals of the first nev pairs."""
-        t = self.torch
+        V, ld = B
+        n = self.plan.n_local
+        Y, ldy = self.b.basis(2, n)
         mus, res = [], []
         i = 0
         while i < min(nev, len(vals)):
             g = vecs[:, i]
-            yr = V[:d].T @ t.as_tensor(np.ascontiguousarray(g.real), device=V.device)
             if not _is_complex(vals[i]):
-                nrm = self._norm(yr)
-                yr = yr / nrm
+                self.b.combine(V, ld, n, d, g.real.reshape(d, 1), 1, Y, ldy)
+                yr = Y[0, :n] / self._norm(Y[0, :n])
                 ay = self._spmv(yr)
-                mu = float(self._allreduce((yr @ ay).reshape(1)).item())
+                mu = self._dot(yr, ay)
                 res.append(self._norm(ay - mu * yr))
                 mus.append(complex(mu, 0.0))
                 i += 1
                 continue
-            yi = V[:d].T @ t.as_tensor(np.ascontiguousarray(g.imag), device=V.device)
-            nrm = np.sqrt(self._norm(yr) ** 2 + self._norm(yi) ** 2)
-            yr, yi = yr / nrm, yi / nrm
+            self.b.combine(V, ld, n, d, np.stack([g.real, g.imag], axis=1), 2, Y, ldy)
+            nrm = np.sqrt(self._dot(Y[0, :n], Y[0, :n]) + self._dot(Y[1, :n], Y[1, :n]))
+            yr, yi = Y[0, :n] / nrm, Y[1, :n] / nrm
             ar, ai = self._spmv(yr), self._spmv(yi)
             # mu = y^H A y for unit y = yr + i yi
-            re = float(self._allreduce((yr @ ar + yi @ ai).reshape(1)).item())
-            im = float(self._allreduce((yr @ ai - yi @ ar).reshape(1)).item())
+            re = self._dot(yr, ar) + self._dot(yi, ai)
+            im = self._dot(yr, ai) - self._dot(yi, ar)
             r = np.sqrt(self._norm(ar - re * yr + im * yi) ** 2 +
                         self._norm(ai - re * yi - im * yr) ** 2)
             mus += [complex(re, im), complex(re, -im)]
@@ -374,9 +419,10 @@ class ShardedSolver:
             i += 2
         return mus[:nev], res[:nev]
 
-    def _restart(self, V, H, m, vals, vecs, k):
+    def _restart(self, B, H, m, vals, vecs, k):
         """thick_restart (src/arnoldi.cpp:267-334) on the sharded basis."""
-        t = self.torch
+        V, ld = B
+        n = self.plan.n_local
         cols, j = [], 0
         while len(cols) < k and j < len(vals):
             if not _is_complex(vals[j]):
@@ -391,13 +437,13 @@ class ShardedSolver:
         Q, _ = np.linalg.qr(np.stack(cols, axis=1))
         Hk = Q.T @ H[:m, :m] @ Q
         hrow = H[m, m - 1] * Q[m - 1]
-        Qt = t.as_tensor(np.ascontiguousarray(Q), device=V.device)
-        V[:kk] = (V[:m].T @ Qt).T
-        V[kk] = V[m]
-        c = self._dots(V[:kk], V[kk])
-        V[kk] = V[kk] - V[:kk].T @ c
-        rn = self._norm(V[kk])
-        V[kk] = V[kk] / rn
+        self.b.combine(V, ld, n, m, Q, kk, V, ld)  # V[:, :kk] = V[:, :m] Q, in place
+        V[kk, :n] = V[m, :n]
+        w = V[kk, :n]
+        c = self._allreduce(self.b.cgs_dot(V, ld, n, kk, w))
+        s = self._allreduce(self.b.cgs_update_dot(V, ld, n, kk, w, c))
+        rn = float(np.sqrt(s[kk].item()))
+        V[kk, :n] = w / rn
         Hk = Hk + np.outer(c.cpu().numpy(), hrow)
         H[:] = 0.0
         H[:kk, :kk] = Hk
@@ -422,8 +468,8 @@ class ShardedSolver:
         rtol = rtol_multiplier * est
         ordering = "smallest_magnitude"
         if degree > 0:
-            Vb, Hb = self._init(v0_poly, degree)
-            d, _ = self._extend(Vb, Hb, 0, degree, self._spmv)
+            Bb, Hb = self._init(v0_poly, degree)
+            d, _ = self._extend(Bb, Hb, 0, degree, self._spmv)
             Hd = Hb[:d, :d].copy()
             hs = Hb[d, d - 1]
             if hs != 0.0:
@@ -433,15 +479,15 @@ class ShardedSolver:
             if stability and len(self.roots) >= 2:
                 self.roots = C.add_stability_roots(self.roots, len(self.roots))
             ordering = "target_one"
-        V, H = self._init(v0_arnoldi, m)
+        B, H = self._init(v0_arnoldi, m)
         cur, cycles, mus, res = 0, 0, [], []
         for cycles in range(1, max_cycles + 1):
-            d, bd = self._extend(V, H, cur, m, self._op)
+            d, bd = self._extend(B, H, cur, m, self._op)
             vals, vecs = self._ritz(H, d, ordering)
-            mus, res = self._check(V, d, vals, vecs, nev)
+            mus, res = self._check(B, d, vals, vecs, nev)
             if all(r <= rtol for r in res) or bd or cycles == max_cycles:
                 break
-            cur = self._restart(V, H, m, vals, vecs, k)
+            cur = self._restart(B, H, m, vals, vecs, k)
         return {"eigenvalues": np.asarray(mus), "residuals": np.asarray(res), "rtol": rtol,
                 "converged": bool(len(res) == nev and all(r <= rtol for r in res)),
                 "cycles": cycles, "mvps": self.mvps, "poly": self.roots}

@@ -45,6 +45,29 @@ class OracleBackend:
     def copy_(self, dst, src):
         dst.copy_(src)
 
+    # tall-skinny primitives of the sharded solve (torch CPU stand-ins for
+    # the CUDA backend's kernels; same contracts)
+    def basis(self, cols, n):
+        ld = (n + 31) // 32 * 32
+        return torch.zeros((cols, ld), dtype=torch.float64), ld
+
+    def cgs_dot(self, V, ld, n, c, w):
+        return V[:c, :n] @ w
+
+    def cgs_update_dot(self, V, ld, n, c, w, h):
+        w -= V[:c, :n].T @ h
+        return torch.cat([V[:c, :n] @ w, (w @ w).reshape(1)])
+
+    def cgs_store(self, V, ld, n, c, w, h2, hsub):
+        V[c, :n] = (w - V[:c, :n].T @ h2) / hsub
+
+    def combine(self, V, ld, n, d, G, p, Out, ldo):
+        Y = (torch.as_tensor(np.asarray(G, dtype=np.float64)).T @ V[:d, :n]).clone()
+        Out[:p, :n] = Y
+
+    def dot(self, x, y):
+        return (x @ y).reshape(1)
+
     def factor(self, x, y, mode, c0=0.0, c1=0.0, o=None):
         xs = x.numpy()
         s = self.op.apply(xs)
@@ -266,3 +289,47 @@ def test_sharded_solve_cuda_ws1(cuda):
         assert abs(r["mvps"] - g["cost"]["mvps"]) <= 0.05 * g["cost"]["mvps"]
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_local_cgs_sweeps_equal_cgs2_step(cuda):
+    # the rank-local sweeps of the sharded solve at world size 1 (no
+    # all-reduce) reproduce the single-GPU CGS2 step bit for bit: same
+    # kernels, same summation order
+    import paper_1806_08020_b200 as ppa
+    from oracle import oracle as O
+
+    P = ppa.CsrMatrix.laplacian_3d(30)
+    A = ppa.make_csr_operator(P)
+    n, c = P.n, 24
+    st = ppa.arnoldi_init(cuda.tensor(O.normal_vector(n, 5, 3), device="cuda"), n, c)
+    st.extend(A, c)
+    ld = st.ld
+    w0 = cuda.empty(n, dtype=cuda.float64, device="cuda")
+    ppa.spmv(A, st.V_ptr + 8 * ld * (c - 1), w0)
+    # reference: the fused single-GPU step into a copy of the basis
+    V = cuda.empty((c + 1) * ld, dtype=cuda.float64, device="cuda")
+    V.copy_(cuda.as_tensor(np.zeros((c + 1) * ld), device="cuda"))
+    ppa.ts_combine(st.V_ptr, ld, n, c, cuda.tensor(np.eye(c).T.ravel(), device="cuda"), c, V, ld)
+    V2 = V.clone()
+    w = w0.clone()
+    Hc = cuda.empty(c + 2, dtype=cuda.float64, device="cuda")
+    flag = cuda.zeros(2, dtype=cuda.int32, device="cuda")
+    ppa.cgs2_step(V, ld, n, c, w, Hc, flag)
+    # the three local sweeps
+    w2 = w0.clone()
+    h1 = cuda.empty(c, dtype=cuda.float64, device="cuda")
+    s2 = cuda.empty(c + 1, dtype=cuda.float64, device="cuda")
+    ppa._capi.cgs_dot_local(V2, ld, n, c, w2, h1)
+    ppa._capi.cgs_update_dot_local(V2, ld, n, c, w2, h1, s2)
+    h2 = s2[:c].cpu().numpy()
+    d2 = float(s2[c].item()) - float(sum(x * x for x in h2))
+    hs = cuda.full((1,), np.sqrt(d2), dtype=cuda.float64, device="cuda")
+    ppa._capi.cgs_store_local(V2, ld, n, c, w2, s2[:c], hs)
+    assert np.array_equal((h1 + s2[:c]).cpu().numpy(), Hc[:c].cpu().numpy())
+    assert float(hs.item()) == float(Hc[c].item())
+    assert cuda.equal(V2[c * ld:c * ld + n], V[c * ld:c * ld + n])
+    # and the local dot of the reductions
+    out = cuda.empty(1, dtype=cuda.float64, device="cuda")
+    ppa._capi.dot_local(w0, w0, n, out)
+    assert abs(float(out.item()) - float((w0 @ w0).item())) <= 1e-12 * float((w0 @ w0).item())
