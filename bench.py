@@ -557,7 +557,7 @@ def run_sharded(args):
     bspmv = 12.0 * nnz + 4.0 * (n + 1) + 16.0 * n
     roots, _ = load_golden_poly()
     plan = HaloPlan.build(*csr.arrays(), n, dist)
-    sp = ShardedPoly(plan, CudaBackend(plan), dist)
+    sp = ShardedPoly(plan, CudaBackend(plan), dist, peer=args.peer)
     r0, r1 = plan.ranges[rank]
     v = torch.tensor(ppa.normal_vector(n, 2, ppa.STREAM_ARNOLDI)[r0:r1], device="cuda")
     for _ in range(max(args.warmup, 3)):
@@ -578,7 +578,9 @@ def run_sharded(args):
             "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
             "dtype": "f64", "data": "synthetic (seeded generator; BASELINE config 3)",
             "config": {"workload": "config3-laplace3d-160^3-pi(A)v", "parallelism": f"rowblock{ws}",
-                       "halo_rows_per_rank": plan.n_left + plan.n_right},
+                       "halo_rows_per_rank": plan.n_left + plan.n_right,
+                       "halo": "peer memory (CUDA IPC, epoch flags)" if args.peer
+                               else "NCCL point-to-point"},
         }), flush=True)
     dist.destroy_process_group()
 
@@ -593,6 +595,8 @@ def main():
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="strong-scaling row-block sharded pi(A)v (dist.py) instead of replicas")
+    ap.add_argument("--peer", action="store_true",
+                    help="with --sharded: halos over peer memory (dist.PeerHalo) instead of NCCL")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -245,6 +245,30 @@ int ppa_cgs_update_dot_local(const double* V_dev, long long ld, int n, int c, do
                              const double* h_dev, double* out_dev);
 int ppa_cgs_store_local(double* V_dev, long long ld, int n, int c, const double* w_dev,
                         const double* h2_dev, const double* hsub_dev);
+/* Row-sharded pi(A)v halo over peer memory, without NCCL (dist.py PeerHalo;
+   DESIGN.md 7).  Buffers that peers map come from ppa_dev_alloc (cudaMalloc,
+   zeroed); handles are exchanged out of band (torch.distributed) and opened
+   with ppa_ipc_open.  ppa_halo_publish enqueues a system-scope release store
+   of `epoch` into the caller's flag; ppa_halo_pull enqueues, for each peer
+   descriptor, a bounded acquire wait for *flag >= epoch (*error_dev = 1 on
+   timeout instead of a hang) and the gather
+   x_ext[dst_offset + i] = src[src_index[i]] (i < count); x_ext_dev = NULL
+   waits only (a fence before a rank rewrites buffers its peers read). */
+typedef struct ppa_peer_halo {
+  const double* src;          /* the owner's vector (IPC pointer) */
+  const long long* src_index; /* device, on the reader */
+  long long count;
+  long long dst_offset;
+  const long long* flag;      /* the owner's epoch flag (IPC pointer) */
+} ppa_peer_halo;
+int ppa_dev_alloc(size_t bytes, void** out_dev);
+int ppa_dev_free(void* dev_ptr);
+int ppa_ipc_get_handle(const void* dev_ptr, unsigned char* handle64);
+int ppa_ipc_open(const unsigned char* handle64, void** peer_ptr);
+int ppa_ipc_close(void* peer_ptr);
+int ppa_halo_publish(long long* flag_dev, long long epoch);
+int ppa_halo_pull(const ppa_peer_halo* peers_dev, int npeers, long long max_count,
+                  double* x_ext_dev, long long epoch, int* error_dev);
 /* out_dev[0] = x . y, deterministic (dot, inc/cost.hpp:51-57) */
 int ppa_dot_local(const double* x_dev, const double* y_dev, long long n, double* out_dev);
 /* Out = V[:,0:d] G (G d x p col-major, device); in place allowed for p <= d

@@ -134,6 +134,13 @@ def lib():
             "ppa_cgs_update_dot_local": [vp, C.c_longlong, C.c_int, C.c_int, vp, vp, vp],
             "ppa_cgs_store_local": [vp, C.c_longlong, C.c_int, C.c_int, vp, vp, vp],
             "ppa_dot_local": [vp, vp, C.c_longlong, vp],
+            "ppa_dev_alloc": [C.c_size_t, C.POINTER(vp)],
+            "ppa_dev_free": [vp],
+            "ppa_ipc_get_handle": [vp, vp],
+            "ppa_ipc_open": [vp, C.POINTER(vp)],
+            "ppa_ipc_close": [vp],
+            "ppa_halo_publish": [vp, C.c_longlong],
+            "ppa_halo_pull": [vp, C.c_int, C.c_longlong, vp, C.c_longlong, vp],
             "ppa_op_create_callback": [C.c_int, C.c_int, C.c_double, _APPLY_FN, vp,
                                        C.POINTER(vp)],
             "ppa_arnoldi_ritz_vectors": [vp, C.c_int, vp, vp, vp, vp, vp],
@@ -685,6 +692,43 @@ def cgs_store_local(V, ld, n, c, w, h2, hsub) -> None:
 
 def dot_local(x, y, n, out) -> None:
     _check(lib().ppa_dot_local(_ptr(x), _ptr(y), n, _ptr(out)))
+
+
+# Peer-memory halo (dist.py PeerHalo).
+def dev_alloc(nbytes: int) -> int:
+    p = C.c_void_p()
+    _check(lib().ppa_dev_alloc(nbytes, C.byref(p)))
+    return p.value
+
+
+def dev_free(ptr: int) -> None:
+    _check(lib().ppa_dev_free(ptr))
+
+
+def ipc_get_handle(ptr: int) -> bytes:
+    buf = (C.c_ubyte * 64)()
+    _check(lib().ppa_ipc_get_handle(ptr, buf))
+    return bytes(buf)
+
+
+def ipc_open(handle: bytes) -> int:
+    buf = (C.c_ubyte * 64).from_buffer_copy(handle)
+    p = C.c_void_p()
+    _check(lib().ppa_ipc_open(buf, C.byref(p)))
+    return p.value
+
+
+def ipc_close(ptr: int) -> None:
+    _check(lib().ppa_ipc_close(ptr))
+
+
+def halo_publish(flag_ptr: int, epoch: int) -> None:
+    _check(lib().ppa_halo_publish(flag_ptr, epoch))
+
+
+def halo_pull(peers_ptr: int, npeers: int, max_count: int, x_ext, epoch: int,
+              error_ptr: int) -> None:
+    _check(lib().ppa_halo_pull(peers_ptr, npeers, max_count, _ptr(x_ext), epoch, error_ptr))
 
 
 # ------------------------------------------------------------------ solver --

@@ -802,6 +802,69 @@ int ppa_cgs2_step(double* V, long long ld, int n, int c, double* w, double* Hcol
   });
 }
 
+int ppa_dev_alloc(size_t bytes, void** out) {
+  return guard([&] {
+    need(out, "ppa_dev_alloc");
+    void* p = nullptr;
+    PPA_CUDA(cudaMalloc(&p, bytes ? bytes : 16));
+    PPA_CUDA(cudaMemset(p, 0, bytes ? bytes : 16));
+    *out = p;
+  });
+}
+
+int ppa_dev_free(void* p) {
+  return guard([&] {
+    if (p) PPA_CUDA(cudaFree(p));
+  });
+}
+
+int ppa_ipc_get_handle(const void* dev_ptr, unsigned char* handle) {
+  return guard([&] {
+    need(dev_ptr, "ppa_ipc_get_handle");
+    need(handle, "ppa_ipc_get_handle");
+    cudaIpcMemHandle_t h;
+    PPA_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+    static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+    std::memcpy(handle, &h, sizeof(h));
+  });
+}
+
+int ppa_ipc_open(const unsigned char* handle, void** peer_ptr) {
+  return guard([&] {
+    need(handle, "ppa_ipc_open");
+    need(peer_ptr, "ppa_ipc_open");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    PPA_CUDA(cudaIpcOpenMemHandle(peer_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+int ppa_ipc_close(void* peer_ptr) {
+  return guard([&] {
+    if (peer_ptr) PPA_CUDA(cudaIpcCloseMemHandle(peer_ptr));
+  });
+}
+
+int ppa_halo_publish(long long* flag_dev, long long epoch) {
+  return guard([&] {
+    need(flag_dev, "ppa_halo_publish");
+    ppa::kern::publish(flag_dev, epoch, ppa::current_context().stream());
+  });
+}
+
+int ppa_halo_pull(const ppa_peer_halo* peers_dev, int npeers, long long max_count,
+                  double* x_ext_dev, long long epoch, int* error_dev) {
+  return guard([&] {
+    if (npeers <= 0) return;
+    need(peers_dev, "ppa_halo_pull");
+    need(error_dev, "ppa_halo_pull");
+    static_assert(sizeof(ppa_peer_halo) == sizeof(ppa::kern::PeerHaloDesc), "layout");
+    ppa::kern::halo_pull(reinterpret_cast<const ppa::kern::PeerHaloDesc*>(peers_dev), npeers,
+                         max_count, x_ext_dev, epoch, error_dev,
+                         ppa::current_context().stream());
+  });
+}
+
 int ppa_cgs_dot_local(const double* V, long long ld, int n, int c, const double* w,
                       double* out) {
   return guard([&] {

@@ -131,6 +131,23 @@ void spmv_grid2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y
 void spmv_dia2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y,
                const double* base, cudaStream_t st);
 
+/// Halo of the row-sharded pi(A)v pulled from a peer's memory (peer_halo.cu;
+/// dist.py PeerHalo): x_ext[dst_offset + i] = src[src_index[i]], i < count,
+/// once *flag >= the exchange's epoch.  src and flag are CUDA-IPC pointers
+/// into the owner's HBM; src_index lives on the reader.
+struct PeerHaloDesc {
+  const double* src;
+  const long long* src_index;
+  long long count;
+  long long dst_offset;
+  const long long* flag;
+};
+/// *flag = epoch (system-scope release) after the stream's earlier work.
+void publish(long long* flag, long long epoch, cudaStream_t st);
+/// Waits for every peer's flag (bounded: *error = 1 on timeout) and gathers.
+void halo_pull(const PeerHaloDesc* peers_dev, int npeers, long long max_count, double* x_ext,
+               long long epoch, int* error, cudaStream_t st);
+
 /// SELL-32 is used when its padded entry count is at most this factor of nnz.
 constexpr double kSellMaxPadding = 1.15;
 

@@ -206,18 +206,140 @@ class CudaBackend:
         return out
 
 
-class ShardedPoly:
-    """pi(A) v on the owned row block of every rank (collective call)."""
+def peer_pull_lists(plan: HaloPlan, sends: Sequence[Optional[dict]], rank: int):
+    """What this rank pulls from each owner: [(owner, indices into the owner's
+    x_ext, destination offset in this rank's x_ext)], from every rank's send
+    lists (sends[q] = plan.send of rank q).  Pulling these reproduces
+    ShardedPoly.exchange over NCCL entry for entry."""
+    out = []
+    for q, (a, z) in sorted(plan.recv.items()):
+        idx = np.asarray(sends[q][rank], dtype=np.int64)
+        if idx.size != z - a:
+            raise RuntimeError(f"peer_pull_lists: rank {q} sends {idx.size} entries, "
+                               f"{z - a} expected")
+        out.append((q, idx, a))
+    return out
 
-    def __init__(self, plan: HaloPlan, backend, dist, group=None):
+
+_DESC = np.dtype([("src", "<u8"), ("src_index", "<u8"), ("count", "<i8"),
+                  ("dst_offset", "<i8"), ("flag", "<u8")])  # ppa_peer_halo
+
+
+class PeerHalo:
+    """Halo exchange over peer memory (NVLink / NVSwitch) without NCCL
+    (kernels/peer_halo.cu).  Collective constructor.
+
+    Every rank allocates its ShardedPoly vectors (roles 0, 1: the ping-pong
+    pair; 2: the pair temporary t1) and an epoch flag with ppa_dev_alloc,
+    exports them as CUDA IPC handles, and maps the buffers and flags of the
+    ranks it receives halos from.  An exchange of role r is then: publish my
+    epoch e (after the kernel that wrote my role-r vector), and one pull
+    kernel that waits for every owner's flag >= e and gathers
+    x_ext[recv slice] = owner_vector[owner's send list] straight from the
+    owners' HBM.  No collective call and no staging copy per SpMV."""
+
+    ROLES = 3
+
+    def __init__(self, plan: HaloPlan, dist, group=None):
+        import torch
+
+        from . import _capi as C
+
+        self.C, self.torch, self.plan = C, torch, plan
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        n_ext = plan.n_ext
+        self.bufs = [C.dev_alloc(8 * max(n_ext, 1)) for _ in range(self.ROLES)]
+        self.flag = C.dev_alloc(64)
+        self.err = C.dev_alloc(16)
+        self.views = [_device_view(torch, b, n_ext) for b in self.bufs]
+        mine = {"bufs": [C.ipc_get_handle(b) for b in self.bufs],
+                "flag": C.ipc_get_handle(self.flag),
+                "send": {int(q): np.asarray(idx, dtype=np.int64) for q, idx in plan.send.items()}}
+        everyone: List[Optional[dict]] = [None] * world
+        dist.all_gather_object(everyone, mine, group=group)
+        self.opened = []
+        descs = [[] for _ in range(self.ROLES)]
+        self.idx_dev = []
+        self.max_count = 0
+        lists = peer_pull_lists(plan, [e["send"] if e else {} for e in everyone], rank)
+        for q, idx, a in lists:
+            info = everyone[q]
+            peer_bufs = [C.ipc_open(h) for h in info["bufs"]]
+            peer_flag = C.ipc_open(info["flag"])
+            self.opened += peer_bufs + [peer_flag]
+            it = torch.as_tensor(idx, device="cuda")
+            self.idx_dev.append(it)
+            for r in range(self.ROLES):
+                descs[r].append((peer_bufs[r], it.data_ptr(), idx.size, a, peer_flag))
+            self.max_count = max(self.max_count, int(idx.size))
+        self.npeers = len(descs[0])
+        self.desc_dev = []
+        for r in range(self.ROLES):
+            arr = np.array(descs[r], dtype=_DESC) if descs[r] else np.zeros(1, dtype=_DESC)
+            self.desc_dev.append(torch.as_tensor(arr.view(np.uint8), device="cuda"))
+        self.epoch = 0
+
+    def exchange(self, role: int) -> None:
+        self.epoch += 1
+        self.C.halo_publish(self.flag, self.epoch)
+        if self.npeers:
+            self.C.halo_pull(self.desc_dev[role].data_ptr(), self.npeers, self.max_count,
+                             self.views[role], self.epoch, self.err)
+
+    def fence(self) -> None:
+        """Wait until every peer finished its pulls of the previous exchanges
+        (collective): called before a product rewrites its role buffers."""
+        self.epoch += 1
+        self.C.halo_publish(self.flag, self.epoch)
+        if self.npeers:
+            self.C.halo_pull(self.desc_dev[0].data_ptr(), self.npeers, 0, None, self.epoch,
+                             self.err)
+
+    def check(self) -> None:
+        """Raises if a pull timed out (flags never arrived)."""
+        e = self.torch.empty(1, dtype=self.torch.int32, device="cuda")
+        e.copy_(_device_view(self.torch, self.err, 1, self.torch.int32))
+        if int(e.item()):
+            raise RuntimeError("PeerHalo: an owner's epoch flag never arrived")
+
+    def close(self) -> None:
+        for p in self.opened:
+            self.C.ipc_close(p)
+        self.opened = []
+
+
+def _device_view(torch, ptr: int, n: int, dtype=None):
+    """A torch CUDA tensor over raw device memory (no copy, not owned)."""
+    dtype = dtype or torch.float64
+    typestr = {torch.float64: "<f8", torch.int32: "<i4", torch.int64: "<i8"}[dtype]
+
+    class _V:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                    "version": 3, "strides": None, "stream": None}
+
+    return torch.as_tensor(_V(), device="cuda")
+
+
+class ShardedPoly:
+    """pi(A) v on the owned row block of every rank (collective call).
+
+    Halos travel over NCCL point-to-point (batch_isend_irecv) or, with
+    peer=True on GPUs, over peer memory (PeerHalo: no collective per SpMV)."""
+
+    def __init__(self, plan: HaloPlan, backend, dist, group=None, peer: bool = False):
         self.plan = plan
         self.b = backend
         self.dist = dist
         self.group = group
         self._send_idx = {q: idx for q, idx in plan.send.items()}
+        self.peer = PeerHalo(plan, dist, group) if peer else None
 
     def exchange(self, x_ext) -> None:
         """Fill the halo part of x_ext from the owning ranks."""
+        if self.peer is not None:
+            role = next(r for r, v in enumerate(self.peer.views) if v.data_ptr() == x_ext.data_ptr())
+            self.peer.exchange(role)
+            return
         p, d = self.plan, self.dist
         ops, keep = [], []
         for q, idx in sorted(self._send_idx.items()):
@@ -241,10 +363,12 @@ class ShardedPoly:
 
         p = self.plan
         plan = C.factor_plan(roots)
-        cur = self.b.zeros(p.n_ext)
+        if self.peer is not None:
+            self.peer.fence()
+            cur, nxt, t1 = self.peer.views
+        else:
+            cur, nxt, t1 = self.b.zeros(p.n_ext), self.b.zeros(p.n_ext), self.b.zeros(p.n_ext)
         self.b.copy_(cur[p.owned], v_local)
-        nxt = self.b.zeros(p.n_ext)
-        t1 = self.b.zeros(p.n_ext)
         for pair, c0, c1 in plan:
             self.exchange(cur)
             if not pair:
@@ -313,7 +437,7 @@ class ShardedSolver:
     ts_combine on the local rows; norms and Rayleigh quotients are local dots
     plus an all-reduce."""
 
-    def __init__(self, plan: HaloPlan, backend, dist, group=None):
+    def __init__(self, plan: HaloPlan, backend, dist, group=None, peer: bool = False):
         import torch
 
         self.torch = torch
@@ -321,7 +445,7 @@ class ShardedSolver:
         self.b = backend
         self.dist = dist
         self.group = group
-        self.sp = ShardedPoly(plan, backend, dist, group)
+        self.sp = ShardedPoly(plan, backend, dist, group, peer=peer)
         self.mvps = 0
 
     # -- reductions ----------------------------------------------------------
@@ -338,7 +462,11 @@ class ShardedSolver:
     # -- operators -----------------------------------------------------------
     def _spmv(self, x):
         p = self.plan
-        xe = self.b.zeros(p.n_ext)
+        if self.sp.peer is not None:
+            self.sp.peer.fence()
+            xe = self.sp.peer.views[0]
+        else:
+            xe = self.b.zeros(p.n_ext)
         ye = self.b.zeros(p.n_ext)
         self.b.copy_(xe[p.owned], x)
         self.sp.exchange(xe)

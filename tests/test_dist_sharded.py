@@ -144,6 +144,60 @@ def test_sharded_pi_gloo(ws, case):
             assert set(send) <= {rank - 1, rank + 1} and set(recv) <= {rank - 1, rank + 1}
 
 
+def _pull_worker(rank, ws, port, case, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(ws))
+    import torch.distributed as dist
+
+    from oracle import oracle as O
+    from paper_1806_08020_b200.dist import HaloPlan, ShardedPoly, peer_pull_lists
+
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    try:
+        P = CASES[case](O)
+        n = P.info()[0]
+        plan = HaloPlan.build(*P.arrays(), n, dist)
+        sp = ShardedPoly(plan, OracleBackend(plan, O), dist)
+        # a vector whose owned entries are the global row numbers
+        x = torch.zeros(plan.n_ext, dtype=torch.float64)
+        r0, r1 = plan.ranges[rank]
+        x[plan.owned] = torch.arange(r0, r1, dtype=torch.float64)
+        sends = [None] * ws
+        dist.all_gather_object(sends, plan.send)
+        xs = [None] * ws
+        dist.all_gather_object(xs, x.numpy().copy())
+        # the peer pull from every owner's buffer, simulated on the host
+        pulled = x.clone().numpy()
+        for owner, idx, off in peer_pull_lists(plan, sends, rank):
+            pulled[off:off + idx.size] = xs[owner][idx]
+        sp.exchange(x)  # NCCL-style exchange (gloo here)
+        q.put((rank, bool(np.array_equal(pulled, x.numpy()))))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ws", [2, 3])
+@pytest.mark.parametrize("case", ["laplace3d", "random"])
+def test_peer_pull_lists_match_exchange(ws, case):
+    # the peer-memory halo (dist.PeerHalo) pulls exactly what the
+    # point-to-point exchange delivers, for banded and random matrices
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_pull_worker, args=(r, ws, port, case, q)) for r in range(ws)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=180) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(res.values()), res
+
+
 def _solve_worker(rank, ws, port, case, q):
     import sys
 
@@ -333,3 +387,109 @@ def test_local_cgs_sweeps_equal_cgs2_step(cuda):
     out = cuda.empty(1, dtype=cuda.float64, device="cuda")
     ppa._capi.dot_local(w0, w0, n, out)
     assert abs(float(out.item()) - float((w0 @ w0).item())) <= 1e-12 * float((w0 @ w0).item())
+
+
+@pytest.mark.gpu
+def test_peer_halo_pull_kernel(cuda):
+    # the pull kernel on one GPU with a local "owner" buffer: the gather, the
+    # fence (wait only) and the acquire wait on a flag published later from
+    # another stream (no second rank: the wait primitive itself)
+    import time
+
+    from paper_1806_08020_b200 import _capi as C
+    from paper_1806_08020_b200.dist import _DESC, _device_view
+
+    n_src, n_ext = 5000, 300
+    src = C.dev_alloc(8 * n_src)
+    flag = C.dev_alloc(64)
+    err = C.dev_alloc(16)
+    try:
+        sv = _device_view(cuda, src, n_src)
+        sv.copy_(cuda.arange(n_src, dtype=cuda.float64, device="cuda") * 0.5)
+        x = cuda.zeros(n_ext, dtype=cuda.float64, device="cuda")
+        idx = cuda.tensor([7, 4999, 0, 123, 2500, 11], dtype=cuda.int64, device="cuda")
+        desc = np.array([(src, idx.data_ptr(), 6, 100, flag)], dtype=_DESC)
+        dd = cuda.as_tensor(desc.view(np.uint8), device="cuda")
+        C.halo_publish(flag, 1)
+        C.halo_pull(dd.data_ptr(), 1, 6, x, 1, err)
+        cuda.cuda.synchronize()
+        got = x.cpu().numpy()
+        assert np.array_equal(got[100:106], 0.5 * np.array([7, 4999, 0, 123, 2500, 11]))
+        assert not got[:100].any() and not got[106:].any()
+        # wait: a fence for epoch 2 on a non-blocking stream spins until
+        # another stream stores the flag
+        import paper_1806_08020_b200 as ppa
+
+        import threading
+
+        from cuda.bindings import runtime as cudart
+
+        def nb_stream():  # non-blocking: no implicit sync with the legacy stream
+            err_, h = cudart.cudaStreamCreateWithFlags(cudart.cudaStreamNonBlocking)
+            assert int(err_) == 0
+            return h
+
+        ready, go = threading.Event(), threading.Event()
+
+        def publisher():
+            # another thread: its own library context and stream, set up
+            # before the wait starts (creating a context synchronises the
+            # device, which would wait for the spinning kernel itself)
+            sb = nb_stream()
+            ppa.set_stream(int(sb))
+            C.halo_publish(flag, 1)
+            cudart.cudaStreamSynchronize(sb)
+            ready.set()
+            go.wait()
+            C.halo_publish(flag, 2)
+            cudart.cudaStreamSynchronize(sb)
+
+        th = threading.Thread(target=publisher)
+        th.start()
+        ready.wait()
+        sa = nb_stream()
+        ppa.set_stream(int(sa))
+        try:
+            C.halo_pull(dd.data_ptr(), 1, 0, None, 2, err)
+            time.sleep(0.05)
+            assert int(cudart.cudaStreamQuery(sa)[0]) != 0  # still waiting
+            go.set()
+            th.join()
+            cudart.cudaStreamSynchronize(sa)
+        finally:
+            ppa.set_stream(cuda.cuda.current_stream())
+        cuda.cuda.synchronize()
+        e = _device_view(cuda, err, 2, cuda.int32).cpu().numpy()
+        assert e[0] == 0, e
+        h = C.ipc_get_handle(src)
+        assert len(h) == 64 and any(h)
+    finally:
+        for p in (src, flag, err):
+            C.dev_free(p)
+
+
+@pytest.mark.gpu
+def test_sharded_peer_ws1(cuda):
+    # PeerHalo at world size 1 (no peers: the fence and publish still run)
+    # leaves the sharded pi(A)v bit-identical to apply_poly
+    import torch.distributed as dist
+
+    import paper_1806_08020_b200 as ppa
+    from oracle import oracle as O
+    from paper_1806_08020_b200.dist import CudaBackend, HaloPlan, ShardedPoly
+
+    if not dist.is_initialized():
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()), RANK="0",
+                          WORLD_SIZE="1")
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        P = ppa.CsrMatrix.laplacian_3d(14)
+        plan = HaloPlan.build(*P.arrays(), P.n, dist)
+        sp = ShardedPoly(plan, CudaBackend(plan), dist, peer=True)
+        v = O.normal_vector(P.n, 3, 3)
+        out = sp.apply(_roots(O), torch.tensor(v, device="cuda")).clone()
+        sp.peer.check()
+        ref = O.apply_poly(_roots(O), O.csr_operator(O.Csr.laplacian_3d(14)), v)
+        assert np.array_equal(out.cpu().numpy(), ref)
+    finally:
+        dist.destroy_process_group()
