@@ -63,7 +63,7 @@ constexpr int G2_MAXSLOT = 12;
 // without register spills under __launch_bounds__(NT + 32, 1) (ptxas -v, sm_100a).
 constexpr int g2_maxnt(int nd, int ry) {
   return nd == 7 ? (ry == 2 ? 768 : ry == 3 ? 640 : 512)
-                 : (ry == 1 ? 960 : ry == 2 ? 896 : ry == 3 ? 640 : 512);
+                 : (ry == 1 ? 960 : ry == 2 ? 896 : ry == 3 ? 640 : 448);
 }
 
 struct G2Params {
@@ -77,6 +77,7 @@ struct G2Params {
   int nslot;  // x slots
   int segs;   // 3-D: 32-column segments per line; 2-D: segments per level-1 line
   int cw;     // warps that own cells (the block may be rounded up)
+  int fused;  // steady steps: one block for both levels (PPA_GRID2_FUSED)
   const double* zeros;  // >= one line of zeros: the copy source of planes outside the box
 };
 
@@ -168,6 +169,63 @@ __device__ __forceinline__ bool g2_step(
   mbar_wait(x_full + R.sn, R.pn);
 #pragma unroll
   for (int r = 0; r < RY; ++r) xp[r] = g2_lds<0>(xn + C.aX[r]);
+  if (P.fused && t >= 2 && q >= 0 && q < G.nz) {
+    // steady state: wait for level 1 of step t - 1 first, then compute
+    // level 1 at plane q and level 2 at plane q - 1 in one block, so the
+    // 2 RY row-sum chains interleave (the DADD chains are the latency)
+    mbar_wait(l1_done + R.br, R.brp);
+    const uint32_t lw = R.lw, lr = R.lr;
+    const long long qo = static_cast<long long>(q - 1) * G.D;
+    double u[RY], z[RY];
+#pragma unroll
+    for (int r = 0; r < RY; ++r) {
+      const uint32_t a = xq + C.aX[r];
+      const uint32_t b = lr + C.aL[r];
+      double s1, s2;
+      if constexpr (D3) {
+        const double ym = r > 0 ? x0v[r > 0 ? r - 1 : 0] : g2_lds<0>(xq + C.aXm);
+        const double yp = r < RY - 1 ? x0v[r < RY - 1 ? r + 1 : 0] : g2_lds<0>(xq + C.aXp);
+        const double t1[7] = {xm[r], ym, g2_lds<-8>(a), x0v[r], g2_lds<8>(a), yp, xp[r]};
+        // (halo lines have no level 2: their outer neighbours lie outside
+        // the level-1 slot, so those loads are skipped, warp-uniformly)
+        const double lym = r > 0 ? lc[r > 0 ? r - 1 : 0] : (C.w2[r] ? g2_lds<0>(lr + C.aLm) : 0.0);
+        const double lyp = r < RY - 1 ? lc[r < RY - 1 ? r + 1 : 0]
+                                      : (C.w2[r] ? g2_lds<0>(lr + C.aLp) : 0.0);
+        s1 = g2_sum<7>(v, t1);
+        const double t2[7] = {lm[r], lym, g2_lds<-8>(b), lc[r], g2_lds<8>(b), lyp, 0.0};
+        // the +D term of level 2 is level 1 of this step: summed last
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < 6; ++j) acc = __dadd_rn(acc, __dmul_rn(v[j], t2[j]));
+        s2 = acc;
+      } else {
+        const double t1[5] = {xm[r], g2_lds<-8>(a), x0v[r], g2_lds<8>(a), xp[r]};
+        s1 = g2_sum<5>(v, t1);
+        double acc = 0.0;
+        const double t2[4] = {lm[r], g2_lds<-8>(b), lc[r], g2_lds<8>(b)};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc = __dadd_rn(acc, __dmul_rn(v[j], t2[j]));
+        s2 = acc;
+      }
+      u[r] = PAIR ? s1 : __dadd_rn(x0v[r], __dmul_rn(P.a0, s1));
+      ln[r] = C.v1[r] ? u[r] : 0.0;
+      if (C.v1[r]) g2_sts(lw + C.aL[r], u[r]);
+      // the level-2 sum's last term (+D: level 1 at plane q, own column)
+      s2 = __dadd_rn(s2, __dmul_rn(v[ND - 1], ln[r]));
+      z[r] = PAIR ? __dadd_rn(__dadd_rn(xm[r], __dmul_rn(P.a1, lc[r])), __dmul_rn(P.a0, s2))
+                  : __dadd_rn(lc[r], __dmul_rn(P.b0, s2));
+    }
+    __syncwarp();
+    if (lane == 0) g2_arrive(l1_done + R.bw);
+#pragma unroll
+    for (int r = 0; r < RY; ++r) {
+      if (C.v2[r]) {
+        double zz = z[r];
+        if (COMPL) zz = __dsub_rn(__ldg(bc[r] + qo), zz);
+        yc[r][qo] = zz;
+      }
+    }
+  } else {
   // ---- level 1 at plane q into level-1 slot t % 4 (last read by level 2 of
   // step t - 3, which every warp finished before arriving at step t - 2, and
   // this warp waited for that barrier in step t - 1)
@@ -226,6 +284,7 @@ __device__ __forceinline__ bool g2_step(
         yc[r][qo] = z;
       }
     }
+  }
   }
   // ---- advance the rings
   R.xq = R.xn;
@@ -692,6 +751,7 @@ void spmv_grid2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y
   P.nslot = pl.nslot;
   P.segs = pl.segs;
   P.zeros = grid2_zeros();
+  P.fused = g2_env("PPA_GRID2_FUSED", 1);
   P.cw = pl.cw;
   if (nd == 7) {
     switch (pl.ry) {
