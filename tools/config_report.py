@@ -70,6 +70,19 @@ def report(k):
     ppa.solve_double(A, warm) if k == 5 else ppa.solve(A, warm)
     r = ppa.solve_double(A, cfg) if k == 5 else ppa.solve(A, cfg)
     lam = r["eigenvalues"]
+    status = {2: "residual-certified pseudo-eigenvalues (non-normal: DESIGN.md 4.1)",
+              5: "residual-certified pseudo-eigenvalues (non-normal: DESIGN.md 4.1)",
+              4: "not converged within max_cycles on the GPU or the oracle (DESIGN.md 4.1)"}
+    out.update(eigenvalue_status=status.get(k, "eigenvalues (closed-form checked)"),
+               cycles_per_s=round(r["cycles"] / r["timing"]["total"], 3),
+               mvps_per_s=round(r["cost"]["mvps"] / r["timing"]["total"], 1))
+    gold = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests",
+                        "golden", f"c{k}_solve.json")
+    if os.path.exists(gold):
+        g = json.load(open(gold))
+        out.update(oracle_fixture={"seconds": round(g["oracle_seconds"], 1), "cycles": g["cycles"],
+                                   "mvps": g["cost"]["mvps"],
+                                   "threads": "8 (build container)"})
     out.update(solve_s=round(r["timing"]["total"], 4), converged=r["converged"], cycles=r["cycles"],
                mvps=r["cost"]["mvps"], dots=r["cost"]["dots"], rtol=r["rtol"],
                max_residual=float(np.max(r["residuals"])) if len(r["residuals"]) else None,

@@ -38,7 +38,8 @@ rows = list(csv.reader(io.StringIO(ncu("--page", "source", "--csv", "--print-sou
 hdr = rows[1]
 ia, isrc, iss = hdr.index("Instructions Executed"), hdr.index("Source"), hdr.index(
     "Warp Stall Sampling (All Samples)")
-data = [(r[isrc], int(r[ia] or 0), int(r[iss] or 0)) for r in rows[2:] if len(r) > ia]
+data = [(r[isrc], int(r[ia] or 0), int(r[iss] or 0)) for r in rows[2:]
+        if len(r) > ia and r[ia].strip().isdigit()]  # multi-kernel reports repeat headers
 tot, tots = sum(x[1] for x in data), sum(x[2] for x in data)
 print("total inst", tot, "samples", tots)
 op, ops = collections.Counter(), collections.Counter()
