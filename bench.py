@@ -199,6 +199,8 @@ def count_launches(roots, two_factor=False):
 
 # BASELINE config 3 solve settings (configs.py / tests/golden/c3_solve.json)
 SOLVE_C3 = {"m": 40, "k": 20, "nev": 15, "degree": 50, "stability": "pof_auto", "seed": 2}
+SOLVE_SMALL = {1: {"m": 30, "k": 15, "nev": 10, "degree": 10, "seed": 1},
+               2: {"m": 50, "k": 20, "nev": 20, "degree": 25, "seed": 1}}
 
 
 # --------------------------------------------------------------- reference --
@@ -237,6 +239,17 @@ def run_reference(args):
                       "eff_degree": r["composite_degree"], "smallest": round(float(lam[0]), 6),
                       "timing": {"total": round(r["wall"], 4)}, "threads": threads,
                       "params": p}
+    # the smaller configs' solves as well (config 1: the reference's own
+    # CPU-runnable case; config 2): same settings as the GPU arm's
+    # time_to_nev_configs
+    configs_info = None
+    if not args.no_solve:
+        configs_info = {}
+        for k, p in SOLVE_SMALL.items():
+            Ak = O.csr_operator(O.Csr.config(k))
+            r = O.solve(Ak, p["m"], p["k"], p["nev"], degree=p["degree"], seed=p["seed"])
+            configs_info[f"config{k}"] = {"seconds": round(r["wall"], 4), "converged": r["converged"],
+                                          "cycles": r["cycles"], "mvps": r["cost"]["mvps"]}
     cpu = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
            "sample": f"{nf} of {len(roots)} polynomial factors (SpMV+axpy) per step, "
                      "oracle restatement of src/gmres_poly.cpp:117-147, OpenMP rows",
@@ -251,6 +264,7 @@ def run_reference(args):
         "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "time_to_nev": solve_info,
+        "time_to_nev_configs": configs_info,
     }
     print(json.dumps(line), flush=True)
 
@@ -445,7 +459,7 @@ def run_b200(args):
 
     # time to nev converged eigenpairs (config 3, matrix already on device):
     # default layout, and the SELL-32 layout for comparison
-    solve_info = None
+    solve_info = configs_info = None
     if not args.no_solve:
         cfg = ppa.config_solve_config(3)
 
@@ -466,6 +480,16 @@ def run_b200(args):
 
         solve_info = solve_on(A_auto)
         solve_info["layout"] = lay["layout"]
+        configs_info = {}
+        for k in SOLVE_SMALL:
+            Ak = ppa.make_csr_operator(ppa.CsrMatrix.config(k))
+            ck, wk = ppa.config_solve_config(k), ppa.config_solve_config(k, max_cycles=1)
+            ppa.solve(Ak, wk)
+            with clk.region():
+                rk = ppa.solve(Ak, ck)
+            configs_info[f"config{k}"] = {"seconds": round(rk["timing"]["total"], 4),
+                                          "converged": rk["converged"], "cycles": rk["cycles"],
+                                          "mvps": rk["cost"]["mvps"]}
         solve_info["orthogonalization"] = cfg.orthogonalization
         solve_info["sell32"] = solve_on(A)
         # classical CGS2 (three sweeps over V per step instead of the default
@@ -524,6 +548,7 @@ def run_b200(args):
                      "gbs_moved": round(cgs_phys, 2), "bytes_moved": "8n(3c+5)",
                      "breakdown_flag": cgs_flag},
             "time_to_nev": solve_info,
+            "time_to_nev_configs": configs_info,
             "setup_seconds": round(setup_s, 3),
             "poly_check": poly_check,
         }
