@@ -78,6 +78,8 @@ struct G2Params {
   int segs;   // 3-D: 32-column segments per line; 2-D: segments per level-1 line
   int cw;     // warps that own cells (the block may be rounded up)
   int fused;  // steady steps: one block for both levels (PPA_GRID2_FUSED)
+  double* y_q;            // the output vector (the kernel's y)
+  const double* base_q;   // the complement's base vector (COMPL)
   const double* zeros;  // >= one line of zeros: the copy source of planes outside the box
 };
 
@@ -221,8 +223,8 @@ __device__ __forceinline__ bool g2_step(
     for (int r = 0; r < RY; ++r) {
       if (C.v2[r]) {
         double zz = z[r];
-        if (COMPL) zz = __dsub_rn(__ldg(bc[r] + qo), zz);
-        yc[r][qo] = zz;
+        if (COMPL) zz = __dsub_rn(__ldg(P.base_q + qo + C.row2[r]), zz);
+        (P.y_q + qo)[C.row2[r]] = zz;
       }
     }
   } else {
@@ -280,8 +282,8 @@ __device__ __forceinline__ bool g2_step(
       double z = PAIR ? __dadd_rn(__dadd_rn(xm[r], __dmul_rn(P.a1, lc[r])), __dmul_rn(P.a0, s))
                       : __dadd_rn(lc[r], __dmul_rn(P.b0, s));
       if (C.v2[r]) {
-        if (COMPL) z = __dsub_rn(__ldg(bc[r] + qo), z);
-        yc[r][qo] = z;
+        if (COMPL) z = __dsub_rn(__ldg(P.base_q + qo + C.row2[r]), z);
+        (P.y_q + qo)[C.row2[r]] = z;
       }
     }
   }
@@ -345,10 +347,12 @@ __device__ __forceinline__ void g2_produce(const G2Geo& G, const G2Params& P, ch
 template <int ND, int RY, bool PAIR, bool COMPL, int NT>
 __global__ void __launch_bounds__(NT + 32, 1)
     k_spmv_grid2(const double* __restrict__ x, double* y, const double* __restrict__ base,
-                 const G2Params P) {
+                 G2Params P) {
   static_assert(ND == 5 || ND == 7, "5- or 7-point stencils");
   constexpr bool D3 = ND == 7;
   constexpr int NS = D3 ? 6 : 12;  // x slots
+  P.y_q = y;
+  P.base_q = base;
   extern __shared__ __align__(128) double g2_sm[];
   char* sb = reinterpret_cast<char*>(g2_sm);
   uint64_t* x_full = reinterpret_cast<uint64_t*>(g2_sm);
