@@ -305,3 +305,41 @@ def test_grid2_matches_presence_form(cuda, monkeypatch):
         ppa.apply_poly(roots, A, x, y)
         outs.append(host(y))
     assert np.array_equal(outs[0], outs[1])
+
+
+def _grid_fuzz_case(seed):
+    # the diagonal layout keeps its regular-row (and so presence / box-grid)
+    # form only when at least half the rows are interior rows: draw shapes
+    # until that holds
+    rng = np.random.default_rng(5000 + seed)
+    while True:
+        if rng.integers(0, 2):
+            nx = int(rng.choice([4, 10, 32, 46, 64, 96, 130, 160, 250]))
+            ny = int(rng.integers(2, 60))
+            nz = int(rng.integers(3, 40))
+            interior = max(nx - 2, 0) * max(ny - 2, 0) * max(nz - 2, 0) / (nx * ny * nz)
+        else:
+            nx = int(rng.choice([8, 66, 300, 514, 1000, 1500, 2048]))
+            ny = 1
+            nz = int(rng.integers(3, 200))
+            interior = max(nx - 2, 0) * max(nz - 2, 0) / (nx * nz)
+        if interior >= 0.55:
+            break
+    nd = 7 if ny > 1 else 5
+    vals = [float(v) for v in rng.choice([-1.0, 2.5, -0.75, 4.0, 0.5, -3.0, 6.0], size=nd)]
+    kind = str(rng.choice(["real_even", "real_odd", "mixed", "pairs_only", "single_real"]))
+    return (nx, ny, nz), vals, kind, bool(rng.integers(0, 2))
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_grid2_fuzz_bit_exact(cuda, seed):
+    # seeded box shapes (3-D lines of 4-250 columns, 2-D lines up to 2048,
+    # few and many planes), values per diagonal and root mixes: the
+    # box-grid pass equals the oracle bit for bit
+    box, vals, kind, complement = _grid_fuzz_case(seed)
+    n, rp, ci, vv = _box(*box, vals)
+    P = ppa.CsrMatrix.from_arrays(n, rp, ci, vv)
+    Q = O.Csr.from_arrays(n, rp, ci, vv)
+    lay = ppa.make_csr_operator(P).layout()
+    assert lay["grid"] == box and lay["grid_pass"], (box, lay)
+    _check(cuda, P, Q, ROOTS[kind], complement, seed=seed)
