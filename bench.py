@@ -494,7 +494,9 @@ def run_b200(args):
                 rk = sk(Ak, ck)
             configs_info[f"config{k}"] = {"seconds": round(rk["timing"]["total"], 4),
                                           "converged": rk["converged"], "cycles": rk["cycles"],
-                                          "mvps": rk["cost"]["mvps"]}
+                                          "mvps": rk["cost"]["mvps"],
+                                          "timing": {kk: round(vv, 4)
+                                                     for kk, vv in rk["timing"].items()}}
         solve_info["orthogonalization"] = cfg.orthogonalization
         solve_info["sell32"] = solve_on(A)
         # classical CGS2 (three sweeps over V per step instead of the default

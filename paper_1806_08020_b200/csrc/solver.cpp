@@ -55,12 +55,16 @@ class PinnedPool {
   }
   double* acquire(size_t count) {
     std::lock_guard<std::mutex> g(mu_);
+    // best fit: the smallest free buffer that holds `count`
+    size_t best = free_.size();
     for (size_t i = 0; i < free_.size(); ++i) {
-      if (free_[i].second >= count) {
-        double* p = free_[i].first;
-        free_.erase(free_.begin() + static_cast<long>(i));
-        return p;
-      }
+      if (free_[i].second >= count && (best == free_.size() || free_[i].second < free_[best].second))
+        best = i;
+    }
+    if (best < free_.size()) {
+      double* p = free_[best].first;
+      free_.erase(free_.begin() + static_cast<long>(best));
+      return p;
     }
     void* p = nullptr;
     if (cudaMallocHost(&p, count * sizeof(double)) != cudaSuccess) {
@@ -73,8 +77,15 @@ class PinnedPool {
   void release(double* p) {
     std::lock_guard<std::mutex> g(mu_);
     free_.emplace_back(p, size_[p]);
-    // keep at most four buffers; drop the smallest
-    while (free_.size() > 4) {
+    // keep up to 16 buffers and 1 GiB (solves of different sizes in one
+    // process must not page-lock fresh buffers each time: ~100 ms per
+    // 130 MB); drop the smallest beyond that
+    auto bytes = [&]() {
+      size_t b = 0;
+      for (const auto& f : free_) b += f.second * sizeof(double);
+      return b;
+    };
+    while (free_.size() > 16 || (free_.size() > 1 && bytes() > (size_t{1} << 30))) {
       auto it = std::min_element(free_.begin(), free_.end(),
                                  [](const auto& a, const auto& b) { return a.second < b.second; });
       cudaFreeHost(it->first);
