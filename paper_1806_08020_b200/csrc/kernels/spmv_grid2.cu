@@ -77,7 +77,6 @@ struct G2Params {
   int nslot;  // x slots
   int segs;   // 3-D: 32-column segments per line; 2-D: segments per level-1 line
   int cw;     // warps that own cells (the block may be rounded up)
-  int fused;  // steady steps: one block for both levels (PPA_GRID2_FUSED)
   double* y_q;            // the output vector (the kernel's y)
   const double* base_q;   // the complement's base vector (COMPL)
   const double* zeros;  // >= one line of zeros: the copy source of planes outside the box
@@ -158,8 +157,8 @@ __device__ __forceinline__ void g2_sts(uint32_t a, double v) {
 template <int ND, int RY, bool PAIR, bool COMPL, int NS>
 __device__ __forceinline__ bool g2_step(
     int t, const G2Geo& G, const G2Cells<RY>& C, const G2Params& P, const double (&v)[7],
-    G2Ring& R, uint64_t* x_full, uint64_t* l1_done, int lane, double* const (&yc)[RY],
-    const double* const (&bc)[RY], double (&xm)[RY], double (&x0v)[RY], double (&xp)[RY],
+    G2Ring& R, uint64_t* x_full, uint64_t* l1_done, int lane, double*& yb, const double*& bb,
+    int cs, double (&xm)[RY], double (&x0v)[RY], double (&xp)[RY],
     double (&lm)[RY], double (&lc)[RY], double (&ln)[RY]) {
   constexpr bool D3 = ND == 7;
   if (t >= G.nsteps) return false;
@@ -171,13 +170,12 @@ __device__ __forceinline__ bool g2_step(
   mbar_wait(x_full + R.sn, R.pn);
 #pragma unroll
   for (int r = 0; r < RY; ++r) xp[r] = g2_lds<0>(xn + C.aX[r]);
-  if (P.fused && t >= 2 && q >= 0 && q < G.nz) {
+  if (t >= 2 && q >= 0 && q < G.nz) {
     // steady state: wait for level 1 of step t - 1 first, then compute
     // level 1 at plane q and level 2 at plane q - 1 in one block, so the
     // 2 RY row-sum chains interleave (the DADD chains are the latency)
     mbar_wait(l1_done + R.br, R.brp);
     const uint32_t lw = R.lw, lr = R.lr;
-    const long long qo = static_cast<long long>(q - 1) * G.D;
     double u[RY], z[RY];
 #pragma unroll
     for (int r = 0; r < RY; ++r) {
@@ -223,8 +221,8 @@ __device__ __forceinline__ bool g2_step(
     for (int r = 0; r < RY; ++r) {
       if (C.v2[r]) {
         double zz = z[r];
-        if (COMPL) zz = __dsub_rn(__ldg(P.base_q + qo + C.row2[r]), zz);
-        (P.y_q + qo)[C.row2[r]] = zz;
+        if (COMPL) zz = __dsub_rn(__ldg(bb + r * cs), zz);
+        yb[r * cs] = zz;
       }
     }
   } else {
@@ -264,7 +262,6 @@ __device__ __forceinline__ bool g2_step(
   if (t >= 2) {
     mbar_wait(l1_done + R.br, R.brp);
     const uint32_t lr = R.lr;
-    const long long qo = static_cast<long long>(q - 1) * G.D;
 #pragma unroll
     for (int r = 0; r < RY; ++r) {
       if (!C.w2[r]) continue;  // warp-uniform: a halo line
@@ -282,13 +279,15 @@ __device__ __forceinline__ bool g2_step(
       double z = PAIR ? __dadd_rn(__dadd_rn(xm[r], __dmul_rn(P.a1, lc[r])), __dmul_rn(P.a0, s))
                       : __dadd_rn(lc[r], __dmul_rn(P.b0, s));
       if (C.v2[r]) {
-        if (COMPL) z = __dsub_rn(__ldg(P.base_q + qo + C.row2[r]), z);
-        (P.y_q + qo)[C.row2[r]] = z;
+        if (COMPL) z = __dsub_rn(__ldg(bb + r * cs), z);
+        yb[r * cs] = z;
       }
     }
   }
   }
-  // ---- advance the rings
+  // ---- advance the output rows and the rings
+  yb += G.D;
+  if (COMPL) bb += G.D;
   R.xq = R.xn;
   R.xn += R.xstep;
   if (++R.sn == NS) {
@@ -456,13 +455,13 @@ __global__ void __launch_bounds__(NT + 32, 1)
     asm volatile("" : "+d"(v[j]));  // keep the coefficients in registers
   }
   const uint32_t sbase = smem_u32(g2_sm);
-  double* yc[RY];
-  const double* bc[RY];
-#pragma unroll
-  for (int r = 0; r < RY; ++r) {
-    yc[r] = y + C.row2[r];
-    bc[r] = COMPL ? base + C.row2[r] : nullptr;
-  }
+  // output rows of cell 0 at the level-2 plane of step 0 (za - 2; advanced
+  // by one plane per step, dereferenced only for level-2 cells); cell r sits
+  // cs rows further (3-D: the next grid line, 2-D: the next 32-column segment)
+  const long long row0 = static_cast<long long>(G.za - 2) * G.D + C.row2[0];
+  double* yb = y + row0;
+  const double* bb = COMPL ? base + row0 : nullptr;
+  const int cs = D3 ? nx : 32;
 
   // registers: x and level-1 values of three consecutive planes per cell,
   // in rotating triples (a, b, c); x planes za-2 and za-1 first
@@ -495,8 +494,8 @@ __global__ void __launch_bounds__(NT + 32, 1)
   R.br = 2 * NS - 1;
   R.brp = 1;
 #define G2_STEP(XM, X0, XP, LM, LC, LN)                                                     \
-  if (!g2_step<ND, RY, PAIR, COMPL, NS>(t++, G, C, P, v, R, x_full, l1_done, lane, yc,       \
-                                        bc, XM, X0, XP, LM, LC, LN)) {                      \
+  if (!g2_step<ND, RY, PAIR, COMPL, NS>(t++, G, C, P, v, R, x_full, l1_done, lane, yb, bb, cs, \
+                                        XM, X0, XP, LM, LC, LN)) {                          \
     break;                                                                                  \
   }
   for (int t = 0;;) {
@@ -755,7 +754,6 @@ void spmv_grid2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y
   P.nslot = pl.nslot;
   P.segs = pl.segs;
   P.zeros = grid2_zeros();
-  P.fused = g2_env("PPA_GRID2_FUSED", 1);
   P.cw = pl.cw;
   if (nd == 7) {
     switch (pl.ry) {
