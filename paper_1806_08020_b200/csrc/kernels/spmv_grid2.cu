@@ -382,15 +382,12 @@ __global__ void __launch_bounds__(NT + 32, 1)
   G.slot_l = P.LL * Pt;
   const int nload = G.nsteps + 2;  // x planes za-2 .. zb+1
 
-  // ---- zero every slot (the cells outside the box are never written
-  // again), init barriers; overlaps the previous pass (PDL)
-  for (int i = tid; i < G.ls0 + G2_LSLOT * G.slot_l - G.xs0; i += NT + 32) g2_sm[G.xs0 + i] = 0.0;
+  // ---- init barriers; overlaps the previous pass (PDL)
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(x_full + s, 1);
     for (int s = 0; s < 2 * NS; ++s) mbar_init(l1_done + s, NT / 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
   pdl_trigger();
   pdl_wait();  // x is the previous pass's output
@@ -407,6 +404,42 @@ __global__ void __launch_bounds__(NT + 32, 1)
     g2_produce<D3, NS>(G, P, sb, x_full, l1_done, lane, x, x0, xa, y0, ylo, yhi, line_bytes,
                        plane_bytes, NS, nload, 0);
     return;
+  }
+
+  // ---- zero the slot cells that are read but never written - the pad
+  // columns of each line and whole lines outside the box or the tile - while
+  // the first planes are in flight (the copies and the level-1 stores write
+  // the other cells before they are read; these cells are disjoint from the
+  // copies, so no proxy fence is needed)
+  {
+    // x slots: copies write lines [xl0, xl1), columns [xw0, xw1)
+    const int xw0 = xa - (x0 - 2), xw1 = xb - (x0 - 2);
+    const int xl0 = D3 ? ylo - (y0 - 2) : 0, xl1 = D3 ? yhi - (y0 - 2) : 1;
+    // level-1 slots: stores write lines [ll0, ll1), columns [lw0, lw1)
+    int lw0, lw1, ll0, ll1;
+    if (D3) {
+      lw0 = 2;
+      lw1 = nx + 2;
+      ll0 = max(0, 1 - y0);
+      ll1 = min(y1 - y0 + 2, ny - y0 + 1);
+    } else {
+      lw0 = max(x0 - 1, 0) - x0 + 2;
+      lw1 = min(x1 + 1, nx) - x0 + 2;
+      ll0 = 0;
+      ll1 = 1;
+    }
+    const int nxl = NS * P.SL, nll = G2_LSLOT * P.LL;
+    for (int k = tid; k < nxl + nll; k += NT) {
+      const bool isx = k < nxl;
+      const int kk = isx ? k : k - nxl;
+      const int sl = kk / (isx ? P.SL : P.LL), line = kk % (isx ? P.SL : P.LL);
+      double* row = g2_sm + (isx ? G.xs0 + sl * G.slot_x : G.ls0 + sl * G.slot_l) + line * Pt;
+      const bool in = isx ? (line >= xl0 && line < xl1) : (line >= ll0 && line < ll1);
+      const int c0 = in ? (isx ? xw0 : lw0) : Pt, c1 = in ? (isx ? xw1 : lw1) : Pt;
+      for (int c = 0; c < c0; ++c) row[c] = 0.0;
+      for (int c = c1; c < Pt; ++c) row[c] = 0.0;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory");
   }
 
   // ---- cells of this (consumer) thread
