@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -457,6 +458,139 @@ void dispatch(const PipeArgs& a, ReduceWorkspace& ws, int sm_count, cudaStream_t
   return launch_pipe<MODE, 16>(a, ws, sm_count, st);
 }
 
+// Out[:, 0:p] = V[:, 0:d] * G, the thick-restart recombination V*Q and the
+// batched Ritz vectors (src/arnoldi.cpp:258, 306-309), on the same persistent
+// tile pipeline as the sweeps above: 128-row tiles of V[:, 0:d] arrive by
+// TMA in `stages` shared-memory stages.  Thread t owns row t & 127 of a tile
+// and the HP output columns [h HP, h HP + HP) of half h = t >> 7; G sits
+// row-major in shared memory and is read as 16-byte broadcasts.  Per output
+// the FMAs run over j = 0..d-1 in order, exactly as the register kernel of
+// tallskinny.cu, so both give the same bits.  A tile's outputs are written
+// after the tile is in shared memory and other tiles' rows are disjoint, so
+// Out may alias V[:, 0:p] (p <= d).
+template <int HP>
+__global__ void __launch_bounds__(NT) k_combine_tma(const __grid_constant__ CUtensorMap vmap, int n,
+                                                    int d, const double* __restrict__ G, int p,
+                                                    double* Out, long long ldo, int tiles_per_cta,
+                                                    int S) {
+  constexpr int PB = 2 * HP;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  double* gs = reinterpret_cast<double*>(smem + 128);
+  const int gsz = (d * PB + 127) / 128 * 128;  // doubles, a multiple of 1 KB
+  double* stage0 = gs + gsz;
+  const size_t stage_elems = static_cast<size_t>(d) * TR;
+  const int tid = threadIdx.x;
+  const int ntiles = (n + TR - 1) / TR;
+  const int t_begin = blockIdx.x * tiles_per_cta;
+  const int count = max(0, min(ntiles, t_begin + tiles_per_cta) - t_begin);
+  for (int k = tid; k < d * PB; k += NT) {
+    const int j = k / PB, c = k - j * PB;
+    gs[k] = c < p ? G[static_cast<long long>(c) * d + j] : 0.0;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint64_t policy = evict_first_policy();
+  auto issue = [&](int i) {
+    const int s = i % S;
+    mbar_expect_tx(&bar[s], static_cast<uint32_t>(TR * d * 8));
+    tma_load_2d(stage0 + s * stage_elems, &vmap, (t_begin + i) * TR, 0, &bar[s], policy);
+  };
+  if (tid == 0) {
+    for (int i = 0; i < min(S, count); ++i) issue(i);
+  }
+  // the CTA's halves take alternate tiles (S is even); in a half, thread u
+  // owns rows u & 63 and (u & 63) + 64 and output columns [h HP, h HP + HP)
+  // of h = u >> 6: every broadcast of a G pair serves four FMAs
+  const int half = tid >> 7, u = tid & 127;
+  const int r = u & 63, h = u >> 6;
+  const double* gh = gs + h * HP;
+  for (int i0 = 0; i0 < count; i0 += 2) {
+    const int i = i0 + half;
+    if (i < count) {
+      const int s = i % S;
+      mbar_wait(&bar[s], (i / S) & 1);
+      const double* T = stage0 + s * stage_elems + r;
+      double acc[2][HP];
+#pragma unroll
+      for (int c = 0; c < HP; ++c) acc[0][c] = acc[1][c] = 0.0;
+      auto fma_row = [&](double v0, double v1, int j) {
+        const double2* g2 = reinterpret_cast<const double2*>(gh + j * PB);
+#pragma unroll
+        for (int q = 0; q < HP / 2; ++q) {
+          const double2 gv = g2[q];
+          acc[0][2 * q] = fma(v0, gv.x, acc[0][2 * q]);
+          acc[0][2 * q + 1] = fma(v0, gv.y, acc[0][2 * q + 1]);
+          acc[1][2 * q] = fma(v1, gv.x, acc[1][2 * q]);
+          acc[1][2 * q + 1] = fma(v1, gv.y, acc[1][2 * q + 1]);
+        }
+      };
+      int j = 0;
+      for (; j + 2 <= d; j += 2) {
+        const double a0 = T[j * TR], b0 = T[j * TR + 64];
+        const double a1 = T[(j + 1) * TR], b1 = T[(j + 1) * TR + 64];
+        fma_row(a0, b0, j);
+        fma_row(a1, b1, j + 1);
+      }
+      for (; j < d; ++j) fma_row(T[j * TR], T[j * TR + 64], j);
+      const long long row = static_cast<long long>(t_begin + i) * TR + r;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (row + 64 * k < n) {
+#pragma unroll
+          for (int c = 0; c < HP; ++c) {
+            const int col = h * HP + c;
+            if (col < p) Out[row + 64 * k + static_cast<long long>(col) * ldo] = acc[k][c];
+          }
+        }
+      }
+    }
+    // both halves are done with their stages: refill them
+    __syncthreads();
+    if (tid == 0) {
+      if (i0 + S < count) issue(i0 + S);
+      if (i0 + 1 + S < count) issue(i0 + 1 + S);
+    }
+  }
+}
+
+template <int HP>
+void launch_combine_tma(const double* V, long long ld, int n, int d, const double* G, int p,
+                        double* Out, long long ldo, int sm_count, cudaStream_t st) {
+  const size_t stage_bytes = static_cast<size_t>(d) * TR * sizeof(double);
+  const size_t g_bytes = static_cast<size_t>((d * 2 * HP + 127) / 128 * 128) * sizeof(double);
+  // an even number of stages (the CTA's two halves take alternate tiles),
+  // at least four so that a pair of tiles is in flight while a pair is
+  // consumed: two CTAs per SM when both get four stages, else one with up
+  // to six
+  int per_sm = 2 * (128 + g_bytes + 4 * stage_bytes) <= kSmemPerSm ? 2 : 1;
+  const size_t budget = kSmemPerSm / per_sm - 128 - g_bytes;
+  const int stages = static_cast<int>(std::max<size_t>(2, std::min<size_t>(6, budget / stage_bytes))) & ~1;
+  const size_t smem = 128 + g_bytes + stages * stage_bytes;
+  static const bool capped = [] {
+    PPA_CUDA(cudaFuncSetAttribute(k_combine_tma<HP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  max_dynamic_smem(k_combine_tma<HP>)));
+    return true;
+  }();
+  (void)capped;
+  int fit = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, k_combine_tma<HP>, NT, smem) ==
+          cudaSuccess &&
+      fit > 0) {
+    per_sm = std::min(per_sm, fit);
+  }
+  const int ntiles = (n + TR - 1) / TR;
+  const int grid0 = std::max(1, std::min(ntiles, sm_count * per_sm));
+  const int tpc = (ntiles + grid0 - 1) / grid0;
+  const int grid = (ntiles + tpc - 1) / tpc;
+  const CUtensorMap map = basis_map(V, ld, n, d);
+  k_combine_tma<HP><<<grid, NT, smem, st>>>(map, n, d, G, p, Out, ldo, tpc, stages);
+  PPA_CUDA(cudaGetLastError());
+}
+
 void check_aligned(const void* p, const char* who) {
   if (reinterpret_cast<uintptr_t>(p) % 16 != 0) {
     throw std::invalid_argument(std::string(who) + ": vectors must be 16-byte aligned");
@@ -481,6 +615,27 @@ PipeArgs base_args(const double* V, long long ld, int n, int c) {
 }
 
 }  // namespace
+
+bool ts_combine_tma(const double* V, long long ldv, int n, int d, const double* G, int p,
+                    double* Out, long long ldo, int sm_count, cudaStream_t st) {
+  // the tensor map needs a 16-byte aligned base and an even ld; tiles of
+  // d <= 96 columns keep two stages within the shared-memory budget
+  if (p < 1 || p > 32 || d < 1 || d > 96 || n < TR) return false;
+  if (reinterpret_cast<uintptr_t>(V) % 16 || ldv % 2 || ldv < n) return false;
+  const char* off = std::getenv("PPA_COMBINE_TMA");
+  if (off && off[0] == '0') return false;
+  switch ((p + 3) / 4) {  // outputs per thread: half the padded column count
+    case 1: launch_combine_tma<2>(V, ldv, n, d, G, p, Out, ldo, sm_count, st); break;
+    case 2: launch_combine_tma<4>(V, ldv, n, d, G, p, Out, ldo, sm_count, st); break;
+    case 3: launch_combine_tma<6>(V, ldv, n, d, G, p, Out, ldo, sm_count, st); break;
+    case 4: launch_combine_tma<8>(V, ldv, n, d, G, p, Out, ldo, sm_count, st); break;
+    case 5: launch_combine_tma<10>(V, ldv, n, d, G, p, Out, ldo, sm_count, st); break;
+    case 6: launch_combine_tma<12>(V, ldv, n, d, G, p, Out, ldo, sm_count, st); break;
+    case 7: launch_combine_tma<14>(V, ldv, n, d, G, p, Out, ldo, sm_count, st); break;
+    default: launch_combine_tma<16>(V, ldv, n, d, G, p, Out, ldo, sm_count, st); break;
+  }
+  return true;
+}
 
 void ts_dot(const double* V, long long ld, int n, int c, const double* w, double* out,
             ReduceWorkspace& ws, int sm_count, cudaStream_t st) {

@@ -431,10 +431,18 @@ void ts_combine(const double* V, long long ldv, int n, int d, const double* G, i
   }
   // accumulator count bucketed so registers stay <= ~128 per thread; the
   // passes only read V, so they are independent (in place: one pass)
+  int sms = 148;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) {
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+  }
   for (int c0 = 0; c0 < p; c0 += 32) {
     const int pc = std::min(32, p - c0);
     const double* g = G + static_cast<long long>(c0) * d;
     double* out = Out + static_cast<long long>(c0) * ldo;
+    if (ts_combine_tma(V, ldv, n, d, g, pc, out, ldo, sms, st)) continue;
     auto sm = [&](int pb) { return static_cast<size_t>(d) * pb * sizeof(double); };
     switch ((pc + 3) / 4) {  // accumulators rounded up to a multiple of 4
       case 1: launch_combine<4>(V, ldv, n, d, g, pc, out, ldo, sm(4), st); break;

@@ -304,6 +304,10 @@ void cgs1_pass(const double* V, long long ld, int n, int c, double* v, double* c
 /// Out[:,0:p] = V[:,0:d] * G, G column-major d x p on device.  In place
 /// (Out == V, same ld) is allowed when p <= d: every row block is staged in
 /// shared memory before it is overwritten.
+/// TMA-fed form of ts_combine (cgs.cu k_combine_tma), same bits; false when
+/// it does not apply (p > 32, d > 96, misaligned V, PPA_COMBINE_TMA=0).
+bool ts_combine_tma(const double* V, long long ldv, int n, int d, const double* G, int p,
+                    double* Out, long long ldo, int sm_count, cudaStream_t st);
 void ts_combine(const double* V, long long ldv, int n, int d, const double* G, int p,
                 double* Out, long long ldo, cudaStream_t st);
 

@@ -753,3 +753,33 @@ def test_ts_combine_shapes(cuda, d, p, inplace):
     assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(ref)) * d
     if inplace:  # columns p..d untouched
         assert np.array_equal(host(V).reshape(d + 1, ld)[p:, :n], Vh[p:, :n])
+
+
+@pytest.mark.parametrize("d,p,inplace,n", [(40, 20, True, 4099), (40, 15, False, 3001),
+                                           (41, 21, True, 128), (7, 3, False, 1000),
+                                           (96, 32, True, 2177), (60, 45, True, 1500),
+                                           (30, 20, False, 257)])
+def test_ts_combine_tma_equals_register_kernel(cuda, monkeypatch, d, p, inplace, n):
+    # the TMA-fed V*G (cgs.cu k_combine_tma) and the register kernel
+    # (tallskinny.cu) sum each output over j in the same order with fma:
+    # identical bits, in place and out of place, ragged last tiles
+    ld = (n + 31) // 32 * 32
+    rng = np.random.default_rng(d * 7 + p + n)
+    Vh = np.zeros((d + 1, ld))
+    Vh[:, :n] = rng.standard_normal((d + 1, n))
+    Gh = rng.standard_normal((p, d))
+    outs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("PPA_COMBINE_TMA", flag)
+        V = cuda.tensor(Vh.ravel(), device="cuda")
+        G = cuda.tensor(Gh.ravel(), device="cuda")
+        if inplace:
+            ppa.ts_combine(V, ld, n, d, G, p, V, ld)
+            outs.append(host(V).reshape(d + 1, ld)[:, :n])
+        else:
+            Out = cuda.zeros(p * ld, dtype=cuda.float64, device="cuda")
+            ppa.ts_combine(V, ld, n, d, G, p, Out, ld)
+            outs.append(host(Out).reshape(p, ld)[:, :n])
+    assert np.array_equal(outs[0], outs[1])
+    ref = Gh @ Vh[:d, :n]
+    assert np.max(np.abs(outs[0][:p] - ref)) <= 1e-13 * np.max(np.abs(ref)) * d
