@@ -269,6 +269,25 @@ int ppa_ipc_close(void* peer_ptr);
 int ppa_halo_publish(long long* flag_dev, long long epoch);
 int ppa_halo_pull(const ppa_peer_halo* peers_dev, int npeers, long long max_count,
                   double* x_ext_dev, long long epoch, int* error_dev);
+/* Sharded box-grid pass with the halo exchange fused in (dist.py
+   ShardedGridPoly): polynomial factors of the chain of
+   src/gmres_poly.cpp:129-143 - kind 0: two real roots (a0 = -1/theta1,
+   b0 = -1/theta2), kind 1: a conjugate pair (a0 = 1/|theta|^2,
+   a1 = -2 Re theta/|theta|^2), kind 2: one real root (a0) - over the planes
+   [zo0, zo1) of an nx x ny x nz box stencil (nd = 7; nd = 5 with ny = 1: the
+   2-D 5-point form) with the nd diagonal values vals (host, increasing
+   offset).  x_dev / y_dev hold the owned planes only.  The kernel's copy
+   engine reads the two halo planes below from xl_dev (a neighbour's vector,
+   its local plane 0 = global plane zl0) and the two above from xr_dev (local
+   plane 0 = global plane zo1) once the neighbours' flags (fl_dev, fr_dev,
+   IPC pointers from ppa_halo_publish's protocol) reach `epoch`; *err_dev = 1
+   if a flag never arrives (~10 s).  Pointers of absent neighbours (zo0 = 0,
+   zo1 = nz) may be NULL.  Bit-identical to the unsharded pass. */
+int ppa_grid2_slab_pass(int nd, int nx, int ny, int nz, const double* vals, int zo0, int zo1,
+                        int kind, double a0, double a1, double b0, const double* x_dev,
+                        double* y_dev, const double* xl_dev, int zl0, const long long* fl_dev,
+                        const double* xr_dev, const long long* fr_dev, long long epoch,
+                        int* err_dev);
 /* out_dev[0] = x . y, deterministic (dot, inc/cost.hpp:51-57) */
 int ppa_dot_local(const double* x_dev, const double* y_dev, long long n, double* out_dev);
 /* Out = V[:,0:d] G (G d x p col-major, device); in place allowed for p <= d

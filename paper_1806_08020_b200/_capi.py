@@ -141,6 +141,9 @@ def lib():
             "ppa_ipc_close": [vp],
             "ppa_halo_publish": [vp, C.c_longlong],
             "ppa_halo_pull": [vp, C.c_int, C.c_longlong, vp, C.c_longlong, vp],
+            "ppa_grid2_slab_pass": [C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int,
+                                    C.c_int, C.c_double, C.c_double, C.c_double, vp, vp, vp,
+                                    C.c_int, vp, vp, vp, C.c_longlong, vp],
             "ppa_op_create_callback": [C.c_int, C.c_int, C.c_double, _APPLY_FN, vp,
                                        C.POINTER(vp)],
             "ppa_arnoldi_ritz_vectors": [vp, C.c_int, vp, vp, vp, vp, vp],
@@ -729,6 +732,17 @@ def halo_publish(flag_ptr: int, epoch: int) -> None:
 def halo_pull(peers_ptr: int, npeers: int, max_count: int, x_ext, epoch: int,
               error_ptr: int) -> None:
     _check(lib().ppa_halo_pull(peers_ptr, npeers, max_count, _ptr(x_ext), epoch, error_ptr))
+
+
+def grid2_slab_pass(nd, nx, ny, nz, vals, zo0, zo1, kind, a0, a1, b0, x, y, xl=0, zl0=0,
+                    fl=0, xr=0, fr=0, epoch=0, err=0) -> None:
+    """The sharded box-grid pass with the halo planes read from the
+    neighbours' buffers inside the kernel (ppa_grid2_slab_pass; kind 0: two
+    real roots, 1: a conjugate pair, 2: one real root)."""
+    v = np.ascontiguousarray(vals, dtype=np.float64)
+    _check(lib().ppa_grid2_slab_pass(nd, nx, ny, nz, _np_ptr(v), zo0, zo1, int(kind), a0, a1, b0,
+                                     _ptr(x), _ptr(y), xl or None, zl0, fl or None, xr or None,
+                                     fr or None, epoch, err or None))
 
 
 # ------------------------------------------------------------------ solver --

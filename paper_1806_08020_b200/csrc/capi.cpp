@@ -865,6 +865,27 @@ int ppa_halo_pull(const ppa_peer_halo* peers_dev, int npeers, long long max_coun
   });
 }
 
+int ppa_grid2_slab_pass(int nd, int nx, int ny, int nz, const double* vals, int zo0, int zo1,
+                        int kind, double a0, double a1, double b0, const double* x, double* y,
+                        const double* xl, int zl0, const long long* fl, const double* xr,
+                        const long long* fr, long long epoch, int* err) {
+  return guard([&] {
+    need(vals, "ppa_grid2_slab_pass");
+    need(x, "ppa_grid2_slab_pass");
+    need(y, "ppa_grid2_slab_pass");
+    if (x == y) throw std::invalid_argument("ppa_grid2_slab_pass: x and y must differ");
+    if (kind < 0 || kind > 2) throw std::invalid_argument("ppa_grid2_slab_pass: kind must be 0, 1 or 2");
+    ppa::kern::Mp2Pass m;
+    m.pair = kind == 1;
+    m.one = kind == 2;
+    m.a0 = a0;
+    m.a1 = a1;
+    m.b0 = b0;
+    ppa::kern::spmv_grid2_slab(nd, nx, ny, nz, vals, zo0, zo1, m, x, y, xl, zl0, fl, xr, fr, epoch,
+                               err, ppa::current_context().stream());
+  });
+}
+
 int ppa_cgs_dot_local(const double* V, long long ld, int n, int c, const double* w,
                       double* out) {
   return guard([&] {

@@ -80,6 +80,19 @@ struct G2Params {
   double* y_q;            // the output vector (the kernel's y)
   const double* base_q;   // the complement's base vector (COMPL)
   const double* zeros;  // >= one line of zeros: the copy source of planes outside the box
+  // z-slab mode (the sharded pass, dist.py ShardedGridPoly): this rank owns
+  // the global planes [zo0, zo1); x, y and base hold those planes only (local
+  // plane 0 = global plane zo0).  The halo planes below / above come straight
+  // from the neighbours' buffers xl / xr (their local plane 0 = global planes
+  // zl0 / zo1) once the neighbours' epoch flags fl / fr reach `epoch`.
+  // Unsharded: zo0 = 0, zo1 = nz, no neighbours.
+  int zo0, zo1, zl0;
+  const double* xl;
+  const double* xr;
+  const long long* fl;
+  const long long* fr;
+  long long epoch;
+  int* err;  // set when a neighbour's flag does not arrive (~10 s)
 };
 
 __device__ __forceinline__ void g2_bulk(uint32_t dst, const void* src, uint32_t bytes,
@@ -154,7 +167,7 @@ __device__ __forceinline__ void g2_sts(uint32_t a, double v) {
 // One consumer step t.  Shared memory is addressed with 32-bit shared-window
 // addresses: a block-uniform slot address plus the cell's byte offset, with
 // the +-1 neighbours at immediate offsets.
-template <int ND, int RY, bool PAIR, bool COMPL, int NS>
+template <int ND, int RY, bool PAIR, bool COMPL, int NS, bool ONE>
 __device__ __forceinline__ bool g2_step(
     int t, const G2Geo& G, const G2Cells<RY>& C, const G2Params& P, const double (&v)[7],
     G2Ring& R, uint64_t* x_full, uint64_t* l1_done, int lane, double*& yb, const double*& bb,
@@ -170,7 +183,7 @@ __device__ __forceinline__ bool g2_step(
   mbar_wait(x_full + R.sn, R.pn);
 #pragma unroll
   for (int r = 0; r < RY; ++r) xp[r] = g2_lds<0>(xn + C.aX[r]);
-  if (t >= 2 && q >= 0 && q < G.nz) {
+  if (!ONE && t >= 2 && q >= 0 && q < G.nz) {
     // steady state: wait for level 1 of step t - 1 first, then compute
     // level 1 at plane q and level 2 at plane q - 1 in one block, so the
     // 2 RY row-sum chains interleave (the DADD chains are the latency)
@@ -245,8 +258,14 @@ __device__ __forceinline__ bool g2_step(
         s = g2_sum<5>(v, tt);
       }
       const double u = PAIR ? s : __dadd_rn(x0v[r], __dmul_rn(P.a0, s));
-      ln[r] = C.v1[r] ? u : 0.0;
-      if (C.v1[r]) g2_sts(lw + C.aL[r], u);
+      if constexpr (ONE) {
+        // one factor: level 1 of the tile's planes [za, zb) is the output
+        // (yb points at plane q - 1)
+        if (C.v2[r] && t >= 1 && t <= G.nsteps - 2) yb[G.D + r * cs] = u;
+      } else {
+        ln[r] = C.v1[r] ? u : 0.0;
+        if (C.v1[r]) g2_sts(lw + C.aL[r], u);
+      }
     }
   } else {
 #pragma unroll
@@ -259,7 +278,7 @@ __device__ __forceinline__ bool g2_step(
   if (lane == 0) g2_arrive(l1_done + R.bw);
   // ---- level 2 at plane q - 1: wait until every warp stored level 1 of
   // step t - 1 (this warp's own level-1 work of step t overlapped the wait)
-  if (t >= 2) {
+  if (!ONE && t >= 2) {
     mbar_wait(l1_done + R.br, R.brp);
     const uint32_t lr = R.lr;
 #pragma unroll
@@ -310,7 +329,25 @@ __device__ __forceinline__ bool g2_step(
 // The producer warp: refills the x slot of load index t with load index
 // t + NS once every consumer warp has stored level 1 of step t - 1 (the last
 // reader of that slot, x plane q - 1).
-template <bool D3, int NS>
+// Wait (all lanes of the producer warp, system scope) until a neighbour
+// published the pass that wrote its buffer; then its halo planes may be
+// copied through the async proxy.  Bounded: on timeout the error word is set
+// and the copies go ahead with stale data rather than hanging the consumers.
+__device__ __forceinline__ void g2_peer_wait(const long long* flag, long long epoch, int* err) {
+  long long spins = 0, v;
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+    if (v >= epoch) break;
+    __nanosleep(256);
+    if (++spins > (1LL << 25)) {
+      if (err) atomicExch(err, 1);
+      break;
+    }
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+template <bool D3, int NS, bool SLAB>
 __device__ __forceinline__ void g2_produce(const G2Geo& G, const G2Params& P, char* sb,
                                            uint64_t* x_full, uint64_t* l1_done, int lane,
                                            const double* __restrict__ x, int x0, int xa, int y0,
@@ -328,6 +365,23 @@ __device__ __forceinline__ void g2_produce(const G2Geo& G, const G2Params& P, ch
     const int p = G.za - 2 + i;
     const bool pin = p >= 0 && p < G.nz;
     const int sl_i = i % NS;
+    // the plane's source: this rank's x, a neighbour's buffer (slab mode:
+    // the first halo plane of a pass waits for the neighbour's flag), or the
+    // zero page outside the box
+    const double* pb = P.zeros;
+    if (!SLAB) {
+      if (pin) pb = x + static_cast<long long>(p) * G.D;
+    } else if (pin) {
+      if (p < P.zo0) {
+        if (i == 0 || p == 0) g2_peer_wait(P.fl, P.epoch, P.err);  // first halo plane
+        pb = P.xl + static_cast<long long>(p - P.zl0) * G.D;
+      } else if (p >= P.zo1) {
+        if (p == P.zo1) g2_peer_wait(P.fr, P.epoch, P.err);
+        pb = P.xr + static_cast<long long>(p - P.zo1) * G.D;
+      } else {
+        pb = x + static_cast<long long>(p - P.zo0) * G.D;
+      }
+    }
     if (lane == 0) mbar_expect_tx(x_full + sl_i, plane_bytes);
     __syncwarp();
     for (int yy = ylo + lane; yy < yhi; yy += 32) {
@@ -335,15 +389,14 @@ __device__ __forceinline__ void g2_produce(const G2Geo& G, const G2Params& P, ch
       const uint32_t dst = sbase + 8u * static_cast<uint32_t>(G.xs0 + sl_i * G.slot_x +
                                                                sl * P.P + (xa - (x0 - 2)));
       const double* src =
-          pin ? x + (static_cast<long long>(p) * G.D + static_cast<long long>(yy) * P.nx + xa)
-              : P.zeros;
+          pin ? pb + (static_cast<long long>(yy) * P.nx + xa) : P.zeros;
       g2_bulk(dst, src, line_bytes, smem_u32(x_full + sl_i));
     }
   }
 }
 
 // NT consumer threads plus one producer warp.
-template <int ND, int RY, bool PAIR, bool COMPL, int NT>
+template <int ND, int RY, bool PAIR, bool COMPL, int NT, bool ONE, bool SLAB>
 __global__ void __launch_bounds__(NT + 32, 1)
     k_spmv_grid2(const double* __restrict__ x, double* y, const double* __restrict__ base,
                  G2Params P) {
@@ -371,8 +424,10 @@ __global__ void __launch_bounds__(NT + 32, 1)
   const int y0 = D3 ? ty * ny / P.nty : 0;
   const int y1 = D3 ? (ty + 1) * ny / P.nty : 1;
   G2Geo G;
-  G.za = static_cast<int>(static_cast<long long>(chunk) * nz / P.nchunks);
-  const int zb = static_cast<int>(static_cast<long long>(chunk + 1) * nz / P.nchunks);
+  // chunks of the owned planes [zo0, zo1) (all of [0, nz) unsharded)
+  const int zo0 = SLAB ? P.zo0 : 0, nzo = SLAB ? P.zo1 - P.zo0 : nz;
+  G.za = zo0 + static_cast<int>(static_cast<long long>(chunk) * nzo / P.nchunks);
+  const int zb = zo0 + static_cast<int>(static_cast<long long>(chunk + 1) * nzo / P.nchunks);
   G.nsteps = zb - G.za + 2;  // level-1 planes za-1 .. zb
   G.nz = nz;
   G.D = P.D;
@@ -399,10 +454,10 @@ __global__ void __launch_bounds__(NT + 32, 1)
 
   if (warp == NT / 32) {
     // producer warp: the first NS loads at once, then one refill per step
-    g2_produce<D3, NS>(G, P, sb, x_full, l1_done, lane, x, x0, xa, y0, ylo, yhi, line_bytes,
-                       plane_bytes, 0, min(NS, nload), 0);
-    g2_produce<D3, NS>(G, P, sb, x_full, l1_done, lane, x, x0, xa, y0, ylo, yhi, line_bytes,
-                       plane_bytes, NS, nload, 0);
+    g2_produce<D3, NS, SLAB>(G, P, sb, x_full, l1_done, lane, x, x0, xa, y0, ylo, yhi,
+                             line_bytes, plane_bytes, 0, min(NS, nload), 0);
+    g2_produce<D3, NS, SLAB>(G, P, sb, x_full, l1_done, lane, x, x0, xa, y0, ylo, yhi,
+                             line_bytes, plane_bytes, NS, nload, 0);
     return;
   }
 
@@ -491,7 +546,7 @@ __global__ void __launch_bounds__(NT + 32, 1)
   // output rows of cell 0 at the level-2 plane of step 0 (za - 2; advanced
   // by one plane per step, dereferenced only for level-2 cells); cell r sits
   // cs rows further (3-D: the next grid line, 2-D: the next 32-column segment)
-  const long long row0 = static_cast<long long>(G.za - 2) * G.D + C.row2[0];
+  const long long row0 = static_cast<long long>(G.za - 2 - zo0) * G.D + C.row2[0];
   double* yb = y + row0;
   const double* bb = COMPL ? base + row0 : nullptr;
   const int cs = D3 ? nx : 32;
@@ -527,7 +582,7 @@ __global__ void __launch_bounds__(NT + 32, 1)
   R.br = 2 * NS - 1;
   R.brp = 1;
 #define G2_STEP(XM, X0, XP, LM, LC, LN)                                                     \
-  if (!g2_step<ND, RY, PAIR, COMPL, NS>(t++, G, C, P, v, R, x_full, l1_done, lane, yb, bb, cs, \
+  if (!g2_step<ND, RY, PAIR, COMPL, NS, ONE>(t++, G, C, P, v, R, x_full, l1_done, lane, yb, bb, cs, \
                                         XM, X0, XP, LM, LC, LN)) {                          \
     break;                                                                                  \
   }
@@ -692,10 +747,10 @@ G2Plan g2_plan(int nd, int nx, int ny, int nz) {
   return plan;
 }
 
-template <int ND, int RY, bool PAIR, bool COMPL, int NT>
+template <int ND, int RY, bool PAIR, bool COMPL, int NT, bool ONE, bool SLAB>
 void launch_g2(const G2Params& P, const G2Plan& pl, const double* x, double* y,
                const double* base, cudaStream_t st) {
-  auto kernel = k_spmv_grid2<ND, RY, PAIR, COMPL, NT>;
+  auto kernel = k_spmv_grid2<ND, RY, PAIR, COMPL, NT, ONE, SLAB>;
   // the attribute is per device: set it on every launch (cheap) rather than
   // once per process
   PPA_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -704,7 +759,7 @@ void launch_g2(const G2Params& P, const G2Plan& pl, const double* x, double* y,
              P);
 }
 
-template <int ND, int RY, bool PAIR, bool COMPL>
+template <int ND, int RY, bool PAIR, bool COMPL, bool ONE = false, bool SLAB = false>
 void launch_g2_nt(const G2Params& P, const G2Plan& pl, const double* x, double* y,
                   const double* base, cudaStream_t st) {
   // thread counts in steps of 32 lanes x segments: instantiate the multiples
@@ -713,7 +768,7 @@ void launch_g2_nt(const G2Params& P, const G2Plan& pl, const double* x, double* 
 #define G2_NT(k)                                                     \
   case k:                                                            \
     if constexpr (64 * k <= g2_maxnt(ND, RY)) {                      \
-      return launch_g2<ND, RY, PAIR, COMPL, 64 * k>(P, pl, x, y, base, st); \
+      return launch_g2<ND, RY, PAIR, COMPL, 64 * k, ONE, SLAB>(P, pl, x, y, base, st); \
     }                                                                \
     break;
     G2_NT(1) G2_NT(2) G2_NT(3) G2_NT(4) G2_NT(5) G2_NT(6) G2_NT(7) G2_NT(8) G2_NT(9)
@@ -726,8 +781,16 @@ void launch_g2_nt(const G2Params& P, const G2Plan& pl, const double* x, double* 
 
 template <int ND, int RY>
 void launch_g2_m(const G2Params& P, const G2Plan& pl, bool pair, const double* x, double* y,
-                 const double* base, cudaStream_t st) {
-  if (pair) {
+                 const double* base, cudaStream_t st, bool one = false, bool slab = false) {
+  // slab mode (neighbours' halo planes, owned plane range) and single real
+  // factors have their own instantiations, so the unsharded pass's producer
+  // keeps its plain source computation
+  if (one) {  // a single real factor (the sharded pass's leftovers; no complement)
+    launch_g2_nt<ND, RY, false, false, true, true>(P, pl, x, y, base, st);
+  } else if (slab) {
+    pair ? launch_g2_nt<ND, RY, true, false, false, true>(P, pl, x, y, base, st)
+         : launch_g2_nt<ND, RY, false, false, false, true>(P, pl, x, y, base, st);
+  } else if (pair) {
     base ? launch_g2_nt<ND, RY, true, true>(P, pl, x, y, base, st)
          : launch_g2_nt<ND, RY, true, false>(P, pl, x, y, base, st);
   } else {
@@ -765,19 +828,25 @@ bool grid2_supported(const CsrDevice& a) {
   return g2_plan(a.dia_ndiag, a.grid_nx, a.grid_ny, a.grid_nz).ok != 0;
 }
 
-void spmv_grid2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y,
-                const double* base, cudaStream_t st) {
-  const int nd = a.dia_ndiag;
-  const G2Plan pl = g2_plan(nd, a.grid_nx, a.grid_ny, a.grid_nz);
+namespace {
+
+// One pass over the owned planes [zo0, zo1) of an nx x ny x nz box (ny = 1:
+// 5-point 2-D) with the diagonal values vals; plan for the owned planes.
+void grid2_launch(int nd, int nx, int ny, int nz, const double* vals, const Mp2Pass& p,
+                  const double* x, double* y, const double* base, int zo0, int zo1,
+                  const double* xl, int zl0, const long long* fl, const double* xr,
+                  const long long* fr, long long epoch, int* err, cudaStream_t st) {
+  const G2Plan pl = g2_plan(nd, nx, ny, zo1 - zo0);
+  if (!pl.ok) throw std::invalid_argument("spmv_grid2: no launch plan for this box");
   G2Params P{};
-  for (int j = 0; j < nd; ++j) P.val[j] = a.dia_dflt[j];
+  for (int j = 0; j < nd; ++j) P.val[j] = vals[j];
   P.a0 = p.a0;
   P.a1 = p.a1;
   P.b0 = p.b0;
-  P.nx = a.grid_nx;
-  P.ny = a.grid_ny;
-  P.nz = a.grid_nz;
-  P.D = a.grid_nx * a.grid_ny;
+  P.nx = nx;
+  P.ny = ny;
+  P.nz = nz;
+  P.D = nx * ny;
   P.ntx = pl.ntx;
   P.nty = pl.nty;
   P.nchunks = pl.nchunks;
@@ -788,21 +857,59 @@ void spmv_grid2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y
   P.segs = pl.segs;
   P.zeros = grid2_zeros();
   P.cw = pl.cw;
+  P.zo0 = zo0;
+  P.zo1 = zo1;
+  P.zl0 = zl0;
+  P.xl = xl;
+  P.xr = xr;
+  P.fl = fl;
+  P.fr = fr;
+  P.epoch = epoch;
+  P.err = err;
+  const bool slab = zo0 != 0 || zo1 != nz || xl || xr;
+  if (slab && base) throw std::invalid_argument("spmv_grid2: no complement in slab mode");
   if (nd == 7) {
     switch (pl.ry) {
-      case 2: launch_g2_m<7, 2>(P, pl, p.pair, x, y, base, st); break;
-      case 3: launch_g2_m<7, 3>(P, pl, p.pair, x, y, base, st); break;
-      default: launch_g2_m<7, 4>(P, pl, p.pair, x, y, base, st); break;
+      case 2: launch_g2_m<7, 2>(P, pl, p.pair, x, y, base, st, p.one, slab); break;
+      case 3: launch_g2_m<7, 3>(P, pl, p.pair, x, y, base, st, p.one, slab); break;
+      default: launch_g2_m<7, 4>(P, pl, p.pair, x, y, base, st, p.one, slab); break;
     }
   } else {
     switch (pl.ry) {
-      case 1: launch_g2_m<5, 1>(P, pl, p.pair, x, y, base, st); break;
-      case 2: launch_g2_m<5, 2>(P, pl, p.pair, x, y, base, st); break;
-      case 3: launch_g2_m<5, 3>(P, pl, p.pair, x, y, base, st); break;
-      default: launch_g2_m<5, 4>(P, pl, p.pair, x, y, base, st); break;
+      case 1: launch_g2_m<5, 1>(P, pl, p.pair, x, y, base, st, p.one, slab); break;
+      case 2: launch_g2_m<5, 2>(P, pl, p.pair, x, y, base, st, p.one, slab); break;
+      case 3: launch_g2_m<5, 3>(P, pl, p.pair, x, y, base, st, p.one, slab); break;
+      default: launch_g2_m<5, 4>(P, pl, p.pair, x, y, base, st, p.one, slab); break;
     }
   }
   PPA_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+void spmv_grid2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y,
+                const double* base, cudaStream_t st) {
+  grid2_launch(a.dia_ndiag, a.grid_nx, a.grid_ny, a.grid_nz, a.dia_dflt, p, x, y, base, 0,
+               a.grid_nz, nullptr, 0, nullptr, nullptr, nullptr, 0, nullptr, st);
+}
+
+void spmv_grid2_slab(int nd, int nx, int ny, int nz, const double* vals, int zo0, int zo1,
+                     const Mp2Pass& p, const double* x, double* y, const double* xl, int zl0,
+                     const long long* fl, const double* xr, const long long* fr,
+                     long long epoch, int* err, cudaStream_t st) {
+  if (nd != 5 && nd != 7) throw std::invalid_argument("spmv_grid2_slab: 5- or 7-point stencil");
+  if ((nd == 5) != (ny == 1)) throw std::invalid_argument("spmv_grid2_slab: 2-D boxes have ny = 1");
+  if (zo0 < 0 || zo1 > nz || zo1 - zo0 < 2) {
+    throw std::invalid_argument("spmv_grid2_slab: a slab needs >= 2 planes inside the box");
+  }
+  if ((zo0 > 0 && (!xl || !fl || zo0 - zl0 < 2)) || (zo1 < nz && (!xr || !fr))) {
+    throw std::invalid_argument("spmv_grid2_slab: missing neighbour buffer or flag");
+  }
+  if (static_cast<long long>(nx) * ny * (zo1 - zo0) + 4LL * nx * ny >= (1LL << 31)) {
+    throw std::invalid_argument("spmv_grid2_slab: slab too large");
+  }
+  grid2_launch(nd, nx, ny, nz, vals, p, x, y, nullptr, zo0, zo1, xl, zl0, fl, xr, fr, epoch,
+               err, st);
 }
 
 }  // namespace kern

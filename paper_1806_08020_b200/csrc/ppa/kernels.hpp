@@ -110,6 +110,7 @@ inline double packed_entry_bytes(int ndict) { return 2.0 + (ndict > 0 ? 1.0 : 8.
 struct Mp2Pass {
   bool pair = false;
   double a0 = 0.0, a1 = 0.0, b0 = 0.0;
+  bool one = false;  // box-grid slab pass only: a single real factor y = x + a0 (A x)
 };
 
 /// True when two factors can run as one temporally blocked pass over the
@@ -126,6 +127,16 @@ const double* grid2_zeros();
 /// The box-grid two-factor pass (same contract as spmv_dia2).
 void spmv_grid2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y,
                 const double* base, cudaStream_t st);
+/// The box-grid pass over one rank's z-slab (planes [zo0, zo1) of an
+/// nx x ny x nz box; ny = 1 for the 2-D 5-point form), the halo planes read
+/// by the kernel straight from the neighbours' buffers xl (local plane 0 =
+/// global plane zl0) and xr (local plane 0 = global plane zo1) after their
+/// 64-bit epoch flags fl / fr reach `epoch` (dist.py ShardedGridPoly).
+/// x and y hold the owned planes only.  *err is set if a flag never arrives.
+void spmv_grid2_slab(int nd, int nx, int ny, int nz, const double* vals, int zo0, int zo1,
+                     const Mp2Pass& p, const double* x, double* y, const double* xl, int zl0,
+                     const long long* fl, const double* xr, const long long* fr,
+                     long long epoch, int* err, cudaStream_t st);
 /// One two-factor pass (Mp2Pass semantics, y2 only; t / y1 never stored).
 /// x and y distinct and 16-byte aligned; `base` folds the complement.
 void spmv_dia2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y,

@@ -381,6 +381,146 @@ class ShardedPoly:
         return cur[p.owned]
 
 
+# ------------------------------------------- sharded box-grid pass (fused) --
+# Box-grid stencils (configs 2, 3, 5) split into z-slabs, two polynomial
+# factors per pass (one where the plan leaves a real root alone), the halo
+# exchange inside the pass kernel: the producer
+# warp of rank q's box-grid pass (kernels/spmv_grid2.cu, slab mode) copies the
+# two planes below its slab straight from rank q-1's buffer and the two above
+# from rank q+1's, over NVLink through CUDA IPC mappings, after an acquire
+# wait on that neighbour's epoch flag.  No collective, no pull kernel and no
+# x_ext staging per pass; each rank moves 16 n_local bytes per two factors
+# plus 4 halo planes.
+#
+# Epochs: every rank publishes epoch e after the kernel that made its
+# vector x_e ready (the copy of v, then one publish per pass), in the same
+# order on every rank, so "neighbour flag >= e" means "x_e is complete and
+# every pass before it, including its reads of my buffers, has finished".
+# Pass k reads the neighbours' x_k (the pass waits for it); it overwrites my
+# x_{k-1} buffer, which the neighbours read during their pass k-1, only in
+# the planes they read after its own wait on their x_k, which they publish
+# after finishing pass k-1.  A new product first waits for the neighbours'
+# last publish of the previous one before it overwrites x_0.
+
+
+def partition_planes(nz: int, world: int) -> List[Tuple[int, int]]:
+    """Contiguous plane blocks (sizes differing by at most one), each with
+    >= 2 planes: a neighbour's two halo planes then belong to one rank."""
+    if world < 1:
+        raise ValueError("partition_planes: world must be >= 1")
+    if nz < 2 * world:
+        raise ValueError("partition_planes: every slab needs >= 2 planes")
+    return partition_rows(nz, world)
+
+
+GRID_TWO_REAL, GRID_PAIR, GRID_ONE_REAL = 0, 1, 2
+
+
+def grid_passes(plan) -> List[Tuple[int, float, float, float]]:
+    """Passes (kind, a0, a1, b0) of a factor plan in apply_poly's order
+    (src/gmres_poly.cpp:129-143): a conjugate pair is one pass (kind 1), two
+    consecutive real roots one pass (kind 0), a real root followed by a pair
+    or by nothing a one-level pass (kind 2) - the grouping of the single-GPU
+    chain (gmres_poly.cpp apply_poly_csr)."""
+    out, k = [], 0
+    while k < len(plan):
+        pair, c0, c1 = plan[k]
+        if pair:
+            out.append((GRID_PAIR, c0, c1, 0.0))
+            k += 1
+        elif k + 1 < len(plan) and not plan[k + 1][0]:
+            out.append((GRID_TWO_REAL, c0, 0.0, plan[k + 1][1]))
+            k += 2
+        else:
+            out.append((GRID_ONE_REAL, c0, 0.0, 0.0))
+            k += 1
+    return out
+
+
+class ShardedGridPoly:
+    """pi(A) v for an nx x ny x nz box stencil (ny = 1: 5-point 2-D) split
+    into z-slabs, one per rank, with the halo exchange fused into the pass
+    kernel (collective constructor; CUDA, one GPU per rank).
+
+    `vals` are the nd diagonal values in increasing offset (nd = 7 in 3-D,
+    5 in 2-D).  apply(roots, v_local) takes and returns the owned planes."""
+
+    def __init__(self, nx: int, ny: int, nz: int, vals, dist, group=None):
+        import torch
+
+        from . import _capi as C
+
+        self.C, self.torch, self.dist, self.group = C, torch, dist, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.nx, self.ny, self.nz = nx, ny, nz
+        self.nd = 7 if ny > 1 else 5
+        self.vals = np.ascontiguousarray(vals, dtype=np.float64)
+        if self.vals.size != self.nd:
+            raise ValueError(f"ShardedGridPoly: {self.nd} diagonal values expected")
+        self.ranges = partition_planes(nz, self.world)
+        self.z0, self.z1 = self.ranges[self.rank]
+        self.D = nx * ny
+        self.n_local = (self.z1 - self.z0) * self.D
+        self.bufs = [C.dev_alloc(8 * self.n_local) for _ in range(2)]
+        self.flag = C.dev_alloc(64)
+        self.err = C.dev_alloc(16)
+        self.views = [_device_view(torch, b, self.n_local) for b in self.bufs]
+        mine = {"bufs": [C.ipc_get_handle(b) for b in self.bufs],
+                "flag": C.ipc_get_handle(self.flag)}
+        everyone: List[Optional[dict]] = [None] * self.world
+        dist.all_gather_object(everyone, mine, group=group)
+        self.opened = []
+        self.nb = {}
+        for side, q in (("left", self.rank - 1), ("right", self.rank + 1)):
+            if 0 <= q < self.world:
+                bufs = [C.ipc_open(h) for h in everyone[q]["bufs"]]
+                flag = C.ipc_open(everyone[q]["flag"])
+                self.opened += bufs + [flag]
+                self.nb[side] = (bufs, flag, self.ranges[q][0])
+        # the neighbours' flags as wait-only halo descriptors (the fence of a
+        # new product)
+        descs = [(0, 0, 0, 0, nb[1]) for nb in self.nb.values()]
+        arr = np.array(descs, dtype=_DESC) if descs else np.zeros(1, dtype=_DESC)
+        self.fence_desc = torch.as_tensor(arr.view(np.uint8), device="cuda")
+        self.epoch = 0
+
+    def _publish(self) -> None:
+        self.epoch += 1
+        self.C.halo_publish(self.flag, self.epoch)
+
+    def apply(self, roots, v_local):
+        C = self.C
+        passes = grid_passes(C.factor_plan(roots))
+        if self.nb:
+            # the neighbours finished every pass of the previous product
+            C.halo_pull(self.fence_desc.data_ptr(), len(self.nb), 0, None, self.epoch, self.err)
+        self.views[0].copy_(v_local)
+        self._publish()
+        left, right = self.nb.get("left"), self.nb.get("right")
+        for k, (kind, a0, a1, b0) in enumerate(passes):
+            x, y = self.bufs[k % 2], self.bufs[(k + 1) % 2]
+            C.grid2_slab_pass(self.nd, self.nx, self.ny, self.nz, self.vals, self.z0, self.z1,
+                              kind, a0, a1, b0, x, y,
+                              xl=left[0][k % 2] if left else 0, zl0=left[2] if left else 0,
+                              fl=left[1] if left else 0,
+                              xr=right[0][k % 2] if right else 0, fr=right[1] if right else 0,
+                              epoch=self.epoch, err=self.err)
+            self._publish()
+        return self.views[len(passes) % 2]
+
+    def check(self) -> None:
+        """Raises if a neighbour's flag never arrived during a pass."""
+        e = self.torch.empty(1, dtype=self.torch.int32, device="cuda")
+        e.copy_(_device_view(self.torch, self.err, 1, self.torch.int32))
+        if int(e.item()):
+            raise RuntimeError("ShardedGridPoly: a neighbour's epoch flag never arrived")
+
+    def close(self) -> None:
+        for p in self.opened:
+            self.C.ipc_close(p)
+        self.opened = []
+
+
 # ------------------------------------------------------------ sharded solve --
 # Thick-restarted Arnoldi with the Krylov basis sharded by rows.  Every
 # reduction (CGS2 coefficients, norms, Rayleigh quotients, residuals) is a
