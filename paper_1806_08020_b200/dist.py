@@ -116,12 +116,17 @@ class HaloPlan:
                 vals, recv, wants)
 
     @classmethod
-    def build(cls, row_ptr, col_idx, values, n: int, dist, group=None) -> "HaloPlan":
+    def build(cls, row_ptr, col_idx, values, n: int, dist, group=None,
+              ranges=None) -> "HaloPlan":
         """Collective: every rank calls it with the matrix rows it owns
-        (the arrays may hold the whole matrix; only the owned rows are read)."""
+        (the arrays may hold the whole matrix; only the owned rows are read).
+        `ranges` overrides the row partition (e.g. box_row_ranges, so that the
+        rows match a ShardedGridPoly's z-slabs)."""
         world = dist.get_world_size(group)
         rank = dist.get_rank(group)
-        ranges = partition_rows(n, world)
+        ranges = list(ranges) if ranges is not None else partition_rows(n, world)
+        if len(ranges) != world or ranges[0][0] != 0 or ranges[-1][1] != n:
+            raise ValueError("HaloPlan.build: ranges must partition [0, n) over the ranks")
         (n_left, n_local, n_right, lrp, lci, vals, recv, wants) = cls.local_part(
             row_ptr, col_idx, values, ranges, rank)
         # tell each owner which of its columns this rank needs
@@ -416,6 +421,12 @@ def partition_planes(nz: int, world: int) -> List[Tuple[int, int]]:
 GRID_TWO_REAL, GRID_PAIR, GRID_ONE_REAL = 0, 1, 2
 
 
+def box_row_ranges(nx: int, ny: int, nz: int, world: int) -> List[Tuple[int, int]]:
+    """The row blocks of ShardedGridPoly's z-slabs (for HaloPlan.build)."""
+    D = nx * ny
+    return [(z0 * D, z1 * D) for z0, z1 in partition_planes(nz, world)]
+
+
 def grid_passes(plan) -> List[Tuple[int, float, float, float]]:
     """Passes (kind, a0, a1, b0) of a factor plan in apply_poly's order
     (src/gmres_poly.cpp:129-143): a conjugate pair is one pass (kind 1), two
@@ -577,7 +588,12 @@ class ShardedSolver:
     ts_combine on the local rows; norms and Rayleigh quotients are local dots
     plus an all-reduce."""
 
-    def __init__(self, plan: HaloPlan, backend, dist, group=None, peer: bool = False):
+    def __init__(self, plan: HaloPlan, backend, dist, group=None, peer: bool = False,
+                 grid: Optional["ShardedGridPoly"] = None):
+        """grid: a ShardedGridPoly over the same rows (plan built with
+        box_row_ranges): the polynomial operator then runs as fused-halo
+        box-grid passes; single SpMVs (polynomial build, residual checks)
+        stay on the plan's exchange."""
         import torch
 
         self.torch = torch
@@ -586,6 +602,11 @@ class ShardedSolver:
         self.dist = dist
         self.group = group
         self.sp = ShardedPoly(plan, backend, dist, group, peer=peer)
+        self.grid = grid
+        if grid is not None and (grid.z0 * grid.D, grid.z1 * grid.D) != tuple(
+                plan.ranges[plan.rank]):
+            raise ValueError("ShardedSolver: the grid's slab and the plan's rows differ "
+                             "(build the plan with box_row_ranges)")
         self.mvps = 0
 
     # -- reductions ----------------------------------------------------------
@@ -618,6 +639,8 @@ class ShardedSolver:
         if self.roots is None:
             return self._spmv(x)
         self.mvps += len(self.roots)
+        if self.grid is not None:
+            return self.grid.apply(self.roots, x).clone()
         return self.sp.apply(self.roots, x).clone()
 
     # -- Arnoldi -------------------------------------------------------------

@@ -160,3 +160,42 @@ def test_sharded_grid_poly_ws1(cuda):
         sg.close()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sharded_solve_on_grid_slabs_ws1(cuda):
+    # the sharded solve with its polynomial operator on the fused-halo slab
+    # pass reproduces the same solve on the plan's exchange exactly (both
+    # pi(A)v paths are bit-identical to the unsharded product)
+    import torch.distributed as dist
+
+    import paper_1806_08020_b200 as ppa
+    from paper_1806_08020_b200.dist import (CudaBackend, HaloPlan, ShardedGridPoly,
+                                            ShardedSolver, box_row_ranges)
+
+    if not dist.is_initialized():
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()), RANK="0",
+                          WORLD_SIZE="1")
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        N = 24
+        P = ppa.CsrMatrix.laplacian_3d(N)
+        n = P.n
+        rp, ci, va = P.arrays()
+        mid = ((N // 2) * N + N // 2) * N + N // 2  # an interior row: its 7 values in order
+        vals = [float(t) for t in va[rp[mid]:rp[mid + 1]]]
+        plan = HaloPlan.build(rp, ci, va, n, dist, ranges=box_row_ranges(N, N, N, 1))
+        vec = lambda s: torch.tensor(ppa.normal_vector(n, 2, s), device="cuda")
+        out = []
+        for grid in (None, ShardedGridPoly(N, N, N, vals, dist)):
+            sol = ShardedSolver(plan, CudaBackend(plan), dist, grid=grid)
+            out.append(sol.solve(vec(2), vec(3), vec(1), 40, 20, 15, degree=20, max_cycles=60))
+            if grid is not None:
+                grid.check()
+                grid.close()
+        a, b = out
+        assert a["converged"] and b["converged"]
+        assert a["cycles"] == b["cycles"] and a["mvps"] == b["mvps"]
+        assert np.array_equal(np.asarray(a["eigenvalues"]), np.asarray(b["eigenvalues"]))
+    finally:
+        dist.destroy_process_group()
