@@ -588,9 +588,23 @@ def run_sharded(args):
     n, nnz, _ = csr.info()
     bspmv = 12.0 * nnz + 4.0 * (n + 1) + 16.0 * n
     roots, _ = load_golden_poly()
-    plan = HaloPlan.build(*csr.arrays(), n, dist)
-    sp = ShardedPoly(plan, CudaBackend(plan), dist, peer=args.peer)
-    r0, r1 = plan.ranges[rank]
+    if args.grid:
+        # z-slabs, halo planes copied by the pass kernel from the neighbours'
+        # buffers (dist.ShardedGridPoly)
+        from paper_1806_08020_b200.dist import ShardedGridPoly, box_row_ranges
+
+        rp, ci, va = csr.arrays()
+        mid = (80 * 160 + 80) * 160 + 80  # an interior row: the 7 diagonal values in order
+        sp = ShardedGridPoly(160, 160, 160, [float(t) for t in va[rp[mid]:rp[mid + 1]]], dist)
+        r0, r1 = box_row_ranges(160, 160, 160, ws)[rank]
+        halo_rows = 4 * 160 * 160
+        halo = "fused: the pass kernel copies the neighbours' halo planes (CUDA IPC, epoch flags)"
+    else:
+        plan = HaloPlan.build(*csr.arrays(), n, dist)
+        sp = ShardedPoly(plan, CudaBackend(plan), dist, peer=args.peer)
+        r0, r1 = plan.ranges[rank]
+        halo_rows = plan.n_left + plan.n_right
+        halo = "peer memory (CUDA IPC, epoch flags)" if args.peer else "NCCL point-to-point"
     v = torch.tensor(ppa.normal_vector(n, 2, ppa.STREAM_ARNOLDI)[r0:r1], device="cuda")
     for _ in range(max(args.warmup, 3)):
         sp.apply(roots, v)
@@ -610,9 +624,7 @@ def run_sharded(args):
             "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
             "dtype": "f64", "data": "synthetic (seeded generator; BASELINE config 3)",
             "config": {"workload": "config3-laplace3d-160^3-pi(A)v", "parallelism": f"rowblock{ws}",
-                       "halo_rows_per_rank": plan.n_left + plan.n_right,
-                       "halo": "peer memory (CUDA IPC, epoch flags)" if args.peer
-                               else "NCCL point-to-point"},
+                       "halo_rows_per_rank": halo_rows, "halo": halo},
         }), flush=True)
     dist.destroy_process_group()
 
@@ -627,6 +639,8 @@ def main():
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="strong-scaling row-block sharded pi(A)v (dist.py) instead of replicas")
+    ap.add_argument("--grid", action="store_true",
+                    help="with --sharded: z-slab box-grid passes with the halo fused into the kernel")
     ap.add_argument("--peer", action="store_true",
                     help="with --sharded: halos over peer memory (dist.PeerHalo) instead of NCCL")
     args = ap.parse_args()

@@ -282,12 +282,28 @@ int ppa_halo_pull(const ppa_peer_halo* peers_dev, int npeers, long long max_coun
    plane 0 = global plane zo1) once the neighbours' flags (fl_dev, fr_dev,
    IPC pointers from ppa_halo_publish's protocol) reach `epoch`; *err_dev = 1
    if a flag never arrives (~10 s).  Pointers of absent neighbours (zo0 = 0,
-   zo1 = nz) may be NULL.  Bit-identical to the unsharded pass. */
+   zo1 = nz) may be NULL.  own_dev (the caller's flag: two zero-initialised
+   64-bit words, flag and ticket counter) non-NULL: the pass's last CTA
+   publishes epoch + 1 into it (system-scope release; no ppa_halo_publish
+   launch per pass).  Bit-identical to the unsharded pass. */
 int ppa_grid2_slab_pass(int nd, int nx, int ny, int nz, const double* vals, int zo0, int zo1,
                         int kind, double a0, double a1, double b0, const double* x_dev,
                         double* y_dev, const double* xl_dev, int zl0, const long long* fl_dev,
                         const double* xr_dev, const long long* fr_dev, long long epoch,
-                        int* err_dev);
+                        int* err_dev, long long* own_dev);
+/* The whole chain of one sharded pi(A)v in one call: pass k runs
+   ppa_grid2_slab_pass(kinds[k], a0[k], a1[k], b0[k]) from role k % 2 to role
+   (k + 1) % 2 of the caller's two buffers (buf0, buf1), reading the
+   neighbours' buffers of the same role (xl0/xl1, xr0/xr1), waiting for
+   epoch0 + k and publishing epoch0 + k + 1 into own_dev.  *out_role = the
+   role holding the result. */
+int ppa_grid2_slab_chain(int nd, int nx, int ny, int nz, const double* vals, int zo0, int zo1,
+                         int npass, const int* kinds, const double* a0, const double* a1,
+                         const double* b0, double* buf0_dev, double* buf1_dev,
+                         const double* xl0_dev, const double* xl1_dev, int zl0,
+                         const long long* fl_dev, const double* xr0_dev, const double* xr1_dev,
+                         const long long* fr_dev, long long epoch0, int* err_dev,
+                         long long* own_dev, int* out_role);
 /* out_dev[0] = x . y, deterministic (dot, inc/cost.hpp:51-57) */
 int ppa_dot_local(const double* x_dev, const double* y_dev, long long n, double* out_dev);
 /* Out = V[:,0:d] G (G d x p col-major, device); in place allowed for p <= d

@@ -141,9 +141,12 @@ def lib():
             "ppa_ipc_close": [vp],
             "ppa_halo_publish": [vp, C.c_longlong],
             "ppa_halo_pull": [vp, C.c_int, C.c_longlong, vp, C.c_longlong, vp],
+            "ppa_grid2_slab_chain": [C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int,
+                                     C.c_int, _ip, vp, vp, vp, vp, vp, vp, vp, C.c_int, vp, vp,
+                                     vp, vp, C.c_longlong, vp, vp, _ip],
             "ppa_grid2_slab_pass": [C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int,
                                     C.c_int, C.c_double, C.c_double, C.c_double, vp, vp, vp,
-                                    C.c_int, vp, vp, vp, C.c_longlong, vp],
+                                    C.c_int, vp, vp, vp, C.c_longlong, vp, vp],
             "ppa_op_create_callback": [C.c_int, C.c_int, C.c_double, _APPLY_FN, vp,
                                        C.POINTER(vp)],
             "ppa_arnoldi_ritz_vectors": [vp, C.c_int, vp, vp, vp, vp, vp],
@@ -735,14 +738,32 @@ def halo_pull(peers_ptr: int, npeers: int, max_count: int, x_ext, epoch: int,
 
 
 def grid2_slab_pass(nd, nx, ny, nz, vals, zo0, zo1, kind, a0, a1, b0, x, y, xl=0, zl0=0,
-                    fl=0, xr=0, fr=0, epoch=0, err=0) -> None:
+                    fl=0, xr=0, fr=0, epoch=0, err=0, own=0) -> None:
     """The sharded box-grid pass with the halo planes read from the
     neighbours' buffers inside the kernel (ppa_grid2_slab_pass; kind 0: two
     real roots, 1: a conjugate pair, 2: one real root)."""
     v = np.ascontiguousarray(vals, dtype=np.float64)
     _check(lib().ppa_grid2_slab_pass(nd, nx, ny, nz, _np_ptr(v), zo0, zo1, int(kind), a0, a1, b0,
                                      _ptr(x), _ptr(y), xl or None, zl0, fl or None, xr or None,
-                                     fr or None, epoch, err or None))
+                                     fr or None, epoch, err or None, own or None))
+
+
+def grid2_slab_chain(nd, nx, ny, nz, vals, zo0, zo1, passes, buf0, buf1, xl=(0, 0), zl0=0,
+                     fl=0, xr=(0, 0), fr=0, epoch0=0, err=0, own=0) -> int:
+    """All passes [(kind, a0, a1, b0), ...] of one sharded pi(A)v in one call
+    (ppa_grid2_slab_chain); returns the role (0, 1) holding the result."""
+    v = np.ascontiguousarray(vals, dtype=np.float64)
+    k = len(passes)
+    kinds = np.array([p[0] for p in passes] or [0], dtype=np.int32)
+    a0, a1, b0 = (np.array([p[i] for p in passes] or [0.0], dtype=np.float64) for i in (1, 2, 3))
+    role = C.c_int()
+    _check(lib().ppa_grid2_slab_chain(nd, nx, ny, nz, _np_ptr(v), zo0, zo1, k,
+                                      kinds.ctypes.data_as(_ip), _np_ptr(a0), _np_ptr(a1),
+                                      _np_ptr(b0), _ptr(buf0), _ptr(buf1), xl[0] or None,
+                                      xl[1] or None, zl0, fl or None, xr[0] or None,
+                                      xr[1] or None, fr or None, epoch0, err or None, own or None,
+                                      C.byref(role)))
+    return role.value
 
 
 # ------------------------------------------------------------------ solver --

@@ -868,7 +868,7 @@ int ppa_halo_pull(const ppa_peer_halo* peers_dev, int npeers, long long max_coun
 int ppa_grid2_slab_pass(int nd, int nx, int ny, int nz, const double* vals, int zo0, int zo1,
                         int kind, double a0, double a1, double b0, const double* x, double* y,
                         const double* xl, int zl0, const long long* fl, const double* xr,
-                        const long long* fr, long long epoch, int* err) {
+                        const long long* fr, long long epoch, int* err, long long* own) {
   return guard([&] {
     need(vals, "ppa_grid2_slab_pass");
     need(x, "ppa_grid2_slab_pass");
@@ -882,7 +882,47 @@ int ppa_grid2_slab_pass(int nd, int nx, int ny, int nz, const double* vals, int 
     m.a1 = a1;
     m.b0 = b0;
     ppa::kern::spmv_grid2_slab(nd, nx, ny, nz, vals, zo0, zo1, m, x, y, xl, zl0, fl, xr, fr, epoch,
-                               err, ppa::current_context().stream());
+                               err, own, ppa::current_context().stream());
+  });
+}
+
+int ppa_grid2_slab_chain(int nd, int nx, int ny, int nz, const double* vals, int zo0, int zo1,
+                         int npass, const int* kinds, const double* a0, const double* a1,
+                         const double* b0, double* buf0, double* buf1, const double* xl0,
+                         const double* xl1, int zl0, const long long* fl, const double* xr0,
+                         const double* xr1, const long long* fr, long long epoch0, int* err,
+                         long long* own, int* out_role) {
+  return guard([&] {
+    need(vals, "ppa_grid2_slab_chain");
+    need(buf0, "ppa_grid2_slab_chain");
+    need(buf1, "ppa_grid2_slab_chain");
+    need(out_role, "ppa_grid2_slab_chain");
+    if (npass < 0) throw std::invalid_argument("ppa_grid2_slab_chain: negative pass count");
+    if (npass > 0) {
+      need(kinds, "ppa_grid2_slab_chain");
+      need(a0, "ppa_grid2_slab_chain");
+      need(a1, "ppa_grid2_slab_chain");
+      need(b0, "ppa_grid2_slab_chain");
+    }
+    double* buf[2] = {buf0, buf1};
+    const double* xl[2] = {xl0, xl1};
+    const double* xr[2] = {xr0, xr1};
+    const cudaStream_t st = ppa::current_context().stream();
+    for (int k = 0; k < npass; ++k) {
+      if (kinds[k] < 0 || kinds[k] > 2) {
+        throw std::invalid_argument("ppa_grid2_slab_chain: kind must be 0, 1 or 2");
+      }
+      ppa::kern::Mp2Pass m;
+      m.pair = kinds[k] == 1;
+      m.one = kinds[k] == 2;
+      m.a0 = a0[k];
+      m.a1 = a1[k];
+      m.b0 = b0[k];
+      const int r = k & 1;
+      ppa::kern::spmv_grid2_slab(nd, nx, ny, nz, vals, zo0, zo1, m, buf[r], buf[r ^ 1], xl[r], zl0,
+                                 fl, xr[r], fr, epoch0 + k, err, own, st);
+    }
+    *out_role = npass & 1;
   });
 }
 

@@ -93,6 +93,9 @@ struct G2Params {
   const long long* fr;
   long long epoch;
   int* err;  // set when a neighbour's flag does not arrive (~10 s)
+  // this rank's flag (word 0) and pass ticket counter (word 1): the last
+  // CTA of the pass publishes epoch + 1 (nullptr: no publish)
+  long long* own;
 };
 
 __device__ __forceinline__ void g2_bulk(uint32_t dst, const void* src, uint32_t bytes,
@@ -592,6 +595,37 @@ __global__ void __launch_bounds__(NT + 32, 1)
     G2_STEP(xc_, xa_, xb_, lcc, la, lb)
   }
 #undef G2_STEP
+  if constexpr (SLAB) {
+    // publish the pass: every consumer's stores, then a device-scope fence
+    // per CTA and a ticket; the CTA that completes the grid's count has
+    // observed every CTA's stores through the tickets and releases epoch + 1
+    // into this rank's flag at system scope (cumulative; no publish launch)
+    // Only CTAs whose chunk reads a neighbour's planes or writes planes a
+    // neighbour reads (within two planes of a shared slab face) take part;
+    // the others exit at once (the next pass on this rank is stream-ordered).
+    auto touches = [&](int a, int b) {
+      return (P.zo0 > 0 && a < P.zo0 + 2) || (P.zo1 < nz && b > P.zo1 - 2);
+    };
+    if (P.own && touches(G.za, zb)) {
+      int parts = 0;  // participating CTAs (every tile of a touching chunk)
+      for (int c = 0; c < P.nchunks; ++c) {
+        const int a = zo0 + static_cast<int>(static_cast<long long>(c) * nzo / P.nchunks);
+        const int b = zo0 + static_cast<int>(static_cast<long long>(c + 1) * nzo / P.nchunks);
+        parts += touches(a, b) ? P.ntx * P.nty : 0;
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory");
+      if (tid == 0) {
+        __threadfence();
+        const unsigned long long tk =
+            atomicAdd(reinterpret_cast<unsigned long long*>(P.own + 1), 1ull);
+        if ((tk + 1) % static_cast<unsigned long long>(parts) == 0) {
+          asm volatile("fence.acq_rel.sys;" ::: "memory");
+          asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(P.own), "l"(P.epoch + 1)
+                       : "memory");
+        }
+      }
+    }
+  }
 }
 
 // ------------------------------------------------------------------ host --
@@ -835,7 +869,8 @@ namespace {
 void grid2_launch(int nd, int nx, int ny, int nz, const double* vals, const Mp2Pass& p,
                   const double* x, double* y, const double* base, int zo0, int zo1,
                   const double* xl, int zl0, const long long* fl, const double* xr,
-                  const long long* fr, long long epoch, int* err, cudaStream_t st) {
+                  const long long* fr, long long epoch, int* err, long long* own,
+                  cudaStream_t st) {
   const G2Plan pl = g2_plan(nd, nx, ny, zo1 - zo0);
   if (!pl.ok) throw std::invalid_argument("spmv_grid2: no launch plan for this box");
   G2Params P{};
@@ -866,7 +901,8 @@ void grid2_launch(int nd, int nx, int ny, int nz, const double* vals, const Mp2P
   P.fr = fr;
   P.epoch = epoch;
   P.err = err;
-  const bool slab = zo0 != 0 || zo1 != nz || xl || xr;
+  P.own = own;
+  const bool slab = zo0 != 0 || zo1 != nz || xl || xr || own;
   if (slab && base) throw std::invalid_argument("spmv_grid2: no complement in slab mode");
   if (nd == 7) {
     switch (pl.ry) {
@@ -890,13 +926,13 @@ void grid2_launch(int nd, int nx, int ny, int nz, const double* vals, const Mp2P
 void spmv_grid2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y,
                 const double* base, cudaStream_t st) {
   grid2_launch(a.dia_ndiag, a.grid_nx, a.grid_ny, a.grid_nz, a.dia_dflt, p, x, y, base, 0,
-               a.grid_nz, nullptr, 0, nullptr, nullptr, nullptr, 0, nullptr, st);
+               a.grid_nz, nullptr, 0, nullptr, nullptr, nullptr, 0, nullptr, nullptr, st);
 }
 
 void spmv_grid2_slab(int nd, int nx, int ny, int nz, const double* vals, int zo0, int zo1,
                      const Mp2Pass& p, const double* x, double* y, const double* xl, int zl0,
                      const long long* fl, const double* xr, const long long* fr,
-                     long long epoch, int* err, cudaStream_t st) {
+                     long long epoch, int* err, long long* own, cudaStream_t st) {
   if (nd != 5 && nd != 7) throw std::invalid_argument("spmv_grid2_slab: 5- or 7-point stencil");
   if ((nd == 5) != (ny == 1)) throw std::invalid_argument("spmv_grid2_slab: 2-D boxes have ny = 1");
   if (zo0 < 0 || zo1 > nz || zo1 - zo0 < 2) {
@@ -909,7 +945,7 @@ void spmv_grid2_slab(int nd, int nx, int ny, int nz, const double* vals, int zo0
     throw std::invalid_argument("spmv_grid2_slab: slab too large");
   }
   grid2_launch(nd, nx, ny, nz, vals, p, x, y, nullptr, zo0, zo1, xl, zl0, fl, xr, fr, epoch,
-               err, st);
+               err, own, st);
 }
 
 }  // namespace kern

@@ -133,10 +133,12 @@ void spmv_grid2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y
 /// global plane zl0) and xr (local plane 0 = global plane zo1) after their
 /// 64-bit epoch flags fl / fr reach `epoch` (dist.py ShardedGridPoly).
 /// x and y hold the owned planes only.  *err is set if a flag never arrives.
+/// own (this rank's flag, 2 words: flag, ticket counter) non-null: the
+/// pass's last CTA publishes epoch + 1 into it (system-scope release).
 void spmv_grid2_slab(int nd, int nx, int ny, int nz, const double* vals, int zo0, int zo1,
                      const Mp2Pass& p, const double* x, double* y, const double* xl, int zl0,
                      const long long* fl, const double* xr, const long long* fr,
-                     long long epoch, int* err, cudaStream_t st);
+                     long long epoch, int* err, long long* own, cudaStream_t st);
 /// One two-factor pass (Mp2Pass semantics, y2 only; t / y1 never stored).
 /// x and y distinct and 16-byte aligned; `base` folds the complement.
 void spmv_dia2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y,

@@ -397,9 +397,10 @@ class ShardedPoly:
 # x_ext staging per pass; each rank moves 16 n_local bytes per two factors
 # plus 4 halo planes.
 #
-# Epochs: every rank publishes epoch e after the kernel that made its
-# vector x_e ready (the copy of v, then one publish per pass), in the same
-# order on every rank, so "neighbour flag >= e" means "x_e is complete and
+# Epochs: every rank publishes epoch e once its vector x_e is ready (after the
+# copy of v with ppa_halo_publish, then from inside each pass: its last CTA,
+# found by a ticket counter, fences system-wide and releases the flag), in the
+# same order on every rank, so "neighbour flag >= e" means "x_e is complete and
 # every pass before it, including its reads of my buffers, has finished".
 # Pass k reads the neighbours' x_k (the pass waits for it); it overwrites my
 # x_{k-1} buffer, which the neighbours read during their pass k-1, only in
@@ -508,16 +509,17 @@ class ShardedGridPoly:
         self.views[0].copy_(v_local)
         self._publish()
         left, right = self.nb.get("left"), self.nb.get("right")
-        for k, (kind, a0, a1, b0) in enumerate(passes):
-            x, y = self.bufs[k % 2], self.bufs[(k + 1) % 2]
-            C.grid2_slab_pass(self.nd, self.nx, self.ny, self.nz, self.vals, self.z0, self.z1,
-                              kind, a0, a1, b0, x, y,
-                              xl=left[0][k % 2] if left else 0, zl0=left[2] if left else 0,
-                              fl=left[1] if left else 0,
-                              xr=right[0][k % 2] if right else 0, fr=right[1] if right else 0,
-                              epoch=self.epoch, err=self.err)
-            self._publish()
-        return self.views[len(passes) % 2]
+        # every pass in one C call (ppa_grid2_slab_chain): pass k reads role
+        # k % 2, waits for epoch + k and its last CTA publishes epoch + k + 1
+        role = C.grid2_slab_chain(self.nd, self.nx, self.ny, self.nz, self.vals, self.z0, self.z1,
+                                  passes, self.bufs[0], self.bufs[1],
+                                  xl=tuple(left[0]) if left else (0, 0),
+                                  zl0=left[2] if left else 0, fl=left[1] if left else 0,
+                                  xr=tuple(right[0]) if right else (0, 0),
+                                  fr=right[1] if right else 0, epoch0=self.epoch, err=self.err,
+                                  own=self.flag)
+        self.epoch += len(passes)
+        return self.views[role]
 
     def check(self) -> None:
         """Raises if a neighbour's flag never arrived during a pass."""

@@ -72,10 +72,11 @@ def _virtual_slabs(cuda, nx, ny, nz, vals, world, roots, v):
                               fl=fl[left] if left is not None else 0,
                               xr=bufs[right][k % 2].data_ptr() if right is not None else 0,
                               fr=fl[right] if right is not None else 0,
-                              epoch=1 + k, err=err.data_ptr())
-        for q in range(world):
-            C.halo_publish(fl[q], 2 + k)
+                              epoch=1 + k, err=err.data_ptr(), own=fl[q])
     assert int(err[0].item()) == 0
+    # every pass published its epoch from inside (flag word 0; word 1 counts
+    # the publishing CTAs); a lone slab has no neighbours to publish to
+    assert flags[:, 0].tolist() == [1 + len(passes) if world > 1 else 1] * world
     return torch.cat([bufs[q][len(passes) % 2] for q in range(world)]).cpu().numpy()
 
 
