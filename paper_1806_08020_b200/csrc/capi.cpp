@@ -875,6 +875,7 @@ int ppa_grid2_slab_pass(int nd, int nx, int ny, int nz, const double* vals, int 
     need(y, "ppa_grid2_slab_pass");
     if (x == y) throw std::invalid_argument("ppa_grid2_slab_pass: x and y must differ");
     if (kind < 0 || kind > 2) throw std::invalid_argument("ppa_grid2_slab_pass: kind must be 0, 1 or 2");
+    ppa::kern::spmv_grid2_slab_check(nd, nx, ny, nz, zo0, zo1, xl, zl0, fl, xr, fr);
     ppa::kern::Mp2Pass m;
     m.pair = kind == 1;
     m.one = kind == 2;
@@ -907,11 +908,14 @@ int ppa_grid2_slab_chain(int nd, int nx, int ny, int nz, const double* vals, int
     double* buf[2] = {buf0, buf1};
     const double* xl[2] = {xl0, xl1};
     const double* xr[2] = {xr0, xr1};
-    const cudaStream_t st = ppa::current_context().stream();
     for (int k = 0; k < npass; ++k) {
       if (kinds[k] < 0 || kinds[k] > 2) {
         throw std::invalid_argument("ppa_grid2_slab_chain: kind must be 0, 1 or 2");
       }
+    }
+    ppa::kern::spmv_grid2_slab_check(nd, nx, ny, nz, zo0, zo1, xl0, zl0, fl, xr0, fr);
+    const cudaStream_t st = ppa::current_context().stream();
+    for (int k = 0; k < npass; ++k) {
       ppa::kern::Mp2Pass m;
       m.pair = kinds[k] == 1;
       m.one = kinds[k] == 2;

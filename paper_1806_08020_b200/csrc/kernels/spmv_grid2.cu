@@ -929,10 +929,9 @@ void spmv_grid2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y
                a.grid_nz, nullptr, 0, nullptr, nullptr, nullptr, 0, nullptr, nullptr, st);
 }
 
-void spmv_grid2_slab(int nd, int nx, int ny, int nz, const double* vals, int zo0, int zo1,
-                     const Mp2Pass& p, const double* x, double* y, const double* xl, int zl0,
-                     const long long* fl, const double* xr, const long long* fr,
-                     long long epoch, int* err, long long* own, cudaStream_t st) {
+void spmv_grid2_slab_check(int nd, int nx, int ny, int nz, int zo0, int zo1, const double* xl,
+                           int zl0, const long long* fl, const double* xr,
+                           const long long* fr) {
   if (nd != 5 && nd != 7) throw std::invalid_argument("spmv_grid2_slab: 5- or 7-point stencil");
   if ((nd == 5) != (ny == 1)) throw std::invalid_argument("spmv_grid2_slab: 2-D boxes have ny = 1");
   if (zo0 < 0 || zo1 > nz || zo1 - zo0 < 2) {
@@ -941,9 +940,17 @@ void spmv_grid2_slab(int nd, int nx, int ny, int nz, const double* vals, int zo0
   if ((zo0 > 0 && (!xl || !fl || zo0 - zl0 < 2)) || (zo1 < nz && (!xr || !fr))) {
     throw std::invalid_argument("spmv_grid2_slab: missing neighbour buffer or flag");
   }
+  if (nx < 2 || ny < 1) throw std::invalid_argument("spmv_grid2_slab: bad box");
   if (static_cast<long long>(nx) * ny * (zo1 - zo0) + 4LL * nx * ny >= (1LL << 31)) {
     throw std::invalid_argument("spmv_grid2_slab: slab too large");
   }
+}
+
+void spmv_grid2_slab(int nd, int nx, int ny, int nz, const double* vals, int zo0, int zo1,
+                     const Mp2Pass& p, const double* x, double* y, const double* xl, int zl0,
+                     const long long* fl, const double* xr, const long long* fr,
+                     long long epoch, int* err, long long* own, cudaStream_t st) {
+  spmv_grid2_slab_check(nd, nx, ny, nz, zo0, zo1, xl, zl0, fl, xr, fr);
   grid2_launch(nd, nx, ny, nz, vals, p, x, y, nullptr, zo0, zo1, xl, zl0, fl, xr, fr, epoch,
                err, own, st);
 }

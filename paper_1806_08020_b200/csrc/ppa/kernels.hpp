@@ -135,6 +135,9 @@ void spmv_grid2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y
 /// x and y hold the owned planes only.  *err is set if a flag never arrives.
 /// own (this rank's flag, 2 words: flag, ticket counter) non-null: the
 /// pass's last CTA publishes epoch + 1 into it (system-scope release).
+/// Argument checks of spmv_grid2_slab (std::invalid_argument), no device work.
+void spmv_grid2_slab_check(int nd, int nx, int ny, int nz, int zo0, int zo1, const double* xl,
+                           int zl0, const long long* fl, const double* xr, const long long* fr);
 void spmv_grid2_slab(int nd, int nx, int ny, int nz, const double* vals, int zo0, int zo1,
                      const Mp2Pass& p, const double* x, double* y, const double* xl, int zl0,
                      const long long* fl, const double* xr, const long long* fr,

@@ -178,3 +178,27 @@ def test_bench_launch_count_model():
     assert bench.count_launches(roots, True) == 6
     assert bench.count_launches([], True) == 0
     assert bench.count_launches([1.0] * 51, True) == 26
+
+
+def test_grid2_slab_argument_checks():
+    """The sharded box-grid entry points reject bad arguments with the
+    reference's invalid_argument convention before any device work."""
+    from paper_1806_08020_b200 import _capi as C
+
+    vals7 = [-1.0, -1.0, -1.0, 6.0, -1.0, -1.0, -1.0]
+    fake = 1 << 20  # never dereferenced: every case fails validation first
+    cases = [
+        dict(nd=7, ny=8, zo0=0, zo1=8, kind=3),            # kind out of range
+        dict(nd=7, ny=8, zo0=3, zo1=4, kind=0),            # a slab of one plane
+        dict(nd=7, ny=8, zo0=2, zo1=8, kind=0),            # left neighbour missing
+        dict(nd=5, ny=8, zo0=0, zo1=8, kind=0),            # 2-D stencil needs ny = 1
+    ]
+    for c in cases:
+        vals = vals7 if c["nd"] == 7 else vals7[:5]
+        with pytest.raises(ValueError):
+            C.grid2_slab_pass(c["nd"], 8, c["ny"], 8, vals, c["zo0"], c["zo1"], c["kind"], 1.0,
+                              0.0, 1.0, fake, fake + 4096)
+    with pytest.raises(ValueError):
+        C.grid2_slab_pass(7, 8, 8, 8, vals7, 0, 8, 0, 1.0, 0.0, 1.0, fake, fake)  # x == y
+    with pytest.raises(ValueError):
+        C.grid2_slab_chain(7, 8, 8, 8, vals7, 0, 8, [(5, 1.0, 0.0, 0.0)], fake, fake + 4096)
