@@ -433,6 +433,22 @@ def run_b200(args):
                      "bytes_note": note},
         "bit_identical_to_sell32": auto_match,
     }
+    rows = lay.get("grid_rows_per_pass")
+    if two and rows and not any(abs(z.imag) > 1e-13 * abs(z) for z in roots):
+        # the box-grid pass's FP64 view: every row evaluation is nd mul + nd
+        # add (the sum starts at +0.0) plus the real-root epilogue's mul + add,
+        # no FMA (bit-exact mul-then-add order); peak = the measured non-FMA
+        # DADD/DMUL rate (tools/micro/fp64_rate.cu: 61.7 lane-ops per clock per
+        # SM at 1965 MHz on this pool's B200)
+        nd = 7 if lay["grid"][1] > 1 else 5
+        flop = float(rows[0] + rows[1]) * (2 * nd + 2)
+        fp64_peak = 61.7 * 148 * 1.965e9 / 1e12
+        ach = flop / auto_launch_s / 1e12
+        default_layout["fp64"] = {
+            "bound": "fp64 pipe (no FMA)", "achieved": round(ach, 3), "peak": round(fp64_peak, 2),
+            "unit": "TFLOP/s", "frac": round(ach / fp64_peak, 4),
+            "flop_per_launch": flop, "row_evaluations_per_launch": list(rows),
+            "peak_kind": "measured, tools/micro/fp64_rate.cu"}
 
     # CGS2 step at basis size c = 40 (config 3's m) on a real Arnoldi basis of
     # A: w = A v_39 orthogonalised against V[:,0:40] (3 sweeps, V[:,40] written).

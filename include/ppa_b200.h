@@ -148,6 +148,10 @@ int ppa_csr_two_factor_pass(const ppa_op* op, int* supported);
    nx, ny, nz of the 7-point (3-D) or 5-point (2-D, ny = 1) stencil the matrix
    is, or nx = 0; *supported = 1 when that form runs.  Introspection only. */
 int ppa_csr_grid_form(const ppa_op* op, int* nx, int* ny, int* nz, int* supported);
+/* Row evaluations one box-grid pass performs (the bench's FP64 roofline):
+   level 1 over the widened tiles and the chunks' extra planes, level 2 over
+   the n rows; both 0 when the form does not run.  Introspection only. */
+int ppa_csr_grid_work(const ppa_op* op, long long* l1_rows, long long* l2_rows);
 
 /* ---- polynomial -------------------------------------------------------- */
 /* apply_poly (src/gmres_poly.cpp:117-147): out_dev = pi(A) v_dev */

@@ -123,6 +123,7 @@ def lib():
             "ppa_host_csr_multiply": [vp, vp, vp],
             "ppa_csr_operator_layout": [vp, C.c_int, C.POINTER(vp)],
             "ppa_csr_two_factor_pass": [vp, _ip],
+            "ppa_csr_grid_work": [vp, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)],
             "ppa_csr_grid_form": [vp, _ip, _ip, _ip, _ip],
             "ppa_arnoldi_set_orthogonalization": [vp, C.c_int],
             "ppa_apply_poly": [vp, vp, C.c_int, vp, vp, vp, C.POINTER(CostRecord)],
@@ -413,11 +414,14 @@ class LinearOperator:
         gx, gy, gz, g2 = C.c_int(), C.c_int(), C.c_int(), C.c_int()
         _check(lib().ppa_csr_grid_form(self._h, C.byref(gx), C.byref(gy), C.byref(gz),
                                        C.byref(g2)))
+        l1, l2 = C.c_longlong(), C.c_longlong()
+        _check(lib().ppa_csr_grid_work(self._h, C.byref(l1), C.byref(l2)))
         return {"layout": ("csr", "sell32", "sell32_packed", "dia_coded")[lay.value],
                 "stream_bytes": sb.value, "sigma": sig.value, "dict_size": nd.value,
                 "two_factor_pass": bool(two.value),
                 "grid": (gx.value, gy.value, gz.value) if gx.value else None,
-                "grid_pass": bool(g2.value)}
+                "grid_pass": bool(g2.value),
+                "grid_rows_per_pass": (l1.value, l2.value) if g2.value else None}
 
 
 LAYOUTS = {"auto": 0, "csr": 1, "sell32": 2, "sell32_packed": 3, "dia_coded": 4}

@@ -475,6 +475,17 @@ int ppa_csr_grid_form(const ppa_op* op, int* nx, int* ny, int* nz, int* supporte
   });
 }
 
+int ppa_csr_grid_work(const ppa_op* op, long long* l1_rows, long long* l2_rows) {
+  return guard([&] {
+    need(op, "ppa_csr_grid_work");
+    need(l1_rows, "ppa_csr_grid_work");
+    need(l2_rows, "ppa_csr_grid_work");
+    const auto* c = dynamic_cast<const ppa::CsrOperator*>(op->p.get());
+    if (!c) throw std::invalid_argument("ppa_csr_grid_work: not a CSR operator");
+    ppa::kern::grid2_row_evals(c->device(), l1_rows, l2_rows);
+  });
+}
+
 int ppa_apply_poly(const double* re, const double* im, int nroots, const ppa_op* a,
                    const double* v, double* out, ppa_cost* cost) {
   return guard([&] {

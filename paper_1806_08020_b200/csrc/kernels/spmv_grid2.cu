@@ -923,6 +923,37 @@ void grid2_launch(int nd, int nx, int ny, int nz, const double* vals, const Mp2P
 
 }  // namespace
 
+void grid2_row_evals(const CsrDevice& a, long long* l1, long long* l2) {
+  *l1 = *l2 = 0;
+  if (!grid2_supported(a)) return;
+  const int nd = a.dia_ndiag, nx = a.grid_nx, ny = a.grid_ny, nz = a.grid_nz;
+  const G2Plan pl = g2_plan(nd, nx, ny, nz);
+  // the kernel's tiles and chunks (k_spmv_grid2): level 1 runs on the tile
+  // widened by one line (3-D) or column (2-D) each side and on one more
+  // plane each side of the chunk, clipped to the box; level 2 on every row
+  long long cells = 0;  // level-1 cells per plane, summed over tiles
+  if (nd == 7) {
+    for (int ty = 0; ty < pl.nty; ++ty) {
+      const int y0 = ty * ny / pl.nty, y1 = (ty + 1) * ny / pl.nty;
+      cells += static_cast<long long>(std::min(y1 + 1, ny) - std::max(y0 - 1, 0)) * nx;
+    }
+  } else {
+    for (int tx = 0; tx < pl.ntx; ++tx) {
+      const int x0 = (tx * nx / pl.ntx) & ~1;
+      const int x1 = tx + 1 == pl.ntx ? nx : ((tx + 1) * nx / pl.ntx) & ~1;
+      cells += std::min(x1 + 1, nx) - std::max(x0 - 1, 0);
+    }
+  }
+  long long planes = 0;
+  for (int c = 0; c < pl.nchunks; ++c) {
+    const int za = static_cast<int>(static_cast<long long>(c) * nz / pl.nchunks);
+    const int zb = static_cast<int>(static_cast<long long>(c + 1) * nz / pl.nchunks);
+    planes += std::min(zb + 1, nz) - std::max(za - 1, 0);
+  }
+  *l1 = cells * planes;
+  *l2 = static_cast<long long>(nx) * ny * nz;
+}
+
 void spmv_grid2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y,
                 const double* base, cudaStream_t st) {
   grid2_launch(a.dia_ndiag, a.grid_nx, a.grid_ny, a.grid_nz, a.dia_dflt, p, x, y, base, 0,

@@ -124,6 +124,9 @@ bool grid2_supported(const CsrDevice& a);
 /// box (allocated on first use; layout_build.cu touches it so that a capture
 /// never allocates).
 const double* grid2_zeros();
+/// Row evaluations of one box-grid pass: level 1 (the widened tiles and
+/// the chunks' extra planes) and level 2 (= n); 0 when the form does not run.
+void grid2_row_evals(const CsrDevice& a, long long* l1, long long* l2);
 /// The box-grid two-factor pass (same contract as spmv_dia2).
 void spmv_grid2(const CsrDevice& a, const Mp2Pass& p, const double* x, double* y,
                 const double* base, cudaStream_t st);
