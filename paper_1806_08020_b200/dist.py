@@ -529,9 +529,15 @@ class ShardedGridPoly:
             raise RuntimeError("ShardedGridPoly: a neighbour's epoch flag never arrived")
 
     def close(self) -> None:
+        """Unmap the neighbours' buffers and free this rank's (collective: the
+        neighbours must be done with them)."""
         for p in self.opened:
             self.C.ipc_close(p)
         self.opened = []
+        self.torch.cuda.synchronize()
+        for p in self.bufs + [self.flag, self.err]:
+            self.C.dev_free(p)
+        self.bufs, self.views = [], []
 
 
 # ------------------------------------------------------------ sharded solve --
