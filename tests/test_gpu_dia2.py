@@ -288,6 +288,11 @@ def test_grid2_configs_detected(cuda):
     for k, g in ((2, (1000, 1, 1000)), (3, (160, 160, 160)), (5, (2048, 1, 2048))):
         lay = ppa.make_csr_operator(ppa.CsrMatrix.config(k)).layout()
         assert lay["grid"] == g and lay["grid_pass"], (k, lay)
+        # the pass's row evaluations (ppa_csr_grid_work, the bench's FP64
+        # roofline): level 2 once per row, level 1 on the tiles plus halo
+        l1, l2 = lay["grid_rows_per_pass"]
+        n = g[0] * g[1] * g[2]
+        assert l2 == n and n <= l1 < 1.6 * n, (k, l1, l2)
     assert ppa.make_csr_operator(ppa.CsrMatrix.convection_diffusion(64)).layout()["grid"] is None
 
 
