@@ -925,6 +925,9 @@ int ppa_grid2_slab_chain(int nd, int nx, int ny, int nz, const double* vals, int
       }
     }
     ppa::kern::spmv_grid2_slab_check(nd, nx, ny, nz, zo0, zo1, xl0, zl0, fl, xr0, fr);
+    if ((zo0 > 0 && !xl1) || (zo1 < nz && !xr1)) {
+      throw std::invalid_argument("ppa_grid2_slab_chain: missing neighbour buffer (role 1)");
+    }
     const cudaStream_t st = ppa::current_context().stream();
     for (int k = 0; k < npass; ++k) {
       ppa::kern::Mp2Pass m;

@@ -202,3 +202,6 @@ def test_grid2_slab_argument_checks():
         C.grid2_slab_pass(7, 8, 8, 8, vals7, 0, 8, 0, 1.0, 0.0, 1.0, fake, fake)  # x == y
     with pytest.raises(ValueError):
         C.grid2_slab_chain(7, 8, 8, 8, vals7, 0, 8, [(5, 1.0, 0.0, 0.0)], fake, fake + 4096)
+    with pytest.raises(ValueError):  # a right neighbour without its role-1 buffer
+        C.grid2_slab_chain(7, 8, 8, 8, vals7, 0, 4, [(0, 1.0, 0.0, 1.0)], fake, fake + 4096,
+                           xr=(fake + 8192, 0), fr=fake + 16384)
