@@ -254,6 +254,15 @@ def run_reference(args):
             r = O.solve(Ak, p["m"], p["k"], p["nev"], seed=p["seed"], **extra)
             configs_info[f"config{k}"] = {"seconds": round(r["wall"], 4), "converged": r["converged"],
                                           "cycles": r["cycles"], "mvps": r["cost"]["mvps"]}
+    # one orthogonalisation step of arnoldi_extend at the GPU arm's basis size
+    # (MGS + MGS reorthogonalisation, src/arnoldi.cpp:129-150), all host threads
+    c_cgs = 40
+    t_cgs = O.time_mgs2_step(n, c_cgs, 3)
+    cgs_info = {"c": c_cgs, "ms": round(t_cgs * 1e3, 3),
+                "gbs_model": round(8.0 * n * (3 * c_cgs + 7) / t_cgs / 1e9, 3),
+                "bytes_model": "8n(3c+7)", "reps": 3, "threads": threads,
+                "what": "MGS + MGS reorthogonalisation + norm + scaled store of "
+                        "arnoldi_extend (src/arnoldi.cpp:129-150), oracle restatement"}
     cpu = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
            "sample": f"{nf} of {len(roots)} polynomial factors (SpMV+axpy) per step, "
                      "oracle restatement of src/gmres_poly.cpp:117-147, OpenMP rows",
@@ -267,6 +276,7 @@ def run_reference(args):
         "cpu_baseline": cpu,
         "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "cgs2": cgs_info,
         "time_to_nev": solve_info,
         "time_to_nev_configs": configs_info,
     }
@@ -287,9 +297,15 @@ def cpu_baseline_port(roots):
     t1 = O.time_poly_factors(A, roots, 1, 1)
     nf = int(max(1, min(len(roots), 10.0 / max(t1, 1e-3))))
     t = O.time_poly_factors(A, roots, nf, 1)
+    # one orthogonalisation step at c = 40 (MGS2, src/arnoldi.cpp:129-150)
+    t_cgs = O.time_mgs2_step(n, 40, 1)
     return {"value": round(nf * bspmv / t / 1e9, 3), "unit": "GB/s", "cores": 1, "kind": "port",
             "sample": f"{nf} of {len(roots)} factors of pi(A)v on config 3 "
-                      f"({t:.1f} s, single thread, oracle -O3)", **cpu_info()}
+                      f"({t:.1f} s, single thread, oracle -O3)",
+            "cgs2_step_ms": round(t_cgs * 1e3, 2),
+            "cgs2_step_gbs_model": round(8.0 * n * (3 * 40 + 7) / t_cgs / 1e9, 3),
+            "cgs2_sample": "one MGS2 orthogonalisation step at c = 40 on config 3's n "
+                           "(single thread, oracle)", **cpu_info()}
 
 
 def run_b200(args):

@@ -91,6 +91,8 @@ def lib():
         L.orc_op_free.restype = None
         L.orc_time_poly_factors.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.c_int]
         L.orc_time_poly_factors.restype = C.c_double
+        L.orc_time_mgs2_step.argtypes = [C.c_long, C.c_int, C.c_int]
+        L.orc_time_mgs2_step.restype = C.c_double
         _L = L
     return _L
 
@@ -416,3 +418,9 @@ def solve(a: Op, m, k, nev, degree=0, rtol_multiplier=1e-8, rtol_absolute=0.0, s
 def time_poly_factors(a: Op, roots, nfactors, reps=1) -> float:
     re, im = _ri(roots)
     return float(lib().orc_time_poly_factors(a.h, _p(re), _p(im), len(re), nfactors, reps))
+
+
+def time_mgs2_step(n: int, c: int, reps: int = 1) -> float:
+    """Seconds per orthogonalisation step of arnoldi_extend at basis size c
+    (src/arnoldi.cpp:129-150 without the operator application)."""
+    return float(lib().orc_time_mgs2_step(n, c, reps))

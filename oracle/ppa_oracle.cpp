@@ -1960,4 +1960,39 @@ double orc_time_poly_factors(const orc_op* a, const double* re, const double* im
   return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
+// Seconds per orthogonalisation step of arnoldi_extend at basis size c (the
+// MGS + MGS reorthogonalisation loops, the norm and the scaled store of
+// src/arnoldi.cpp:129-150, without the operator application), mean of reps.
+// The timing does not depend on the values: the basis is c scaled Gaussian
+// columns.  For bench.py's CPU arm only.
+double orc_time_mgs2_step(long n, int c, int reps) {
+  orc::Vec V(static_cast<size_t>(n) * (c + 1));
+  for (int j = 0; j < c; ++j) {
+    const orc::Vec g = orc::rng::gauss_vec(n, 100 + j, orc::rng::ARNOLDI);
+    const double s = 1.0 / std::sqrt(static_cast<double>(n));
+    for (long i = 0; i < n; ++i) V[static_cast<size_t>(j) * n + i] = g[i] * s;
+  }
+  const orc::Vec w0 = orc::rng::gauss_vec(n, 7, orc::rng::ARNOLDI);
+  orc::Vec w(n);
+  std::vector<double> h(static_cast<size_t>(c) + 1);
+  orc::Cost cost;
+  double total = 0.0;
+  for (int r = 0; r < reps; ++r) {
+    w = w0;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int i = 0; i < c; ++i) {
+        const double hi = orc::dot(V.data() + static_cast<size_t>(i) * n, w.data(), n, cost);
+        h[i] = pass == 0 ? hi : h[i] + hi;
+        orc::axpy(-hi, V.data() + static_cast<size_t>(i) * n, w.data(), n, cost);
+      }
+    }
+    const double hsub = orc::norm(w.data(), n, cost);
+    double* dst = V.data() + static_cast<size_t>(c) * n;
+    for (long i = 0; i < n; ++i) dst[i] = w[i] / hsub;
+    total += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+  return total / std::max(1, reps);
+}
+
 }  // extern "C"
