@@ -1,0 +1,5 @@
+// Box-grid two-factor pass: the 7-point kernels with 3 cells per thread
+// (every block size, root kind, complement, single-factor and slab form).
+#include "spmv_grid2_kernel.cuh"
+
+PPA_G2_DEFINE(7, 3)
