@@ -418,8 +418,9 @@ def run_b200(args):
         kbytes = 16.0 * n
         kname = ("k_spmv_grid2 (two factors per pass over the box-grid stencil: x planes by "
                  "cp.async.bulk into a shared-memory ring, per-warp mbarrier split barriers)")
-        note = ("8n x + 8n y per two-factor launch; bound by the FP64 pipe and issue "
-                "(16 DP ops per row per factor, bit-exact mul-then-add order), not by HBM")
+        note = ("8n x + 8n y per two-factor launch; bound on the SM side (16 DP ops per row per "
+                "factor in the bit-exact mul-then-add order, issue, per-step lockstep of the "
+                "warps; DESIGN.md 3.1c), not by HBM")
     elif two:
         # two factors per launch: x read once (8n), the second factor's y
         # written once (8n), one presence byte per row (n)
