@@ -357,3 +357,14 @@ def test_oracle_harmonic_variant_solve():
     assert np.allclose(np.sort(r["eigenvalues"].real), np.arange(1.0, 11.0), rtol=1e-8)
     assert r["cycles"] != p["cycles"] or r["cost"]["mvps"] != p["cost"]["mvps"] or \
         not np.array_equal(r["eigenvalues"], p["eigenvalues"])
+
+
+def test_bench_timers_run():
+    # the two timers bench.py's CPU arms call (orc_time_poly_factors,
+    # orc_time_mgs2_step): small sizes, finite positive seconds
+    A = O.csr_operator(O.Csr.laplacian_3d(10))
+    roots = O.leja_order([40.0, 30.0 + 5.0j, 30.0 - 5.0j, 12.0])
+    t = O.time_poly_factors(A, roots, 3, 1)
+    assert 0.0 < t < 10.0
+    t = O.time_mgs2_step(20000, 6, 2)
+    assert 0.0 < t < 10.0
